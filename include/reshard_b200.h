@@ -1,0 +1,178 @@
+/*
+ * reshard_b200.h — C ABI of the B200-native resharding path (libreshard_b200.so).
+ *
+ * Drop-in boundary for the reference's planner + transition engine. The reference
+ * exposes a header-only C++ API in namespace reshard (/root/reference/proj/include/
+ * reshard); every entry point below names the reference interface it replaces.
+ * The same C++ API is also shipped, re-implemented, under
+ * paper_2605_18815_b200/csrc/reshard/ for C++ callers.
+ *
+ * Conventions: plain pointers and sizes only; every function returns an int status
+ * (RS_OK = 0) and never throws; rs_last_error() gives the thread-local message of
+ * the last failure. Objects are created and destroyed by the library; the caller
+ * owns device buffers it binds with rs_exec_bind(). Planner calls are reentrant
+ * (SPEC.md:252-253); an rs_exec_t is driven by one host thread.
+ */
+#ifndef RESHARD_B200_H
+#define RESHARD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SPEC.md:523 exit codes 0/1/2 map to OK / VIOLATION / CONFIG) */
+#define RS_OK 0
+#define RS_ERR_VIOLATION 1 /* verification found mismatching elements */
+#define RS_ERR_CONFIG 2    /* reference ConfigError (common.hpp:30-33): bad input */
+#define RS_ERR_INTERNAL 3  /* reference std::logic_error: broken invariant */
+#define RS_ERR_CUDA 4      /* CUDA runtime / driver failure (incl. no GPU) */
+#define RS_ERR_NCCL 5
+#define RS_ERR_BUDGET 6    /* memory-aware schedule infeasible under the HBM cap */
+
+/* ---- state kinds (common.hpp:37 StateKind order) and buffers */
+#define RS_KIND_PARAM 0
+#define RS_KIND_OPTIM 1
+#define RS_KIND_GRAD 2
+#define RS_KIND_SCALAR 3
+
+#define RS_BUF_PARAM 0   /* params, dtype_bytes per element, local_layout order */
+#define RS_BUF_MASTER 1  /* fp32 master weights (optimizer shard) */
+#define RS_BUF_M 2       /* fp32 Adam m */
+#define RS_BUF_V 3       /* fp32 Adam v */
+#define RS_BUF_GRAD 4    /* fp32 grads, param geometry (GradientPolicy::Migrate only) */
+#define RS_BUF_SCALARS 5 /* scalar_words x u64 */
+
+#define RS_SIDE_SRC 0
+#define RS_SIDE_DST 1
+
+typedef struct rs_model rs_model_t;
+typedef struct rs_plan rs_plan_t;
+typedef struct rs_exec rs_exec_t;
+
+/* TensorSpec (model.hpp:30-44). tp_axis / expert_axis: -1 = none. */
+typedef struct {
+    const char* id;
+    int ndim; /* 1..4 */
+    int64_t shape[4];
+    int layer;
+    int tp_axis;
+    int expert_axis;
+    int dtype_bytes;
+} rs_tensor_t;
+
+/* ParallelConfig (parallel.hpp:28-46). order NULL -> "pp-dp-tp". */
+typedef struct {
+    int dp, tp, pp, ep;
+    int zero;
+    const char* order;
+} rs_cfg_t;
+
+/* WorldMap (worldmap.hpp:30-39). */
+typedef struct {
+    int n_src;
+    const int* src_phys;
+    int n_dst;
+    const int* dst_phys;
+} rs_worldmap_t;
+
+/* Topology (topology.hpp:25-31); only the node grouping feeds the planner. */
+typedef struct {
+    int num_nodes;
+    int ranks_per_node;
+} rs_topo_t;
+
+/* PlanOptions (routing.hpp:40-44) + the D2 extension switch. */
+typedef struct {
+    int migrate_grads;     /* GradientPolicy::Migrate */
+    int balance_fanout;
+    int64_t scalar_words;
+    int allow_oversourced; /* extension: resolve over-sourced ZeRO intervals (reference throws) */
+} rs_options_t;
+
+/* SliceTransfer (routing.hpp:50-77) as POD. flat=1: [lo[0],hi[0]) global flat run. */
+typedef struct {
+    int kind, tensor, flat, ndim;
+    int64_t lo[4], hi[4];
+    int src_rank, dst_rank, src_phys, dst_phys;
+    int64_t count, bytes;
+} rs_transfer_t;
+
+typedef struct {
+    int64_t num_transfers;   /* RoutingPlan::transfers.size() */
+    int64_t bytes_moved;     /* RoutingPlan::bytes_moved() routing.hpp:151-156 */
+    int64_t bytes_retained;  /* RoutingPlan::bytes_retained() routing.hpp:157-169 */
+    int64_t num_box_transfers, num_flat_transfers, num_triples;
+    int src_world, dst_world, num_participants;
+    int64_t total_numel;
+    uint64_t fingerprint;    /* ModelSpace::fingerprint() */
+} rs_plan_summary_t;
+
+const char* rs_last_error(void);
+const char* rs_version(void);
+void rs_free(void* p);
+
+/* build_model_space (model.hpp:127-144), validate_model (model.hpp:95-123) */
+int rs_model_create(const rs_tensor_t* tensors, int n, int num_layers, int num_experts, rs_model_t** out);
+void rs_model_destroy(rs_model_t* m);
+
+/* plan_parameters + plan_optimizer + plan_scalars + resolve_peers
+ * (routing.hpp:231, :287, :341, :360), with validate_config x2 first.
+ * wm / topo / opts may be NULL (identity map, 1 node x 8, defaults). The plan keeps a
+ * reference to the model: destroy the plan first. */
+int rs_plan_create(const rs_model_t* m, const rs_cfg_t* src, const rs_cfg_t* dst, const rs_worldmap_t* wm,
+                   const rs_topo_t* topo, const rs_options_t* opts, rs_plan_t** out);
+/* same, from scenario text; the plan owns its model */
+int rs_plan_from_scenario(const char* text, int allow_oversourced, rs_plan_t** out);
+void rs_plan_destroy(rs_plan_t* p);
+int rs_plan_summary(const rs_plan_t* p, rs_plan_summary_t* out);
+/* format_transfer lines (routing.hpp:86-90) in transfer_order_less order
+ * (routing.hpp:79-84). device < 0: host expansion; >= 0: GPU planner on that device. */
+int rs_plan_dump(const rs_plan_t* p, int device, char** out, size_t* len);
+/* resolved transfer list (reference SliceTransfers), same order as rs_plan_dump */
+int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64_t* n);
+/* project / local_layout / project_optimizer of every rank of one side
+ * (project.hpp:44, :94, :146), text lines */
+int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len);
+/* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
+int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
+
+/* ---- executor: Algorithm 1 ExecuteSwitch / SPEC execute
+ * (SPEC.md:375-383), push model over NVLink. One rs_exec_t per GPU/process. */
+typedef struct {
+    int n_gpus;            /* GPUs the plan's physical devices are placed on (contiguous blocks) */
+    int gpu;               /* this process's GPU index */
+    int device;            /* CUDA device ordinal */
+    int with_grads;        /* allocate/migrate grad buffers */
+    int64_t tile_bytes;    /* 0 -> default */
+    int ctas_per_sm;       /* 0 -> default */
+} rs_exec_opts_t;
+
+typedef struct {
+    int64_t local_bytes;   /* bytes copied within this GPU's HBM (incl. retained) */
+    int64_t remote_bytes;  /* bytes stored into peer GPUs over NVLink */
+    int64_t tiles;
+    int64_t tiles_by_class[5];
+} rs_exec_stats_t;
+
+int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
+void rs_exec_destroy(rs_exec_t* e);
+int rs_exec_alloc(rs_exec_t* e);
+int rs_exec_bind(rs_exec_t* e, int side, int rank, int buf, void* dptr, int64_t bytes);
+int rs_exec_buffer(rs_exec_t* e, int side, int rank, int buf, void** dptr, int64_t* bytes, int* gpu);
+int rs_exec_ipc_export(rs_exec_t* e, void* out, size_t cap, size_t* len);
+int rs_exec_ipc_import(rs_exec_t* e, const void* blob, size_t len);
+int rs_exec_prepare(rs_exec_t* e);
+/* load_state on this GPU's ranks of one side */
+int rs_exec_fill(rs_exec_t* e, int side, uint64_t seed, void* stream);
+int rs_exec_run(rs_exec_t* e, void* stream, int* launches);
+/* verify_state on this GPU's ranks of one side */
+int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t* mismatches, int64_t* first_bad);
+int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,149 @@
+"""ctypes binding of include/reshard_b200.h (libreshard_b200.so, built in-tree).
+
+The library is the product: no Python or CPU fallback exists for the executor.
+If the shared library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libreshard_b200.so")
+
+RS_OK, RS_ERR_VIOLATION, RS_ERR_CONFIG, RS_ERR_INTERNAL, RS_ERR_CUDA, RS_ERR_NCCL, RS_ERR_BUDGET = range(7)
+BUF_PARAM, BUF_MASTER, BUF_M, BUF_V, BUF_GRAD, BUF_SCALARS = range(6)
+SIDE_SRC, SIDE_DST = 0, 1
+
+EXPORTED = [
+    "rs_last_error", "rs_version", "rs_free", "rs_model_create", "rs_model_destroy", "rs_plan_create",
+    "rs_plan_from_scenario", "rs_plan_destroy", "rs_plan_summary", "rs_plan_dump", "rs_plan_transfers",
+    "rs_plan_regions", "rs_plan_dump_rows_host", "rs_exec_create", "rs_exec_destroy", "rs_exec_alloc",
+    "rs_exec_bind", "rs_exec_buffer", "rs_exec_ipc_export", "rs_exec_ipc_import", "rs_exec_prepare",
+    "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats",
+]
+
+
+class Tensor_t(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("ndim", C.c_int), ("shape", C.c_int64 * 4), ("layer", C.c_int),
+                ("tp_axis", C.c_int), ("expert_axis", C.c_int), ("dtype_bytes", C.c_int)]
+
+
+class Cfg_t(C.Structure):
+    _fields_ = [("dp", C.c_int), ("tp", C.c_int), ("pp", C.c_int), ("ep", C.c_int), ("zero", C.c_int),
+                ("order", C.c_char_p)]
+
+
+class WorldMap_t(C.Structure):
+    _fields_ = [("n_src", C.c_int), ("src_phys", C.POINTER(C.c_int)), ("n_dst", C.c_int),
+                ("dst_phys", C.POINTER(C.c_int))]
+
+
+class Topo_t(C.Structure):
+    _fields_ = [("num_nodes", C.c_int), ("ranks_per_node", C.c_int)]
+
+
+class Options_t(C.Structure):
+    _fields_ = [("migrate_grads", C.c_int), ("balance_fanout", C.c_int), ("scalar_words", C.c_int64),
+                ("allow_oversourced", C.c_int)]
+
+
+class Transfer_t(C.Structure):
+    _fields_ = [("kind", C.c_int), ("tensor", C.c_int), ("flat", C.c_int), ("ndim", C.c_int),
+                ("lo", C.c_int64 * 4), ("hi", C.c_int64 * 4), ("src_rank", C.c_int), ("dst_rank", C.c_int),
+                ("src_phys", C.c_int), ("dst_phys", C.c_int), ("count", C.c_int64), ("bytes", C.c_int64)]
+
+
+class PlanSummary_t(C.Structure):
+    _fields_ = [("num_transfers", C.c_int64), ("bytes_moved", C.c_int64), ("bytes_retained", C.c_int64),
+                ("num_box_transfers", C.c_int64), ("num_flat_transfers", C.c_int64), ("num_triples", C.c_int64),
+                ("src_world", C.c_int), ("dst_world", C.c_int), ("num_participants", C.c_int),
+                ("total_numel", C.c_int64), ("fingerprint", C.c_uint64)]
+
+
+class ExecOpts_t(C.Structure):
+    _fields_ = [("n_gpus", C.c_int), ("gpu", C.c_int), ("device", C.c_int), ("with_grads", C.c_int),
+                ("tile_bytes", C.c_int64), ("ctas_per_sm", C.c_int)]
+
+
+class ExecStats_t(C.Structure):
+    _fields_ = [("local_bytes", C.c_int64), ("remote_bytes", C.c_int64), ("tiles", C.c_int64),
+                ("tiles_by_class", C.c_int64 * 5)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2605_18815_b200.build` "
+                          "(the product has no fallback path)")
+    L = C.CDLL(LIB_PATH)
+    vp, cp, i64, sz = C.c_void_p, C.c_char_p, C.c_int64, C.c_size_t
+    P = C.POINTER
+    L.rs_last_error.restype = cp
+    L.rs_version.restype = cp
+    L.rs_free.argtypes = [vp]
+    L.rs_model_create.argtypes = [P(Tensor_t), C.c_int, C.c_int, C.c_int, P(vp)]
+    L.rs_model_destroy.argtypes = [vp]
+    L.rs_plan_create.argtypes = [vp, P(Cfg_t), P(Cfg_t), P(WorldMap_t), P(Topo_t), P(Options_t), P(vp)]
+    L.rs_plan_from_scenario.argtypes = [cp, C.c_int, P(vp)]
+    L.rs_plan_destroy.argtypes = [vp]
+    L.rs_plan_summary.argtypes = [vp, P(PlanSummary_t)]
+    L.rs_plan_dump.argtypes = [vp, C.c_int, P(vp), P(sz)]
+    L.rs_plan_dump_rows_host.argtypes = [vp, P(vp), P(sz)]
+    L.rs_plan_transfers.argtypes = [vp, C.c_int, P(vp), P(i64)]
+    L.rs_plan_regions.argtypes = [vp, C.c_int, P(vp), P(sz)]
+    L.rs_exec_create.argtypes = [vp, P(ExecOpts_t), P(vp)]
+    L.rs_exec_destroy.argtypes = [vp]
+    L.rs_exec_alloc.argtypes = [vp]
+    L.rs_exec_bind.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, i64]
+    L.rs_exec_buffer.argtypes = [vp, C.c_int, C.c_int, C.c_int, P(vp), P(i64), P(C.c_int)]
+    L.rs_exec_ipc_export.argtypes = [vp, vp, sz, P(sz)]
+    L.rs_exec_ipc_import.argtypes = [vp, vp, sz]
+    L.rs_exec_prepare.argtypes = [vp]
+    L.rs_exec_fill.argtypes = [vp, C.c_int, C.c_uint64, vp]
+    L.rs_exec_run.argtypes = [vp, vp, P(C.c_int)]
+    L.rs_exec_verify.argtypes = [vp, C.c_int, C.c_uint64, vp, P(i64), P(i64)]
+    L.rs_exec_stats.argtypes = [vp, P(ExecStats_t)]
+    for name in EXPORTED:
+        fn = getattr(L, name)
+        if fn.restype is None and name not in ("rs_free", "rs_model_destroy", "rs_plan_destroy", "rs_exec_destroy"):
+            fn.restype = C.c_int
+    _lib = L
+    return L
+
+
+class ReshardError(Exception):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class ConfigError(ReshardError):
+    """Mirror of reshard::ConfigError (common.hpp:30-33)."""
+
+
+class VerificationError(ReshardError):
+    pass
+
+
+class CudaError(ReshardError):
+    pass
+
+
+def check(rc: int) -> None:
+    if rc == RS_OK:
+        return
+    msg = lib().rs_last_error().decode()
+    cls = {RS_ERR_CONFIG: ConfigError, RS_ERR_VIOLATION: VerificationError, RS_ERR_CUDA: CudaError}.get(rc, ReshardError)
+    raise cls(rc, msg)
+
+
+def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
+    s = C.string_at(ptr.value, n.value).decode() if ptr.value else ""
+    lib().rs_free(ptr)
+    return s

@@ -1,0 +1,184 @@
+"""Python mirror of the reference's resharding interface, over the C ABI.
+
+Same names and argument meaning as namespace reshard (routing.hpp / project.hpp):
+a ModelSpec + two ParallelConfigs (+ WorldMap, Topology, PlanOptions) give a
+RoutingPlan with bytes_moved() / bytes_retained() / transfers / dump; errors raise
+ConfigError where the reference throws ConfigError. The Executor runs a plan on
+B200s (push over NVLink); it has no CPU path and raises CudaError without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+from . import _capi as A
+from ._capi import ConfigError, CudaError, ReshardError, VerificationError  # noqa: F401
+from .scenarios import Cfg, Model, Scenario
+
+
+def _cfg_t(c: Cfg, keep: list) -> A.Cfg_t:
+    order = c.order.encode()
+    keep.append(order)
+    return A.Cfg_t(c.dp, c.tp, c.pp, c.ep, int(c.zero), order)
+
+
+class RoutingPlan:
+    """plan_parameters + plan_optimizer + plan_scalars + resolve_peers (routing.hpp:231-396)."""
+
+    def __init__(self, handle: int, model: Optional["ModelSpace"] = None):
+        self.h = handle
+        self._model = model  # keeps the model alive (the plan references it)
+        s = A.PlanSummary_t()
+        A.check(A.lib().rs_plan_summary(self.h, C.byref(s)))
+        self.summary = s
+
+    @classmethod
+    def from_scenario(cls, sc, allow_oversourced: bool = False) -> "RoutingPlan":
+        text = sc.text() if isinstance(sc, Scenario) else sc
+        h = C.c_void_p()
+        A.check(A.lib().rs_plan_from_scenario(text.encode(), int(allow_oversourced), C.byref(h)))
+        return cls(h.value)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            A.lib().rs_plan_destroy(self.h)
+            self.h = None
+
+    def bytes_moved(self) -> int:
+        return self.summary.bytes_moved
+
+    def bytes_retained(self) -> int:
+        return self.summary.bytes_retained
+
+    def num_transfers(self) -> int:
+        return self.summary.num_transfers
+
+    def dump(self, device: int = -1) -> str:
+        """format_transfer lines in canonical order; device>=0 runs the GPU planner."""
+        p, n = C.c_void_p(), C.c_size_t()
+        A.check(A.lib().rs_plan_dump(self.h, device, C.byref(p), C.byref(n)))
+        return A.take_string(p, n)
+
+    def dump_rows_host(self) -> str:
+        p, n = C.c_void_p(), C.c_size_t()
+        A.check(A.lib().rs_plan_dump_rows_host(self.h, C.byref(p), C.byref(n)))
+        return A.take_string(p, n)
+
+    def regions(self, side: int) -> str:
+        p, n = C.c_void_p(), C.c_size_t()
+        A.check(A.lib().rs_plan_regions(self.h, side, C.byref(p), C.byref(n)))
+        return A.take_string(p, n)
+
+    def transfers(self, device: int = -1) -> List[A.Transfer_t]:
+        p, n = C.c_void_p(), C.c_int64()
+        A.check(A.lib().rs_plan_transfers(self.h, device, C.byref(p), C.byref(n)))
+        arr = C.cast(p, C.POINTER(A.Transfer_t))
+        out = [A.Transfer_t.from_buffer_copy(arr[i]) for i in range(n.value)]
+        A.lib().rs_free(p)
+        return out
+
+
+class ModelSpace:
+    """build_model_space (model.hpp:127-144)."""
+
+    def __init__(self, model: Model):
+        arr = (A.Tensor_t * max(1, len(model.tensors)))()
+        self._ids = []
+        for i, t in enumerate(model.tensors):
+            b = t.id.encode()
+            self._ids.append(b)
+            shape = (C.c_int64 * 4)(*(list(t.shape) + [0] * (4 - len(t.shape))))
+            arr[i] = A.Tensor_t(b, len(t.shape), shape, t.layer, -1 if t.tp is None else t.tp,
+                                -1 if t.expert is None else t.expert, t.dtype)
+        h = C.c_void_p()
+        A.check(A.lib().rs_model_create(arr, len(model.tensors), model.layers, model.experts, C.byref(h)))
+        self.h = h.value
+        self.model = model
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            A.lib().rs_model_destroy(self.h)
+            self.h = None
+
+
+def plan_transition(space: ModelSpace, src: Cfg, dst: Cfg, world_src: Optional[Sequence[int]] = None,
+                    world_dst: Optional[Sequence[int]] = None, nodes: int = 1, rpn: int = 8,
+                    migrate_grads: bool = False, balance_fanout: bool = False, scalar_words: int = 8,
+                    allow_oversourced: bool = False) -> RoutingPlan:
+    keep: list = []
+    s, d = _cfg_t(src, keep), _cfg_t(dst, keep)
+    wm = None
+    if world_src is not None or world_dst is not None:
+        ws = list(world_src if world_src is not None else range(src.world()))
+        wd = list(world_dst if world_dst is not None else range(dst.world()))
+        a, b = (C.c_int * max(1, len(ws)))(*ws), (C.c_int * max(1, len(wd)))(*wd)
+        keep += [a, b]
+        wm = A.WorldMap_t(len(ws), a, len(wd), b)
+    topo = A.Topo_t(nodes, rpn)
+    opts = A.Options_t(int(migrate_grads), int(balance_fanout), scalar_words, int(allow_oversourced))
+    h = C.c_void_p()
+    A.check(A.lib().rs_plan_create(space.h, C.byref(s), C.byref(d), C.byref(wm) if wm else None, C.byref(topo),
+                                   C.byref(opts), C.byref(h)))
+    return RoutingPlan(h.value, space)
+
+
+class Executor:
+    """Per-GPU executor (Algorithm 1 ExecuteSwitch; push model)."""
+
+    def __init__(self, plan: RoutingPlan, n_gpus: int = 1, gpu: int = 0, device: int = 0,
+                 with_grads: bool = False, tile_bytes: int = 0, ctas_per_sm: int = 0):
+        self.plan = plan
+        o = A.ExecOpts_t(n_gpus, gpu, device, int(with_grads), tile_bytes, ctas_per_sm)
+        h = C.c_void_p()
+        A.check(A.lib().rs_exec_create(plan.h, C.byref(o), C.byref(h)))
+        self.h = h.value
+        self.n_gpus, self.gpu, self.device = n_gpus, gpu, device
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            A.lib().rs_exec_destroy(self.h)
+            self.h = None
+
+    def alloc(self) -> None:
+        A.check(A.lib().rs_exec_alloc(self.h))
+
+    def bind(self, side: int, rank: int, buf: int, ptr: int, nbytes: int) -> None:
+        A.check(A.lib().rs_exec_bind(self.h, side, rank, buf, C.c_void_p(ptr), nbytes))
+
+    def buffer(self, side: int, rank: int, buf: int):
+        p, n, g = C.c_void_p(), C.c_int64(), C.c_int()
+        A.check(A.lib().rs_exec_buffer(self.h, side, rank, buf, C.byref(p), C.byref(n), C.byref(g)))
+        return p.value or 0, n.value, g.value
+
+    def ipc_export(self) -> bytes:
+        n = C.c_size_t()
+        A.check(A.lib().rs_exec_ipc_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(max(1, n.value))
+        A.check(A.lib().rs_exec_ipc_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def ipc_import(self, blob: bytes) -> None:
+        A.check(A.lib().rs_exec_ipc_import(self.h, blob, len(blob)))
+
+    def prepare(self) -> None:
+        A.check(A.lib().rs_exec_prepare(self.h))
+
+    def fill(self, side: int, seed: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_fill(self.h, side, seed, C.c_void_p(stream)))
+
+    def run(self, stream: int = 0) -> int:
+        n = C.c_int()
+        A.check(A.lib().rs_exec_run(self.h, C.c_void_p(stream), C.byref(n)))
+        return n.value
+
+    def verify(self, side: int, seed: int, stream: int = 0):
+        bad, first = C.c_int64(), C.c_int64()
+        rc = A.lib().rs_exec_verify(self.h, side, seed, C.c_void_p(stream), C.byref(bad), C.byref(first))
+        if rc not in (A.RS_OK, A.RS_ERR_VIOLATION):
+            A.check(rc)
+        return bad.value, first.value
+
+    def stats(self) -> A.ExecStats_t:
+        s = A.ExecStats_t()
+        A.check(A.lib().rs_exec_stats(self.h, C.byref(s)))
+        return s

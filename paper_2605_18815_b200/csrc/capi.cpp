@@ -1,0 +1,494 @@
+// C ABI (include/reshard_b200.h): thin, exception-free wrappers over the C++
+// planner (reshard::core) and the executor (reshard::exec).
+#include "reshard_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "reshard/executor_rt.hpp"
+#include "reshard/plan_core.hpp"
+
+namespace reshard {
+namespace gpuplan {
+std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device, double* kernel_ms);
+}
+}  // namespace reshard
+
+using namespace reshard;
+
+struct rs_model {
+    ModelSpec spec;
+    ModelSpace space;
+};
+
+struct rs_plan {
+    std::shared_ptr<rs_model> owned;  // set when created from scenario text
+    const rs_model* model = nullptr;
+    core::PlanCore core;
+};
+
+struct rs_exec {
+    const rs_plan* plan = nullptr;
+    std::unique_ptr<exec::Executor> ex;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const ConfigError& e) {
+        return fail(RS_ERR_CONFIG, e.what());
+    } catch (const exec::CudaError& e) {
+        return fail(RS_ERR_CUDA, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(RS_ERR_INTERNAL, "out of host memory");
+    } catch (const std::exception& e) {
+        return fail(RS_ERR_INTERNAL, e.what());
+    }
+}
+
+char* dup_string(const std::string& s, size_t* len) {
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    if (!p) throw std::bad_alloc();
+    std::memcpy(p, s.data(), s.size());
+    p[s.size()] = 0;
+    if (len) *len = s.size();
+    return p;
+}
+
+ParallelConfig to_cfg(const rs_cfg_t& c) {
+    ParallelConfig p;
+    p.dp = c.dp;
+    p.tp = c.tp;
+    p.pp = c.pp;
+    p.ep = c.ep;
+    p.zero_enabled = c.zero != 0;
+    if (c.order) p.rank_order = c.order;
+    return p;
+}
+
+std::vector<std::int64_t> parse_ints(const std::string& s) {
+    std::vector<std::int64_t> v;
+    std::stringstream ss(s);
+    std::string x;
+    while (std::getline(ss, x, ','))
+        if (!x.empty()) v.push_back(std::stoll(x));
+    return v;
+}
+
+struct Scenario {
+    ModelSpec model;
+    ParallelConfig src, dst;
+    bool has_world = false;
+    WorldMap wm;
+    Topology topo;
+    PlanOptions opts;
+};
+
+/// Scenario text: the reference's value structs, one per line.
+Scenario parse_scenario(const std::string& text) {
+    Scenario sc;
+    std::stringstream in(text);
+    std::string line;
+    int lineno = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        std::stringstream ls(line);
+        std::vector<std::string> tok;
+        for (std::string w; ls >> w;) tok.push_back(w);
+        if (tok.empty() || tok[0][0] == '#' || tok[0] == "version" || tok[0] == "seed") continue;
+        auto kv = [&](const std::string& t) {
+            const size_t eq = t.find('=');
+            if (eq == std::string::npos) throw ConfigError(strfmt("line %d: bad token '%s'", lineno, t.c_str()));
+            return std::make_pair(t.substr(0, eq), t.substr(eq + 1));
+        };
+        if (tok[0] == "model") {
+            for (size_t i = 1; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                if (k == "layers") sc.model.num_layers = std::stoi(v);
+                else if (k == "experts") sc.model.num_experts = std::stoi(v);
+                else throw ConfigError(strfmt("line %d: bad model key", lineno));
+            }
+        } else if (tok[0] == "tensor") {
+            if (tok.size() < 3) throw ConfigError(strfmt("line %d: tensor needs id and shape", lineno));
+            TensorSpec t;
+            t.tensor_id = tok[1];
+            t.shape = parse_ints(tok[2]);
+            for (size_t i = 3; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                if (k == "layer") t.layer = std::stoi(v);
+                else if (k == "tp") t.tp_shard_axis = std::stoi(v);
+                else if (k == "expert") t.expert_axis = std::stoi(v), t.is_expert = true;
+                else if (k == "dtype") t.dtype_bytes = std::stoi(v);
+                else throw ConfigError(strfmt("line %d: bad tensor key", lineno));
+            }
+            sc.model.tensors.push_back(std::move(t));
+        } else if (tok[0] == "src" || tok[0] == "dst") {
+            ParallelConfig& c = tok[0] == "src" ? sc.src : sc.dst;
+            for (size_t i = 1; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                if (k == "dp") c.dp = std::stoi(v);
+                else if (k == "tp") c.tp = std::stoi(v);
+                else if (k == "pp") c.pp = std::stoi(v);
+                else if (k == "ep") c.ep = std::stoi(v);
+                else if (k == "zero") c.zero_enabled = std::stoi(v) != 0;
+                else if (k == "order") c.rank_order = v;
+                else throw ConfigError(strfmt("line %d: bad config key", lineno));
+            }
+        } else if (tok[0] == "world") {
+            sc.has_world = true;
+            for (size_t i = 1; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                std::vector<std::int64_t> l = parse_ints(v);
+                std::vector<int> li(l.begin(), l.end());
+                if (k == "src") sc.wm.src_phys = li;
+                else if (k == "dst") sc.wm.dst_phys = li;
+                else throw ConfigError(strfmt("line %d: bad world key", lineno));
+            }
+        } else if (tok[0] == "topology") {
+            for (size_t i = 1; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                if (k == "nodes") sc.topo.num_nodes = std::stoi(v);
+                else if (k == "rpn") sc.topo.ranks_per_node = std::stoi(v);
+                else throw ConfigError(strfmt("line %d: bad topology key", lineno));
+            }
+        } else if (tok[0] == "options") {
+            for (size_t i = 1; i < tok.size(); ++i) {
+                auto [k, v] = kv(tok[i]);
+                if (k == "grads") sc.opts.gradients = v == "migrate" ? GradientPolicy::Migrate : GradientPolicy::Drop;
+                else if (k == "balance") sc.opts.balance_fanout = std::stoi(v) != 0;
+                else if (k == "scalar_words") sc.opts.scalar_words = std::stoll(v);
+                else throw ConfigError(strfmt("line %d: bad option", lineno));
+            }
+        } else {
+            throw ConfigError(strfmt("line %d: unknown keyword '%s'", lineno, tok[0].c_str()));
+        }
+    }
+    return sc;
+}
+
+std::vector<core::FlatXfer> expand(const rs_plan* p, int device) {
+    if (device >= 0) return gpuplan::expand_flat_gpu(p->core, device, nullptr);
+    return core::expand_flat_host(p->core);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+const char* rs_version(void) { return "reshard-b200 0.1 (sm_100a)"; }
+void rs_free(void* p) { std::free(p); }
+
+int rs_model_create(const rs_tensor_t* tensors, int n, int num_layers, int num_experts, rs_model_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto m = std::make_unique<rs_model>();
+        m->spec.num_layers = num_layers;
+        m->spec.num_experts = num_experts;
+        for (int i = 0; i < n; ++i) {
+            const rs_tensor_t& t = tensors[i];
+            if (!t.id || t.ndim < 1 || t.ndim > 4) throw ConfigError("tensor needs an id and 1..4 dims");
+            TensorSpec s;
+            s.tensor_id = t.id;
+            s.shape.assign(t.shape, t.shape + t.ndim);
+            s.layer = t.layer;
+            if (t.tp_axis >= 0) s.tp_shard_axis = t.tp_axis;
+            if (t.expert_axis >= 0) s.expert_axis = t.expert_axis, s.is_expert = true;
+            s.dtype_bytes = t.dtype_bytes;
+            m->spec.tensors.push_back(std::move(s));
+        }
+        m->space = build_model_space(m->spec);
+        *out = m.release();
+        return RS_OK;
+    });
+}
+
+void rs_model_destroy(rs_model_t* m) { delete m; }
+
+int rs_plan_create(const rs_model_t* m, const rs_cfg_t* src, const rs_cfg_t* dst, const rs_worldmap_t* wm,
+                   const rs_topo_t* topo, const rs_options_t* opts, rs_plan_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (!m || !src || !dst) throw ConfigError("null model or config");
+        auto p = std::make_unique<rs_plan>();
+        p->model = m;
+        WorldMap w;
+        if (wm) {
+            w.src_phys.assign(wm->src_phys, wm->src_phys + wm->n_src);
+            w.dst_phys.assign(wm->dst_phys, wm->dst_phys + wm->n_dst);
+        }
+        Topology t;
+        if (topo) t.num_nodes = topo->num_nodes, t.ranks_per_node = topo->ranks_per_node;
+        PlanOptions o;
+        bool allow = false;
+        if (opts) {
+            o.gradients = opts->migrate_grads ? GradientPolicy::Migrate : GradientPolicy::Drop;
+            o.balance_fanout = opts->balance_fanout != 0;
+            o.scalar_words = opts->scalar_words;
+            allow = opts->allow_oversourced != 0;
+        }
+        p->core = core::build_plan(m->space, to_cfg(*src), to_cfg(*dst), wm ? &w : nullptr, t, o, allow);
+        *out = p.release();
+        return RS_OK;
+    });
+}
+
+int rs_plan_from_scenario(const char* text, int allow_oversourced, rs_plan_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        Scenario sc = parse_scenario(text ? text : "");
+        auto m = std::make_shared<rs_model>();
+        m->spec = sc.model;
+        m->space = build_model_space(m->spec);
+        auto p = std::make_unique<rs_plan>();
+        p->owned = m;
+        p->model = m.get();
+        p->core = core::build_plan(m->space, sc.src, sc.dst, sc.has_world ? &sc.wm : nullptr, sc.topo, sc.opts,
+                                   allow_oversourced != 0);
+        *out = p.release();
+        return RS_OK;
+    });
+}
+
+void rs_plan_destroy(rs_plan_t* p) { delete p; }
+
+int rs_plan_summary(const rs_plan_t* p, rs_plan_summary_t* out) {
+    return guarded([&] {
+        std::memset(out, 0, sizeof *out);
+        const core::PlanCore& c = p->core;
+        out->num_box_transfers = static_cast<std::int64_t>(c.box.size());
+        out->num_flat_transfers = c.n_flat;
+        out->num_transfers = c.num_transfers();
+        out->bytes_moved = c.bytes_moved;
+        out->bytes_retained = c.bytes_retained;
+        out->num_triples = static_cast<std::int64_t>(c.triples.size());
+        out->src_world = c.src_cfg.world_size();
+        out->dst_world = c.dst_cfg.world_size();
+        out->num_participants = static_cast<int>(c.routes.size());
+        out->total_numel = c.space->total_numel();
+        out->fingerprint = c.space->fingerprint();
+        return RS_OK;
+    });
+}
+
+int rs_plan_dump(const rs_plan_t* p, int device, char** out, size_t* len) {
+    return guarded([&] {
+        *out = dup_string(core::dump(p->core, expand(p, device)), len);
+        return RS_OK;
+    });
+}
+
+int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len) {
+    return guarded([&] {
+        *out = dup_string(core::dump(p->core, core::expand_flat_rows_host(p->core)), len);
+        return RS_OK;
+    });
+}
+
+int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64_t* n) {
+    return guarded([&] {
+        const core::PlanCore& c = p->core;
+        const std::vector<core::FlatXfer> flat = expand(p, device);
+        const size_t total = c.box.size() + flat.size();
+        rs_transfer_t* arr = static_cast<rs_transfer_t*>(std::calloc(total ? total : 1, sizeof(rs_transfer_t)));
+        if (!arr) throw std::bad_alloc();
+        size_t bi = 0, fi = 0, k = 0;
+        while (bi < c.box.size() || fi < flat.size()) {
+            bool take_box;
+            if (bi == c.box.size()) take_box = false;
+            else if (fi == flat.size()) take_box = true;
+            else {
+                const auto& b = c.box[bi];
+                const auto& f = flat[fi];
+                take_box = b.src != f.src ? b.src < f.src : b.dst != f.dst ? b.dst < f.dst : b.kind < 1;
+            }
+            rs_transfer_t& t = arr[k++];
+            if (take_box) {
+                const auto& b = c.box[bi++];
+                t.kind = b.kind;
+                t.tensor = b.tensor;
+                t.flat = 0;
+                t.ndim = static_cast<int>(c.space->entries()[static_cast<size_t>(b.tensor)].spec.shape.size());
+                for (int d = 0; d < 4; ++d) t.lo[d] = b.lo[d], t.hi[d] = b.hi[d];
+                t.src_rank = b.src;
+                t.dst_rank = b.dst;
+                t.count = b.count;
+                t.bytes = b.bytes;
+            } else {
+                const auto& f = flat[fi++];
+                t.kind = RS_KIND_OPTIM;
+                t.tensor = -1;
+                t.flat = 1;
+                t.ndim = 1;
+                t.lo[0] = f.lo;
+                t.hi[0] = f.hi;
+                t.src_rank = f.src;
+                t.dst_rank = f.dst;
+                t.count = f.hi - f.lo;
+                t.bytes = t.count * kOptimStateBytes;
+            }
+            t.src_phys = c.wm.src_phys[static_cast<size_t>(t.src_rank)];
+            t.dst_phys = c.wm.dst_phys[static_cast<size_t>(t.dst_rank)];
+        }
+        *out = arr;
+        *n = static_cast<int64_t>(total);
+        return RS_OK;
+    });
+}
+
+int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len) {
+    return guarded([&] {
+        const ModelSpace& space = *p->core.space;
+        const ParallelConfig& cfg = side == RS_SIDE_SRC ? p->core.src_cfg : p->core.dst_cfg;
+        std::string s;
+        for (int r = 0; r < cfg.world_size(); ++r) {
+            const RegionSet reg = project(space, cfg, r);
+            for (const auto& [id, boxes] : reg.boxes)
+                for (const Box& b : boxes) s += strfmt("rank %d param %s %s\n", r, id.c_str(), format_box(b).c_str());
+            const LocalLayout L = local_layout(space, cfg, r);
+            for (const auto& seg : L.dense)
+                s += strfmt("rank %d layout dense %s %s %lld %lld\n", r, seg.tensor_id.c_str(), format_box(seg.box).c_str(),
+                            static_cast<long long>(seg.local_lo), static_cast<long long>(seg.local_hi));
+            for (const auto& seg : L.expert)
+                s += strfmt("rank %d layout expert %s %s %lld %lld\n", r, seg.tensor_id.c_str(), format_box(seg.box).c_str(),
+                            static_cast<long long>(seg.local_lo), static_cast<long long>(seg.local_hi));
+            if (cfg.zero_enabled)
+                for (const Interval& iv : project_optimizer(space, cfg, r).flat)
+                    s += strfmt("rank %d optim %s\n", r, format_interval(iv).c_str());
+        }
+        *out = dup_string(s, len);
+        return RS_OK;
+    });
+}
+
+int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        exec::ExecConfig cfg;
+        if (o) {
+            cfg.n_gpus = o->n_gpus;
+            cfg.gpu = o->gpu;
+            cfg.device = o->device;
+            cfg.with_grads = o->with_grads != 0;
+            cfg.tile_bytes = o->tile_bytes;
+            cfg.ctas_per_sm = o->ctas_per_sm;
+        }
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw exec::CudaError("no CUDA device: the executor has no CPU fallback");
+        auto e = std::make_unique<rs_exec>();
+        e->plan = p;
+        e->ex = std::make_unique<exec::Executor>(p->core, cfg);
+        *out = e.release();
+        return RS_OK;
+    });
+}
+
+void rs_exec_destroy(rs_exec_t* e) { delete e; }
+
+int rs_exec_alloc(rs_exec_t* e) {
+    return guarded([&] {
+        e->ex->alloc();
+        return RS_OK;
+    });
+}
+
+int rs_exec_bind(rs_exec_t* e, int side, int rank, int buf, void* dptr, int64_t bytes) {
+    return guarded([&] {
+        e->ex->bind(side, rank, buf, dptr, bytes);
+        return RS_OK;
+    });
+}
+
+int rs_exec_buffer(rs_exec_t* e, int side, int rank, int buf, void** dptr, int64_t* bytes, int* gpu) {
+    return guarded([&] {
+        if (side < 0 || side > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
+        const int n = side == 0 ? e->plan->core.src_cfg.world_size() : e->plan->core.dst_cfg.world_size();
+        if (rank < 0 || rank >= n) throw ConfigError("bad rank");
+        std::int64_t b = 0;
+        *dptr = e->ex->buffer(side, rank, buf, &b);
+        *bytes = b;
+        if (gpu) *gpu = e->ex->rank_gpu(side, rank);
+        return RS_OK;
+    });
+}
+
+int rs_exec_ipc_export(rs_exec_t* e, void* out, size_t cap, size_t* len) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> blob = e->ex->export_ipc();
+        *len = blob.size();
+        if (out && cap >= blob.size()) std::memcpy(out, blob.data(), blob.size());
+        else if (out) throw ConfigError("ipc export buffer too small");
+        return RS_OK;
+    });
+}
+
+int rs_exec_ipc_import(rs_exec_t* e, const void* blob, size_t len) {
+    return guarded([&] {
+        e->ex->import_ipc(static_cast<const std::uint8_t*>(blob), len);
+        return RS_OK;
+    });
+}
+
+int rs_exec_prepare(rs_exec_t* e) {
+    return guarded([&] {
+        e->ex->prepare();
+        return RS_OK;
+    });
+}
+
+int rs_exec_fill(rs_exec_t* e, int side, uint64_t seed, void* stream) {
+    return guarded([&] {
+        e->ex->fill(side, seed, static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
+int rs_exec_run(rs_exec_t* e, void* stream, int* launches) {
+    return guarded([&] {
+        const int n = e->ex->run(static_cast<cudaStream_t>(stream));
+        if (launches) *launches = n;
+        return RS_OK;
+    });
+}
+
+int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t* mismatches, int64_t* first_bad) {
+    return guarded([&] {
+        std::int64_t fb = -1;
+        const std::int64_t bad = e->ex->verify(side, seed, static_cast<cudaStream_t>(stream), &fb);
+        if (mismatches) *mismatches = bad;
+        if (first_bad) *first_bad = fb;
+        return bad ? fail(RS_ERR_VIOLATION, strfmt("%lld mismatching elements (first flat index %lld)",
+                                                   static_cast<long long>(bad), static_cast<long long>(fb)))
+                   : RS_OK;
+    });
+}
+
+int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
+    return guarded([&] {
+        const exec::ExecStats& s = e->ex->stats();
+        out->local_bytes = s.local_bytes;
+        out->remote_bytes = s.remote_bytes;
+        out->tiles = s.tiles;
+        for (int i = 0; i < 5; ++i) out->tiles_by_class[i] = s.tiles_by_class[i];
+        return RS_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,559 @@
+// sm_100a executor: copy-tile kernel (local HBM and NVLink peer stores), canon
+// fill / verify kernels, per-GPU orchestration and cudaIpc peer mapping.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "reshard/executor.hpp"
+#include "reshard/executor_rt.hpp"
+
+namespace reshard {
+namespace exec {
+
+#define RS_CUDA(x)                                                                                          \
+    do {                                                                                                    \
+        cudaError_t e_ = (x);                                                                               \
+        if (e_ != cudaSuccess) throw CudaError(strfmt("%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                                      __FILE__, __LINE__));                                 \
+    } while (0)
+
+// ------------------------------------------------------------------ kernels
+
+constexpr int kThreads = 512;
+constexpr int kUnroll = 4;
+
+template <int V>
+struct VecT;
+template <>
+struct VecT<16> { using T = uint4; };
+template <>
+struct VecT<8> { using T = uint2; };
+template <>
+struct VecT<4> { using T = unsigned int; };
+template <>
+struct VecT<2> { using T = unsigned short; };
+template <>
+struct VecT<1> { using T = unsigned char; };
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint4 ld_stream<uint4>(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+/// Copy tiles of alignment class V (all addresses, pitches and row sizes are
+/// multiples of V). Persistent grid: CTA b takes tiles b, b+grid, ... Each thread
+/// keeps kUnroll independent loads in flight before storing.
+template <int V>
+__global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles) {
+    using T = typename VecT<V>::T;
+    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+        const Tile tl = tiles[ti];
+        const unsigned vpr = tl.row_bytes / V;
+        if (tl.rows == 1) {
+            const T* __restrict__ s = reinterpret_cast<const T*>(tl.src);
+            T* __restrict__ d = reinterpret_cast<T*>(tl.dst);
+            unsigned i = threadIdx.x;
+            for (; i + (kUnroll - 1) * kThreads < vpr; i += kUnroll * kThreads) {
+                T r[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(s + i + u * kThreads);
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) d[i + u * kThreads] = r[u];
+            }
+            for (; i < vpr; i += kThreads) d[i] = ld_stream(s + i);
+        } else {
+            const unsigned n = tl.rows * vpr;
+            for (unsigned i = threadIdx.x; i < n; i += kUnroll * kThreads) {
+                T r[kUnroll];
+                unsigned row[kUnroll], col[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const unsigned e = i + u * kThreads;
+                    row[u] = e / vpr;
+                    col[u] = e - row[u] * vpr;
+                    if (e < n)
+                        r[u] = ld_stream(reinterpret_cast<const T*>(tl.src + row[u] * tl.src_pitch) + col[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const unsigned e = i + u * kThreads;
+                    if (e < n) reinterpret_cast<T*>(tl.dst + row[u] * tl.dst_pitch)[col[u]] = r[u];
+                }
+            }
+        }
+    }
+}
+
+/// value of element with global flat index k for buffer kind
+__device__ __forceinline__ std::uint64_t canon_payload(std::uint64_t seed, std::int64_t k, int kind) {
+    switch (kind) {
+        case 0: return canon_value(seed, k, StateKind::Param);
+        case 1: return canon_value(seed, k, StateKind::Optim) & 0xffffffffull;
+        case 2: return canon_value(seed, k, StateKind::Optim) >> 32;
+        case 3: return canon_value(seed ^ 0x5eedull, k, StateKind::Optim) & 0xffffffffull;
+        default: return canon_value(seed, k, StateKind::Grad) & 0xffffffffull;
+    }
+}
+
+__device__ __forceinline__ std::int64_t task_flat(const FillTask& f, std::int64_t e) {
+    const std::int64_t c = e % f.cols_box;
+    std::int64_t q = e / f.cols_box;
+    const std::int64_t r = q % f.rows_box;
+    q /= f.rows_box;
+    std::int64_t p[2] = {0, 0};
+    for (int i = f.t.np - 1; i >= 0; --i) {
+        p[i] = f.plo[i] + q % f.pext_box[i];
+        q /= f.pext_box[i];
+    }
+    return stair::flat_of(f.t, p, f.rlo + r, f.clo + c);
+}
+
+__global__ void fill_kernel(const FillTask* __restrict__ tasks, int ntasks, std::uint64_t seed) {
+    for (int ti = blockIdx.y; ti < ntasks; ti += gridDim.y) {
+        const FillTask f = tasks[ti];
+        const std::int64_t n = f.e_hi - f.e_lo;
+        for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (std::int64_t)gridDim.x * blockDim.x) {
+            const std::uint64_t v = canon_payload(seed, task_flat(f, f.e_lo + i), f.kind);
+            char* dst = reinterpret_cast<char*>(f.ptr) + i * f.width;
+            switch (f.width) {
+                case 1: *reinterpret_cast<std::uint8_t*>(dst) = static_cast<std::uint8_t>(v); break;
+                case 2: *reinterpret_cast<std::uint16_t*>(dst) = static_cast<std::uint16_t>(v); break;
+                case 4: *reinterpret_cast<std::uint32_t*>(dst) = static_cast<std::uint32_t>(v); break;
+                default: *reinterpret_cast<std::uint64_t*>(dst) = v; break;
+            }
+        }
+    }
+}
+
+__global__ void verify_kernel(const FillTask* __restrict__ tasks, int ntasks, std::uint64_t seed,
+                              unsigned long long* __restrict__ bad, long long* __restrict__ first_bad) {
+    unsigned long long local_bad = 0;
+    for (int ti = blockIdx.y; ti < ntasks; ti += gridDim.y) {
+        const FillTask f = tasks[ti];
+        const std::int64_t n = f.e_hi - f.e_lo;
+        for (std::int64_t i = blockIdx.x * (std::int64_t)blockDim.x + threadIdx.x; i < n;
+             i += (std::int64_t)gridDim.x * blockDim.x) {
+            const std::int64_t k = task_flat(f, f.e_lo + i);
+            const std::uint64_t v = canon_payload(seed, k, f.kind);
+            const char* src = reinterpret_cast<const char*>(f.ptr) + i * f.width;
+            std::uint64_t got;
+            std::uint64_t mask;
+            switch (f.width) {
+                case 1: got = *reinterpret_cast<const std::uint8_t*>(src); mask = 0xffull; break;
+                case 2: got = *reinterpret_cast<const std::uint16_t*>(src); mask = 0xffffull; break;
+                case 4: got = *reinterpret_cast<const std::uint32_t*>(src); mask = 0xffffffffull; break;
+                default: got = *reinterpret_cast<const std::uint64_t*>(src); mask = ~0ull; break;
+            }
+            if (got != (v & mask)) {
+                ++local_bad;
+                atomicMin(first_bad, static_cast<long long>(k));
+            }
+        }
+    }
+    if (local_bad) atomicAdd(bad, local_bad);
+}
+
+__global__ void fill_scalars_kernel(std::uint64_t* p, std::int64_t words, std::uint64_t seed) {
+    for (std::int64_t w = threadIdx.x; w < words; w += blockDim.x) p[w] = canon_value(seed, w, StateKind::Scalar);
+}
+
+__global__ void verify_scalars_kernel(const std::uint64_t* p, std::int64_t words, std::uint64_t seed,
+                                      unsigned long long* bad) {
+    for (std::int64_t w = threadIdx.x; w < words; w += blockDim.x)
+        if (p[w] != canon_value(seed, w, StateKind::Scalar)) atomicAdd(bad, 1ull);
+}
+
+// ------------------------------------------------------------------ host side
+
+namespace {
+
+/// driver API through the runtime's entry-point table (no link-time libcuda
+/// dependency, so the library also loads on GPU-less build hosts)
+CUresult mem_get_address_range(CUdeviceptr* base, size_t* size, CUdeviceptr p) {
+    using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+            return CUDA_ERROR_NOT_SUPPORTED;
+        fn = reinterpret_cast<Fn>(f);
+    }
+    return fn(base, size, p);
+}
+
+int align_class(std::uint64_t x) {
+    if (x % 16 == 0) return 16;
+    if (x % 8 == 0) return 8;
+    if (x % 4 == 0) return 4;
+    if (x % 2 == 0) return 2;
+    return 1;
+}
+int class_index(int v) { return v == 16 ? 0 : v == 8 ? 1 : v == 4 ? 2 : v == 2 ? 3 : 4; }
+
+}  // namespace
+
+Executor::Executor(const core::PlanCore& P, const ExecConfig& cfg) : P_(P), cfg_(cfg) {
+    if (cfg_.n_gpus < 1 || cfg_.gpu < 0 || cfg_.gpu >= cfg_.n_gpus) throw ConfigError("bad executor placement");
+    int max_phys = 0;
+    for (const auto& r : P_.routes) max_phys = std::max(max_phys, r.phys);
+    per_gpu_ = (max_phys + 1 + cfg_.n_gpus - 1) / cfg_.n_gpus;
+    for (int side = 0; side < 2; ++side) {
+        const int n = side == 0 ? P_.src_cfg.world_size() : P_.dst_cfg.world_size();
+        bufs_[side].resize(static_cast<size_t>(n));
+        for (int r = 0; r < n; ++r) {
+            RankBufs& rb = bufs_[side][static_cast<size_t>(r)];
+            buffer_sizes(P_, side, r, cfg_.with_grads, rb.bytes);
+            const int phys = side == 0 ? P_.wm.src_phys[static_cast<size_t>(r)] : P_.wm.dst_phys[static_cast<size_t>(r)];
+            rb.gpu = gpu_of_phys(phys);
+        }
+    }
+    RS_CUDA(cudaSetDevice(cfg_.device));
+}
+
+Executor::~Executor() {
+    cudaSetDevice(cfg_.device);
+    for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
+    for (void* p : owned_) cudaFree(p);
+    if (d_tiles_) cudaFree(d_tiles_);
+    if (d_fill_) cudaFree(d_fill_);
+    if (d_counters_) cudaFree(d_counters_);
+}
+
+int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
+
+void Executor::alloc() {
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    for (int side = 0; side < 2; ++side)
+        for (RankBufs& rb : bufs_[side]) {
+            if (rb.gpu != cfg_.gpu) continue;
+            for (int b = 0; b < kNumBufs; ++b) {
+                if (rb.ptr[b] || rb.bytes[b] == 0) continue;
+                void* p = nullptr;
+                RS_CUDA(cudaMalloc(&p, static_cast<size_t>(rb.bytes[b])));
+                owned_.push_back(p);
+                rb.ptr[b] = p;
+            }
+        }
+}
+
+void Executor::bind(int side, int rank, int buf, void* ptr, std::int64_t bytes) {
+    if (side < 0 || side > 1 || rank < 0 || rank >= static_cast<int>(bufs_[side].size()) || buf < 0 || buf >= kNumBufs)
+        throw ConfigError("bind: bad buffer id");
+    RankBufs& rb = bufs_[side][static_cast<size_t>(rank)];
+    if (bytes < rb.bytes[buf]) throw ConfigError(strfmt("bind: buffer too small (%lld < %lld)",
+                                                         static_cast<long long>(bytes), static_cast<long long>(rb.bytes[buf])));
+    rb.ptr[buf] = ptr;
+}
+
+void* Executor::buffer(int side, int rank, int buf, std::int64_t* bytes) const {
+    const RankBufs& rb = bufs_[side][static_cast<size_t>(rank)];
+    *bytes = rb.bytes[buf];
+    return rb.ptr[buf];
+}
+
+std::vector<std::uint8_t> Executor::export_ipc() const {
+    // [int32 count] then per local dst buffer: int32 rank, int32 buf, int64 offset, handle
+    std::vector<std::uint8_t> out(4, 0);
+    int count = 0;
+    for (size_t r = 0; r < bufs_[1].size(); ++r) {
+        const RankBufs& rb = bufs_[1][r];
+        if (rb.gpu != cfg_.gpu) continue;
+        for (int b = 0; b < kNumBufs; ++b) {
+            if (!rb.ptr[b]) continue;
+            CUdeviceptr base = 0;
+            size_t size = 0;
+            if (mem_get_address_range(&base, &size, reinterpret_cast<CUdeviceptr>(rb.ptr[b])) != CUDA_SUCCESS)
+                throw CudaError("cuMemGetAddressRange failed");
+            cudaIpcMemHandle_t h;
+            RS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+            const std::int32_t rr = static_cast<std::int32_t>(r), bb = b;
+            const std::int64_t off = static_cast<std::int64_t>(reinterpret_cast<CUdeviceptr>(rb.ptr[b]) - base);
+            const size_t at = out.size();
+            out.resize(at + 16 + sizeof h);
+            std::memcpy(out.data() + at, &rr, 4);
+            std::memcpy(out.data() + at + 4, &bb, 4);
+            std::memcpy(out.data() + at + 8, &off, 8);
+            std::memcpy(out.data() + at + 16, &h, sizeof h);
+            ++count;
+        }
+    }
+    std::memcpy(out.data(), &count, 4);
+    return out;
+}
+
+void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    if (len < 4) throw ConfigError("ipc blob too short");
+    int count;
+    std::memcpy(&count, blob, 4);
+    size_t at = 4;
+    for (int i = 0; i < count; ++i) {
+        if (at + 16 + sizeof(cudaIpcMemHandle_t) > len) throw ConfigError("ipc blob truncated");
+        std::int32_t r, b;
+        std::int64_t off;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&r, blob + at, 4);
+        std::memcpy(&b, blob + at + 4, 4);
+        std::memcpy(&off, blob + at + 8, 8);
+        std::memcpy(&h, blob + at + 16, sizeof h);
+        at += 16 + sizeof h;
+        RankBufs& rb = bufs_[1].at(static_cast<size_t>(r));
+        if (rb.gpu == cfg_.gpu) continue;
+        void* base = nullptr;
+        auto key = std::string(reinterpret_cast<const char*>(&h), sizeof h);
+        auto it = ipc_map_.find(key);
+        if (it == ipc_map_.end()) {
+            RS_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened_.push_back(base);
+            ipc_map_.emplace(key, base);
+        } else {
+            base = it->second;
+        }
+        rb.ptr[b] = static_cast<char*>(base) + off;
+    }
+}
+
+void Executor::prepare() {
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    const std::vector<CopyOp> ops = build_ops(P_);
+    std::vector<Tile> cls[5];
+    stats_ = ExecStats{};
+    const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
+    for (const CopyOp& op : ops) {
+        const RankBufs& S = bufs_[0][static_cast<size_t>(op.src_side_rank)];
+        if (S.gpu != cfg_.gpu) continue;  // pushed by the source's GPU
+        const RankBufs& D = bufs_[1][static_cast<size_t>(op.dst_rank)];
+        if (op.rows <= 0 || op.row_bytes <= 0) continue;
+        if (!S.ptr[op.src_buf] || !D.ptr[op.dst_buf])
+            throw ConfigError(strfmt("prepare: buffer not bound (src rank %d buf %d -> dst rank %d buf %d)",
+                                     op.src_side_rank, op.src_buf, op.dst_rank, op.dst_buf));
+        const bool remote = D.gpu != cfg_.gpu;
+        const std::int64_t total = op.rows * op.row_bytes;
+        (remote ? stats_.remote_bytes : stats_.local_bytes) += total;
+        std::uint64_t src = reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off);
+        std::uint64_t dst = reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off);
+        std::int64_t rows = op.rows, rb = op.row_bytes, sp = op.src_pitch, dp = op.dst_pitch;
+        if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
+            rb *= rows;
+            rows = 1;
+        }
+        auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
+            Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
+                   static_cast<std::uint32_t>(nb)};
+            std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
+            if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
+            cls[class_index(align_class(a))].push_back(t);
+        };
+        if (rows == 1 || rb >= kTile) {
+            for (std::int64_t r = 0; r < rows; ++r) {
+                std::uint64_t s = src + static_cast<std::uint64_t>(r * sp), d = dst + static_cast<std::uint64_t>(r * dp);
+                std::int64_t left = rb;
+                // peel an unaligned head so the body runs 16-byte vectors when both
+                // sides share the same misalignment
+                if ((s % 16) == (d % 16) && (s % 16) != 0) {
+                    const std::int64_t head = std::min<std::int64_t>(left, 16 - static_cast<std::int64_t>(s % 16));
+                    emit(s, d, 1, head);
+                    s += static_cast<std::uint64_t>(head);
+                    d += static_cast<std::uint64_t>(head);
+                    left -= head;
+                }
+                while (left > 0) {
+                    const std::int64_t n = std::min(left, kTile);
+                    const bool aligned = (s % 16) == 0 && (d % 16) == 0;
+                    const std::int64_t body = (aligned && n > 16) ? n - n % 16 : n;
+                    emit(s, d, 1, body);
+                    s += static_cast<std::uint64_t>(body);
+                    d += static_cast<std::uint64_t>(body);
+                    left -= body;
+                }
+            }
+        } else {
+            const std::int64_t per = std::max<std::int64_t>(1, kTile / rb);
+            for (std::int64_t r = 0; r < rows; r += per) {
+                const std::int64_t nr = std::min(per, rows - r);
+                emit(src + static_cast<std::uint64_t>(r * sp), dst + static_cast<std::uint64_t>(r * dp), nr, rb);
+            }
+        }
+    }
+    host_tiles_.clear();
+    for (int c = 0; c < 5; ++c) {
+        class_begin_[c] = static_cast<int>(host_tiles_.size());
+        host_tiles_.insert(host_tiles_.end(), cls[c].begin(), cls[c].end());
+        class_count_[c] = static_cast<int>(cls[c].size());
+    }
+    stats_.tiles = static_cast<std::int64_t>(host_tiles_.size());
+    for (int c = 0; c < 5; ++c) stats_.tiles_by_class[c] = class_count_[c];
+    if (d_tiles_) cudaFree(d_tiles_);
+    d_tiles_ = nullptr;
+    if (!host_tiles_.empty()) {
+        RS_CUDA(cudaMalloc(&d_tiles_, host_tiles_.size() * sizeof(Tile)));
+        RS_CUDA(cudaMemcpy(d_tiles_, host_tiles_.data(), host_tiles_.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+    }
+    if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device);
+    sms_ = sms;
+    prepared_ = true;
+}
+
+int Executor::run(cudaStream_t stream) {
+    if (!prepared_) throw ConfigError("run before prepare");
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    int launches = 0;
+    const int grid_cap = sms_ * (cfg_.ctas_per_sm > 0 ? cfg_.ctas_per_sm : 4);
+    const Tile* base = static_cast<const Tile*>(d_tiles_);
+    for (int c = 0; c < 5; ++c) {
+        const int n = class_count_[c];
+        if (!n) continue;
+        const int grid = std::min(n, grid_cap);
+        const Tile* t = base + class_begin_[c];
+        switch (c) {
+            case 0: copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n); break;
+            case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n); break;
+            case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n); break;
+            case 3: copy_tiles_kernel<2><<<grid, kThreads, 0, stream>>>(t, n); break;
+            default: copy_tiles_kernel<1><<<grid, kThreads, 0, stream>>>(t, n); break;
+        }
+        ++launches;
+    }
+    RS_CUDA(cudaGetLastError());
+    return launches;
+}
+
+std::vector<FillTask> Executor::fill_tasks(int side) const {
+    std::vector<FillTask> tasks;
+    const core::Side& S = side == 0 ? P_.src : P_.dst;
+    for (size_t r = 0; r < S.ranks.size(); ++r) {
+        const RankBufs& rb = bufs_[side][r];
+        if (rb.gpu != cfg_.gpu) continue;
+        const core::RankGeom& g = S.ranks[r];
+        for (const core::Seg& s : g.segs) {
+            const auto& e = P_.space->entries()[static_cast<size_t>(s.tensor)];
+            FillTask f{};
+            // lifted box
+            const int nd = static_cast<int>(e.spec.shape.size());
+            std::int64_t l[4], h[4], x[4];
+            int n = 0;
+            if (nd == 1) l[n] = 0, h[n] = 1, x[n] = 1, ++n;
+            for (int d = 0; d < nd; ++d) l[n] = s.blo[d], h[n] = s.bhi[d], x[n] = e.spec.shape[static_cast<size_t>(d)], ++n;
+            f.t.np = n - 2;
+            for (int i = 0; i < f.t.np; ++i) f.t.pext[i] = x[i], f.plo[i] = l[i], f.pext_box[i] = h[i] - l[i];
+            f.t.rows = x[f.t.np];
+            f.t.cols = x[f.t.np + 1];
+            f.t.off = e.offset;
+            f.rlo = l[f.t.np];
+            f.rows_box = h[f.t.np] - l[f.t.np];
+            f.clo = l[f.t.np + 1];
+            f.cols_box = h[f.t.np + 1] - l[f.t.np + 1];
+            const std::int64_t n_el = s.local_hi - s.local_lo;
+            // params
+            if (rb.ptr[kParam]) {
+                FillTask p = f;
+                p.ptr = reinterpret_cast<std::uint64_t>(rb.ptr[kParam]) + static_cast<std::uint64_t>(s.param_byte_off);
+                p.e_lo = 0;
+                p.e_hi = n_el;
+                p.kind = 0;
+                p.width = e.spec.dtype_bytes;
+                tasks.push_back(p);
+            }
+            if (rb.ptr[kGrad]) {
+                FillTask p = f;
+                p.ptr = reinterpret_cast<std::uint64_t>(rb.ptr[kGrad]) + static_cast<std::uint64_t>(s.elem_off * 4);
+                p.e_lo = 0;
+                p.e_hi = n_el;
+                p.kind = 4;
+                p.width = 4;
+                tasks.push_back(p);
+            }
+            const Interval& sh = s.expert ? g.eshard : g.dshard;
+            const std::int64_t lo = std::max(sh.lo, s.local_lo), hi = std::min(sh.hi, s.local_hi);
+            if (lo < hi)
+                for (int b = kMaster; b <= kV; ++b) {
+                    if (!rb.ptr[b]) continue;
+                    FillTask p = f;
+                    const std::int64_t oi = g.optim_index(s.expert, lo);
+                    p.ptr = reinterpret_cast<std::uint64_t>(rb.ptr[b]) + static_cast<std::uint64_t>(oi * 4);
+                    p.e_lo = lo - s.local_lo;
+                    p.e_hi = hi - s.local_lo;
+                    p.kind = b;
+                    p.width = 4;
+                    tasks.push_back(p);
+                }
+        }
+    }
+    return tasks;
+}
+
+void Executor::upload_tasks(const std::vector<FillTask>& tasks) {
+    if (d_fill_) cudaFree(d_fill_);
+    d_fill_ = nullptr;
+    if (tasks.empty()) return;
+    RS_CUDA(cudaMalloc(&d_fill_, tasks.size() * sizeof(FillTask)));
+    RS_CUDA(cudaMemcpy(d_fill_, tasks.data(), tasks.size() * sizeof(FillTask), cudaMemcpyHostToDevice));
+}
+
+void Executor::fill(int side, std::uint64_t seed, cudaStream_t stream) {
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    const std::vector<FillTask> tasks = fill_tasks(side);
+    upload_tasks(tasks);
+    if (!tasks.empty()) {
+        dim3 grid(static_cast<unsigned>(sms_ * 2), static_cast<unsigned>(std::min<size_t>(tasks.size(), 65535)));
+        fill_kernel<<<grid, 256, 0, stream>>>(static_cast<const FillTask*>(d_fill_), static_cast<int>(tasks.size()), seed);
+    }
+    for (size_t r = 0; r < bufs_[side].size(); ++r) {
+        const RankBufs& rb = bufs_[side][r];
+        if (rb.gpu == cfg_.gpu && rb.ptr[kScalars])
+            fill_scalars_kernel<<<1, 64, 0, stream>>>(static_cast<std::uint64_t*>(rb.ptr[kScalars]),
+                                                       rb.bytes[kScalars] / 8, seed);
+    }
+    RS_CUDA(cudaGetLastError());
+    RS_CUDA(cudaStreamSynchronize(stream));
+}
+
+std::int64_t Executor::verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad) {
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    const std::vector<FillTask> tasks = fill_tasks(side);
+    upload_tasks(tasks);
+    unsigned long long* bad = static_cast<unsigned long long*>(d_counters_);
+    long long* first = reinterpret_cast<long long*>(static_cast<char*>(d_counters_) + 8);
+    const long long big = 0x7fffffffffffffffll;
+    RS_CUDA(cudaMemsetAsync(bad, 0, 8, stream));
+    RS_CUDA(cudaMemcpyAsync(first, &big, 8, cudaMemcpyHostToDevice, stream));
+    if (!tasks.empty()) {
+        dim3 grid(static_cast<unsigned>(sms_ * 2), static_cast<unsigned>(std::min<size_t>(tasks.size(), 65535)));
+        verify_kernel<<<grid, 256, 0, stream>>>(static_cast<const FillTask*>(d_fill_), static_cast<int>(tasks.size()),
+                                                seed, bad, first);
+    }
+    for (size_t r = 0; r < bufs_[side].size(); ++r) {
+        const RankBufs& rb = bufs_[side][r];
+        if (rb.gpu == cfg_.gpu && rb.ptr[kScalars])
+            verify_scalars_kernel<<<1, 64, 0, stream>>>(static_cast<const std::uint64_t*>(rb.ptr[kScalars]),
+                                                         rb.bytes[kScalars] / 8, seed, bad);
+    }
+    RS_CUDA(cudaGetLastError());
+    unsigned long long h_bad = 0;
+    long long h_first = 0;
+    RS_CUDA(cudaMemcpyAsync(&h_bad, bad, 8, cudaMemcpyDeviceToHost, stream));
+    RS_CUDA(cudaMemcpyAsync(&h_first, first, 8, cudaMemcpyDeviceToHost, stream));
+    RS_CUDA(cudaStreamSynchronize(stream));
+    if (first_bad) *first_bad = h_bad ? h_first : -1;
+    return static_cast<std::int64_t>(h_bad);
+}
+
+}  // namespace exec
+}  // namespace reshard

@@ -1,0 +1,169 @@
+// CopyOp construction: every element movement of a transition (plan transfers,
+// retained regions, scalar broadcast) as 2-D strided byte copies between the
+// physical buffers of DESIGN.md §3. Pure host code; GPU-independent.
+#include <algorithm>
+
+#include "reshard/executor.hpp"
+
+namespace reshard {
+namespace exec {
+
+namespace {
+
+using core::PlanCore;
+using core::RankGeom;
+using core::Seg;
+
+struct LBox {
+    int np;
+    std::int64_t plo[2], pext[2], rlo, rows, clo, cols;
+};
+
+LBox lift_seg(const TensorSpec& t, const std::int64_t* lo, const std::int64_t* hi) {
+    LBox b{};
+    const int nd = static_cast<int>(t.shape.size());
+    std::int64_t l[4], h[4];
+    int n = 0;
+    if (nd == 1) l[n] = 0, h[n] = 1, ++n;
+    for (int d = 0; d < nd; ++d) l[n] = lo[d], h[n] = hi[d], ++n;
+    b.np = n - 2;
+    for (int i = 0; i < b.np; ++i) b.plo[i] = l[i], b.pext[i] = h[i] - l[i];
+    b.rlo = l[b.np];
+    b.rows = h[b.np] - l[b.np];
+    b.clo = l[b.np + 1];
+    b.cols = h[b.np + 1] - l[b.np + 1];
+    return b;
+}
+
+/// element index of (p, r, c) in the row-major enumeration of box B
+std::int64_t elem_in(const LBox& B, const std::int64_t* p, std::int64_t r, std::int64_t c) {
+    std::int64_t q = 0;
+    for (int i = 0; i < B.np; ++i) q = q * B.pext[i] + (p[i] - B.plo[i]);
+    return (q * B.rows + (r - B.rlo)) * B.cols + (c - B.clo);
+}
+
+struct Emitter {
+    const PlanCore& P;
+    std::vector<CopyOp>& out;
+
+    const Seg& seg(int side, int rank, int t) const {
+        const RankGeom& g = (side == 0 ? P.src : P.dst).ranks[static_cast<size_t>(rank)];
+        return g.segs[static_cast<size_t>(g.seg_of[static_cast<size_t>(t)])];
+    }
+    const RankGeom& geom(int side, int rank) const { return (side == 0 ? P.src : P.dst).ranks[static_cast<size_t>(rank)]; }
+
+    /// rectangle (plane p, rows [r0,r1), cols [c0,c1)) of tensor t, kind, src k -> dst j
+    void rect(int kind, int t, int k, int j, const std::int64_t* p, std::int64_t r0, std::int64_t r1,
+              std::int64_t c0, std::int64_t c1) {
+        const TensorSpec& ts = P.space->entries()[static_cast<size_t>(t)].spec;
+        const Seg& S = seg(0, k, t);
+        const Seg& D = seg(1, j, t);
+        const LBox Bs = lift_seg(ts, S.blo, S.bhi), Bd = lift_seg(ts, D.blo, D.bhi);
+        const std::int64_t es = elem_in(Bs, p, r0, c0), ed = elem_in(Bd, p, r0, c0);
+        const std::int64_t rows = r1 - r0, w = c1 - c0;
+        if (kind == 0) {
+            const int dt = ts.dtype_bytes;
+            out.push_back(CopyOp{k, kParam, j, kParam, S.param_byte_off + es * dt, D.param_byte_off + ed * dt, rows, w * dt,
+                                 Bs.cols * dt, Bd.cols * dt});
+        } else if (kind == 2) {
+            out.push_back(CopyOp{k, kGrad, j, kGrad, (S.elem_off + es) * 4, (D.elem_off + ed) * 4, rows, w * 4,
+                                 Bs.cols * 4, Bd.cols * 4});
+        } else {
+            const std::int64_t os = geom(0, k).optim_index(S.expert, S.local_lo + es);
+            const std::int64_t od = geom(1, j).optim_index(D.expert, D.local_lo + ed);
+            if (os < 0 || od < 0) throw std::logic_error("optimizer move outside the shard");
+            for (int b = kMaster; b <= kV; ++b)
+                out.push_back(CopyOp{k, b, j, b, os * 4, od * 4, rows, w * 4, Bs.cols * 4, Bd.cols * 4});
+        }
+    }
+
+    /// box X (tensor coordinates) of kind from src k to dst j, one rect per plane
+    void box(int kind, int t, int k, int j, const std::int64_t* lo, const std::int64_t* hi) {
+        const TensorSpec& ts = P.space->entries()[static_cast<size_t>(t)].spec;
+        const LBox X = lift_seg(ts, lo, hi);
+        std::int64_t p[2] = {0, 0};
+        const std::int64_t e0 = X.np > 0 ? X.pext[0] : 1, e1 = X.np > 1 ? X.pext[1] : 1;
+        for (std::int64_t a = 0; a < e0; ++a)
+            for (std::int64_t b = 0; b < e1; ++b) {
+                if (X.np > 0) p[0] = X.plo[0] + a;
+                if (X.np > 1) p[1] = X.plo[1] + b;
+                rect(kind, t, k, j, p, X.rlo, X.rlo + X.rows, X.clo, X.clo + X.cols);
+            }
+    }
+
+    void triple(const stair::Triple& T) {
+        core::for_each_band(T, [&](const std::int64_t* p, std::int64_t u, std::int64_t v, const stair::Iv* cols, int n) {
+            for (int i = 0; i < n; ++i) rect(1, T.tensor, T.src, T.dst, p, u, v, cols[i].lo, cols[i].hi);
+        });
+    }
+
+    /// flat run [lo,hi) of optimizer state (D2 override), split at tensor rows
+    void flat_run(const core::FlatXfer& f) {
+        const auto& ents = P.space->entries();
+        std::int64_t x = f.lo;
+        while (x < f.hi) {
+            auto it = std::upper_bound(ents.begin(), ents.end(), x,
+                                       [](std::int64_t v, const ModelSpace::Entry& e) { return v < e.offset; });
+            const int t = static_cast<int>(it - ents.begin()) - 1;
+            const auto& e = ents[static_cast<size_t>(t)];
+            const std::int64_t zero[4] = {0, 0, 0, 0};
+            std::int64_t full[4];
+            for (size_t d = 0; d < e.spec.shape.size(); ++d) full[d] = e.spec.shape[d];
+            const LBox Tb = lift_seg(e.spec, zero, full);
+            const std::int64_t rel = x - e.offset;
+            const std::int64_t grow = rel / Tb.cols, c = rel % Tb.cols;
+            std::int64_t p[2] = {0, 0}, g = grow / Tb.rows;
+            const std::int64_t r = grow % Tb.rows;
+            for (int i = Tb.np - 1; i >= 0; --i) p[i] = g % Tb.pext[i], g /= Tb.pext[i];
+            const std::int64_t end = std::min(f.hi, x + (Tb.cols - c));
+            rect(1, t, f.src, f.dst, p, r, r + 1, c, c + (end - x));
+            x = end;
+        }
+    }
+};
+
+}  // namespace
+
+std::vector<CopyOp> build_ops(const PlanCore& P) {
+    std::vector<CopyOp> ops;
+    Emitter E{P, ops};
+    for (const core::BoxXfer& b : P.box) E.box(b.kind, b.tensor, b.src, b.dst, b.lo, b.hi);
+    for (const core::BoxXfer& b : P.box_retain) E.box(b.kind, b.tensor, b.src, b.dst, b.lo, b.hi);
+    const int nt = P.ntensors();
+    auto overridden = [&](int j, int t) {
+        return !P.d2_tensor_dst.empty() && P.d2_tensor_dst[static_cast<size_t>(j) * nt + t];
+    };
+    for (const stair::Triple& T : P.triples)
+        if (!overridden(T.dst, T.tensor)) E.triple(T);
+    for (const stair::Triple& T : P.retain_triples) E.triple(T);
+    for (const core::FlatXfer& f : P.d2_runs) {
+        // only the overridden tensors of a D2 route come from runs
+        core::FlatXfer g = f;
+        const auto& ents = P.space->entries();
+        std::int64_t x = g.lo;
+        while (x < g.hi) {
+            auto it = std::upper_bound(ents.begin(), ents.end(), x,
+                                       [](std::int64_t v, const ModelSpace::Entry& e) { return v < e.offset; });
+            const int t = static_cast<int>(it - ents.begin()) - 1;
+            const std::int64_t tend = ents[static_cast<size_t>(t)].offset + ents[static_cast<size_t>(t)].spec.numel();
+            const std::int64_t end = std::min(g.hi, tend);
+            if (overridden(g.dst, t)) E.flat_run(core::FlatXfer{x, end, g.src, g.dst});
+            x = end;
+        }
+    }
+    if (P.has_scalars)
+        for (int j = 0; j < P.dst_cfg.world_size(); ++j)
+            ops.push_back(CopyOp{0, kScalars, j, kScalars, 0, 0, 1, P.scalar_bytes_per_rank, 0, 0});
+    return ops;
+}
+
+void buffer_sizes(const PlanCore& P, int side, int rank, bool with_grads, std::int64_t out[kNumBufs]) {
+    const RankGeom& g = (side == 0 ? P.src : P.dst).ranks[static_cast<size_t>(rank)];
+    out[kParam] = g.param_bytes;
+    out[kMaster] = out[kM] = out[kV] = g.optim_len * 4;
+    out[kGrad] = with_grads ? g.nelem * 4 : 0;
+    out[kScalars] = P.opts.scalar_words * kScalarWordBytes;
+}
+
+}  // namespace exec
+}  // namespace reshard

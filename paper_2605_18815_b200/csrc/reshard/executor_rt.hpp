@@ -1,0 +1,96 @@
+// Executor runtime object (per GPU / per process). See executor.hpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "reshard/executor.hpp"
+
+namespace reshard {
+namespace exec {
+
+class CudaError : public std::runtime_error {
+public:
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+struct ExecConfig {
+    int n_gpus = 1;       // GPUs the physical devices of the plan are placed on
+    int gpu = 0;          // this process's GPU index in [0, n_gpus)
+    int device = 0;       // CUDA device ordinal
+    bool with_grads = false;
+    std::int64_t tile_bytes = 0;  // 0 -> 512 KiB
+    int ctas_per_sm = 0;          // 0 -> 4
+};
+
+struct ExecStats {
+    std::int64_t local_bytes = 0;   // bytes this GPU copies into its own HBM
+    std::int64_t remote_bytes = 0;  // bytes this GPU stores into peers' HBM
+    std::int64_t tiles = 0;
+    std::int64_t tiles_by_class[5] = {0, 0, 0, 0, 0};  // 16/8/4/2/1-byte vectors
+};
+
+struct RankBufs {
+    int gpu = -1;
+    void* ptr[kNumBufs] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    std::int64_t bytes[kNumBufs] = {0, 0, 0, 0, 0, 0};
+};
+
+class Executor {
+public:
+    Executor(const core::PlanCore& P, const ExecConfig& cfg);
+    ~Executor();
+    Executor(const Executor&) = delete;
+    Executor& operator=(const Executor&) = delete;
+
+    int gpu_of_phys(int phys) const;
+    /// cudaMalloc every unbound buffer of the virtual ranks placed on this GPU
+    void alloc();
+    /// use a caller-owned device buffer (side 0 src / 1 dst)
+    void bind(int side, int rank, int buf, void* ptr, std::int64_t bytes);
+    void* buffer(int side, int rank, int buf, std::int64_t* bytes) const;
+    int rank_gpu(int side, int rank) const { return bufs_[side][static_cast<size_t>(rank)].gpu; }
+
+    /// cudaIpc handles of this GPU's destination buffers / map a peer's
+    std::vector<std::uint8_t> export_ipc() const;
+    void import_ipc(const std::uint8_t* blob, size_t len);
+
+    /// build device tiles for the moves whose source lives here
+    void prepare();
+    /// launch the transition; returns the number of kernel launches
+    int run(cudaStream_t stream);
+
+    void fill(int side, std::uint64_t seed, cudaStream_t stream);
+    std::int64_t verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad);
+
+    const ExecStats& stats() const { return stats_; }
+    const core::PlanCore& plan() const { return P_; }
+
+private:
+    std::vector<FillTask> fill_tasks(int side) const;
+    void upload_tasks(const std::vector<FillTask>& tasks);
+
+    const core::PlanCore& P_;
+    ExecConfig cfg_;
+    int per_gpu_ = 1;
+    int sms_ = 148;
+    std::vector<RankBufs> bufs_[2];
+    std::vector<void*> owned_;
+    std::vector<void*> ipc_opened_;
+    std::map<std::string, void*> ipc_map_;
+    std::vector<Tile> host_tiles_;
+    int class_begin_[5] = {0, 0, 0, 0, 0};
+    int class_count_[5] = {0, 0, 0, 0, 0};
+    void* d_tiles_ = nullptr;
+    void* d_fill_ = nullptr;
+    void* d_counters_ = nullptr;
+    bool prepared_ = false;
+    ExecStats stats_;
+};
+
+}  // namespace exec
+}  // namespace reshard
