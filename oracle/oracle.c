@@ -1507,16 +1507,28 @@ static void load_fn(void* cx, int rank, rstate_t* R, int si, int64_t e, int64_t 
     }
 }
 
-/* load_state */
-void or_state_load(or_state* st, uint64_t seed) {
-    lv_ctx c = {st, seed, 0, NULL, 0};
-    for (int r = 0; r < st->nranks; ++r) {
-        for_each_elem(st, r, load_fn, &c);
-        for (int64_t w = 0; w < st->s->scalar_words; ++w) {
-            uint64_t v = or_canon(seed, w, 3);
-            memcpy(st->r[r].buf[5] + w * 8, &v, 8);
-        }
+/* load_state; ranks are independent, so they load in parallel */
+typedef struct { or_state* st; uint64_t seed; int rank; } load_job;
+static void* load_worker(void* a) {
+    load_job* j = a;
+    lv_ctx c = {j->st, j->seed, 0, NULL, 0};
+    for_each_elem(j->st, j->rank, load_fn, &c);
+    for (int64_t w = 0; w < j->st->s->scalar_words; ++w) {
+        uint64_t v = or_canon(j->seed, w, 3);
+        memcpy(j->st->r[j->rank].buf[5] + w * 8, &v, 8);
     }
+    return NULL;
+}
+void or_state_load(or_state* st, uint64_t seed) {
+    pthread_t* th = xrealloc(NULL, sizeof(pthread_t) * (size_t)st->nranks);
+    load_job* jobs = xrealloc(NULL, sizeof(load_job) * (size_t)st->nranks);
+    for (int r = 0; r < st->nranks; ++r) {
+        jobs[r] = (load_job){st, seed, r};
+        pthread_create(&th[r], NULL, load_worker, &jobs[r]);
+    }
+    for (int r = 0; r < st->nranks; ++r) pthread_join(th[r], NULL);
+    free(th);
+    free(jobs);
 }
 
 static void verify_fn(void* cx, int rank, rstate_t* R, int si, int64_t e, int64_t k) {
@@ -1550,20 +1562,43 @@ static void verify_fn(void* cx, int rank, rstate_t* R, int si, int64_t e, int64_
 #undef BAD
 }
 
-/* verify_state */
+/* verify_state; ranks checked in parallel, first violation by rank order */
+typedef struct { or_state* st; uint64_t seed; int rank; int64_t bad; char msg[256]; } verify_job;
+static void* verify_worker(void* a) {
+    verify_job* j = a;
+    lv_ctx c = {j->st, j->seed, 0, j->msg, sizeof j->msg};
+    j->msg[0] = 0;
+    for_each_elem(j->st, j->rank, verify_fn, &c);
+    for (int64_t w = 0; w < j->st->s->scalar_words; ++w) {
+        uint64_t v;
+        memcpy(&v, j->st->r[j->rank].buf[5] + w * 8, 8);
+        if (v != or_canon(j->seed, w, 3) && c.bad++ == 0)
+            snprintf(j->msg, sizeof j->msg, "rank %d scalar word %lld mismatch", j->rank, (long long)w);
+    }
+    j->bad = c.bad;
+    return NULL;
+}
 int64_t or_verify(const or_state* stc, uint64_t seed, char* err, size_t errlen) {
     or_state* st = (or_state*)stc;
-    lv_ctx c = {st, seed, 0, err, errlen};
     if (err && errlen) err[0] = 0;
+    pthread_t* th = xrealloc(NULL, sizeof(pthread_t) * (size_t)st->nranks);
+    verify_job* jobs = xrealloc(NULL, sizeof(verify_job) * (size_t)st->nranks);
     for (int r = 0; r < st->nranks; ++r) {
-        for_each_elem(st, r, verify_fn, &c);
-        for (int64_t w = 0; w < st->s->scalar_words; ++w) {
-            uint64_t v;
-            memcpy(&v, st->r[r].buf[5] + w * 8, 8);
-            if (v != or_canon(seed, w, 3)) { if (c.bad++ == 0 && err) snprintf(err, errlen, "rank %d scalar word %lld mismatch", r, (long long)w); }
-        }
+        jobs[r].st = st;
+        jobs[r].seed = seed;
+        jobs[r].rank = r;
+        jobs[r].bad = 0;
+        pthread_create(&th[r], NULL, verify_worker, &jobs[r]);
     }
-    return c.bad;
+    int64_t bad = 0;
+    for (int r = 0; r < st->nranks; ++r) {
+        pthread_join(th[r], NULL);
+        if (jobs[r].bad && bad == 0 && err) snprintf(err, errlen, "%s", jobs[r].msg);
+        bad += jobs[r].bad;
+    }
+    free(th);
+    free(jobs);
+    return bad;
 }
 
 /* locate global coordinate c (tensor t) inside rank R's segment: returns segment
