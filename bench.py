@@ -174,22 +174,32 @@ def run_ours(args):
     sc = S.config2(args.layers)
     t0 = time.perf_counter()
     ab = RoutingPlan.from_scenario(sc)
-    ba = RoutingPlan.from_scenario(sc.reversed())
+    # the way back (DP2xTP4 -> TP8) has TP-replicated norms in several ZeRO shards: the
+    # reference throws there (defect D2); the documented extension resolves it
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
     plan_s = time.perf_counter() - t0
     # forward and backward transitions share buffers: A (TP8) and B (DP2xTP4)
     fwd = Transition(ab, n, rank, dev, alloc=False)
     bwd = Transition(ba, n, rank, dev, alloc=False)
     keep = []
-    for side_ab, side_ba in ((A.SIDE_SRC, A.SIDE_DST), (A.SIDE_DST, A.SIDE_SRC)):
-        nr = ab.summary.src_world if side_ab == A.SIDE_SRC else ab.summary.dst_world
-        for r in range(nr):
-            for b in range(6):
-                _, nbytes, g = fwd.ex.buffer(side_ab, r, b)
-                if nbytes and g == rank:
-                    t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-                    keep.append(t)
-                    fwd.ex.bind(side_ab, r, b, t.data_ptr(), nbytes)
-                    bwd.ex.bind(side_ba, r, b, t.data_ptr(), nbytes)
+    arena = None
+    if n == 1 and not args.no_arena:
+        # 8 virtual ranks on one GPU: old + new state (240.9 GB at L=32) exceed HBM, so
+        # the memory-aware arena maps new-layout chunks onto dead old-layout chunks
+        from paper_2605_18815_b200.api import Arena
+        arena = Arena(ab, ba, device=dev, cap_bytes=args.hbm_cap)
+        arena.bind(fwd.ex, bwd.ex)
+    else:
+        for side_ab, side_ba in ((A.SIDE_SRC, A.SIDE_DST), (A.SIDE_DST, A.SIDE_SRC)):
+            nr = ab.summary.src_world if side_ab == A.SIDE_SRC else ab.summary.dst_world
+            for r in range(nr):
+                for b in range(6):
+                    _, nbytes, g = fwd.ex.buffer(side_ab, r, b)
+                    if nbytes and g == rank:
+                        t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                        keep.append(t)
+                        fwd.ex.bind(side_ab, r, b, t.data_ptr(), nbytes)
+                        bwd.ex.bind(side_ba, r, b, t.data_ptr(), nbytes)
     fwd.connect()
     bwd.connect()
     seed = 0xC0FFEE
@@ -310,8 +320,12 @@ def run_ours(args):
                     "what": "descriptor rebuild + upload, both transitions, result readback"},
             "clocks": clk.summary(),
         }
-        out["gpu_launches"] = sum(1 for c in st_f.tiles_by_class if c) * args.steps + \
-            sum(1 for c in bwd.ex.stats().tiles_by_class if c) * args.steps
+        out["gpu_launches"] = (st_f.launches + bwd.ex.stats().launches) * args.steps
+        if arena is not None:
+            a = arena.stats()
+            out["memory"] = {"physical_gb": round(a.physical_bytes / 1e9, 2), "old_layout_gb": round(a.a_bytes / 1e9, 2),
+                             "new_layout_gb": round(a.b_bytes / 1e9, 2), "aliased_gb": round(a.aliased_bytes / 1e9, 2),
+                             "stages_fwd": arena.stage_order(0), "stages_bwd": arena.stage_order(1)}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -327,6 +341,8 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--cpu-layers", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-arena", action="store_true", help="N=1: plain allocations (needs old+new to fit)")
+    ap.add_argument("--hbm-cap", type=int, default=0, help="arena physical budget in bytes (0: free HBM - 1 GiB)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

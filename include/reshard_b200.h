@@ -155,7 +155,27 @@ typedef struct {
     int64_t remote_bytes;  /* bytes stored into peer GPUs over NVLink */
     int64_t tiles;
     int64_t tiles_by_class[5];
+    int64_t launches;      /* kernel launches per rs_exec_run */
 } rs_exec_stats_t;
+
+/* ---- memory-aware arena (Algorithm 1 FreeObsoleteBuffers / eager free,
+ * PAPER.md:668,689,942): old (A) and new (B) layouts of every virtual rank on one GPU
+ * in CUDA VMM ranges; B chunks reuse the physical memory of A chunks that die in an
+ * earlier stage (for a round trip, also vice versa). plan_ba may be NULL (one way). */
+typedef struct rs_arena rs_arena_t;
+typedef struct {
+    int64_t physical_bytes, a_bytes, b_bytes, aliased_bytes, chunks;
+} rs_arena_stats_t;
+int rs_arena_create(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int device, int64_t cap_bytes,
+                    int64_t chunk_bytes, int with_grads, rs_arena_t** out);
+void rs_arena_destroy(rs_arena_t* a);
+/* layout 0 = A (src of plan_ab), 1 = B (dst of plan_ab) */
+int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** dptr, int64_t* bytes);
+/* destination-rank stage order of direction 0 (A->B) or 1 (B->A) */
+int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n);
+int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out);
+/* run the plan as memory-aware stages: dst ranks in the given order */
+int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n);
 
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
 void rs_exec_destroy(rs_exec_t* e);

@@ -20,7 +20,8 @@ EXPORTED = [
     "rs_plan_from_scenario", "rs_plan_destroy", "rs_plan_summary", "rs_plan_dump", "rs_plan_transfers",
     "rs_plan_regions", "rs_plan_dump_rows_host", "rs_exec_create", "rs_exec_destroy", "rs_exec_alloc",
     "rs_exec_bind", "rs_exec_buffer", "rs_exec_ipc_export", "rs_exec_ipc_import", "rs_exec_prepare",
-    "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats",
+    "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats", "rs_exec_set_stages",
+    "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
 ]
 
 
@@ -68,7 +69,12 @@ class ExecOpts_t(C.Structure):
 
 class ExecStats_t(C.Structure):
     _fields_ = [("local_bytes", C.c_int64), ("remote_bytes", C.c_int64), ("tiles", C.c_int64),
-                ("tiles_by_class", C.c_int64 * 5)]
+                ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64)]
+
+
+class ArenaStats_t(C.Structure):
+    _fields_ = [("physical_bytes", C.c_int64), ("a_bytes", C.c_int64), ("b_bytes", C.c_int64),
+                ("aliased_bytes", C.c_int64), ("chunks", C.c_int64)]
 
 
 _lib = None
@@ -109,9 +115,16 @@ def lib():
     L.rs_exec_run.argtypes = [vp, vp, P(C.c_int)]
     L.rs_exec_verify.argtypes = [vp, C.c_int, C.c_uint64, vp, P(i64), P(i64)]
     L.rs_exec_stats.argtypes = [vp, P(ExecStats_t)]
+    L.rs_exec_set_stages.argtypes = [vp, P(C.c_int), C.c_int]
+    L.rs_arena_create.argtypes = [vp, vp, C.c_int, i64, i64, C.c_int, P(vp)]
+    L.rs_arena_destroy.argtypes = [vp]
+    L.rs_arena_buffer.argtypes = [vp, C.c_int, C.c_int, C.c_int, P(vp), P(i64)]
+    L.rs_arena_stage_order.argtypes = [vp, C.c_int, P(C.c_int), C.c_int, P(C.c_int)]
+    L.rs_arena_stats.argtypes = [vp, P(ArenaStats_t)]
     for name in EXPORTED:
         fn = getattr(L, name)
-        if fn.restype is None and name not in ("rs_free", "rs_model_destroy", "rs_plan_destroy", "rs_exec_destroy"):
+        if fn.restype is None and name not in ("rs_free", "rs_model_destroy", "rs_plan_destroy", "rs_exec_destroy",
+                                                      "rs_arena_destroy"):
             fn.restype = C.c_int
     _lib = L
     return L

@@ -182,3 +182,55 @@ class Executor:
         s = A.ExecStats_t()
         A.check(A.lib().rs_exec_stats(self.h, C.byref(s)))
         return s
+
+    def set_stages(self, dst_order) -> None:
+        arr = (C.c_int * max(1, len(dst_order)))(*dst_order)
+        A.check(A.lib().rs_exec_set_stages(self.h, arr, len(dst_order)))
+
+
+class Arena:
+    """VMM old/new layouts on one GPU with plan-time eager-free aliasing (arena.hpp)."""
+
+    def __init__(self, ab: RoutingPlan, ba: Optional[RoutingPlan] = None, device: int = 0, cap_bytes: int = 0,
+                 chunk_bytes: int = 0, with_grads: bool = False):
+        h = C.c_void_p()
+        A.check(A.lib().rs_arena_create(ab.h, ba.h if ba else None, device, cap_bytes, chunk_bytes,
+                                        int(with_grads), C.byref(h)))
+        self.h = h.value
+        self.ab, self.ba = ab, ba
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            A.lib().rs_arena_destroy(self.h)
+            self.h = None
+
+    def buffer(self, layout: int, rank: int, buf: int):
+        p, n = C.c_void_p(), C.c_int64()
+        A.check(A.lib().rs_arena_buffer(self.h, layout, rank, buf, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
+
+    def stage_order(self, direction: int) -> List[int]:
+        out = (C.c_int * 1024)()
+        n = C.c_int()
+        A.check(A.lib().rs_arena_stage_order(self.h, direction, out, 1024, C.byref(n)))
+        return list(out[: n.value])
+
+    def stats(self) -> A.ArenaStats_t:
+        s = A.ArenaStats_t()
+        A.check(A.lib().rs_arena_stats(self.h, C.byref(s)))
+        return s
+
+    def bind(self, fwd: "Executor", bwd: Optional["Executor"] = None) -> None:
+        """Bind A/B buffers into the forward (A->B) and backward (B->A) executors and
+        set their stage orders."""
+        for layout, nr in ((0, self.ab.summary.src_world), (1, self.ab.summary.dst_world)):
+            for r in range(nr):
+                for b in range(6):
+                    p, n = self.buffer(layout, r, b)
+                    if n:
+                        fwd.bind(layout, r, b, p, n)
+                        if bwd is not None:
+                            bwd.bind(1 - layout, r, b, p, n)
+        fwd.set_stages(self.stage_order(0))
+        if bwd is not None:
+            bwd.set_stages(self.stage_order(1))

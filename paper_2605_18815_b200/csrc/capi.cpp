@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "reshard/arena.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
 
@@ -31,6 +32,10 @@ struct rs_plan {
     std::shared_ptr<rs_model> owned;  // set when created from scenario text
     const rs_model* model = nullptr;
     core::PlanCore core;
+};
+
+struct rs_arena {
+    std::unique_ptr<mem::Arena> a;
 };
 
 struct rs_exec {
@@ -55,6 +60,8 @@ int guarded(F&& f) {
         return fail(RS_ERR_CONFIG, e.what());
     } catch (const exec::CudaError& e) {
         return fail(RS_ERR_CUDA, e.what());
+    } catch (const exec::BudgetError& e) {
+        return fail(RS_ERR_BUDGET, e.what());
     } catch (const std::bad_alloc&) {
         return fail(RS_ERR_INTERNAL, "out of host memory");
     } catch (const std::exception& e) {
@@ -487,6 +494,64 @@ int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
         out->remote_bytes = s.remote_bytes;
         out->tiles = s.tiles;
         for (int i = 0; i < 5; ++i) out->tiles_by_class[i] = s.tiles_by_class[i];
+        out->launches = s.launches;
+        return RS_OK;
+    });
+}
+
+int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n) {
+    return guarded([&] {
+        e->ex->set_stage_order(std::vector<int>(dst_order, dst_order + (dst_order ? n : 0)));
+        return RS_OK;
+    });
+}
+
+int rs_arena_create(const rs_plan_t* ab, const rs_plan_t* ba, int device, int64_t cap_bytes, int64_t chunk_bytes,
+                    int with_grads, rs_arena_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw exec::CudaError("no CUDA device");
+        mem::ArenaConfig cfg;
+        cfg.device = device;
+        cfg.cap_bytes = cap_bytes;
+        if (chunk_bytes > 0) cfg.chunk_bytes = chunk_bytes;
+        auto a = std::make_unique<rs_arena>();
+        a->a = std::make_unique<mem::Arena>(ab->core, ba ? &ba->core : nullptr, cfg, with_grads != 0);
+        *out = a.release();
+        return RS_OK;
+    });
+}
+
+void rs_arena_destroy(rs_arena_t* a) { delete a; }
+
+int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** dptr, int64_t* bytes) {
+    return guarded([&] {
+        if (layout < 0 || layout > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
+        *dptr = a->a->ptr(layout, rank, buf);
+        *bytes = a->a->bytes(layout, rank, buf);
+        return RS_OK;
+    });
+}
+
+int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n) {
+    return guarded([&] {
+        if (dir < 0 || dir > 1) throw ConfigError("bad direction");
+        const std::vector<int>& o = a->a->stage_order(dir);
+        *n = static_cast<int>(o.size());
+        for (int i = 0; i < *n && i < cap; ++i) out[i] = o[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
+int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
+    return guarded([&] {
+        const mem::ArenaStats& s = a->a->stats();
+        out->physical_bytes = s.physical_bytes;
+        out->a_bytes = s.a_bytes;
+        out->b_bytes = s.b_bytes;
+        out->aliased_bytes = s.aliased_bytes;
+        out->chunks = s.chunks;
         return RS_OK;
     });
 }

@@ -236,6 +236,23 @@ Executor::~Executor() {
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
 
+void Executor::set_stage_order(const std::vector<int>& dst_order) {
+    const int nd = P_.dst_cfg.world_size();
+    if (dst_order.empty()) {
+        stage_of_dst_.clear();
+        return;
+    }
+    if (static_cast<int>(dst_order.size()) != nd) throw ConfigError("stage order must list every destination rank once");
+    std::vector<int> pos(static_cast<size_t>(nd), -1);
+    for (size_t s = 0; s < dst_order.size(); ++s) {
+        const int j = dst_order[s];
+        if (j < 0 || j >= nd || pos[static_cast<size_t>(j)] >= 0) throw ConfigError("bad stage order");
+        pos[static_cast<size_t>(j)] = static_cast<int>(s);
+    }
+    stage_of_dst_ = pos;
+    prepared_ = false;
+}
+
 void Executor::alloc() {
     RS_CUDA(cudaSetDevice(cfg_.device));
     for (int side = 0; side < 2; ++side)
@@ -331,7 +348,8 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
 void Executor::prepare() {
     RS_CUDA(cudaSetDevice(cfg_.device));
     const std::vector<CopyOp> ops = build_ops(P_);
-    std::vector<Tile> cls[5];
+    const int nstage = stage_of_dst_.empty() ? 1 : *std::max_element(stage_of_dst_.begin(), stage_of_dst_.end()) + 1;
+    std::vector<std::vector<Tile>> cls(static_cast<size_t>(nstage) * 5);
     stats_ = ExecStats{};
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
     for (const CopyOp& op : ops) {
@@ -352,12 +370,13 @@ void Executor::prepare() {
             rb *= rows;
             rows = 1;
         }
+        const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
         auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
             Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
                    static_cast<std::uint32_t>(nb)};
             std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
             if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-            cls[class_index(align_class(a))].push_back(t);
+            cls[static_cast<size_t>(stage) * 5 + class_index(align_class(a))].push_back(t);
         };
         if (rows == 1 || rb >= kTile) {
             for (std::int64_t r = 0; r < rows; ++r) {
@@ -391,13 +410,17 @@ void Executor::prepare() {
         }
     }
     host_tiles_.clear();
-    for (int c = 0; c < 5; ++c) {
-        class_begin_[c] = static_cast<int>(host_tiles_.size());
-        host_tiles_.insert(host_tiles_.end(), cls[c].begin(), cls[c].end());
-        class_count_[c] = static_cast<int>(cls[c].size());
-    }
+    groups_.clear();
+    for (int st = 0; st < nstage; ++st)
+        for (int c = 0; c < 5; ++c) {
+            const auto& v = cls[static_cast<size_t>(st) * 5 + c];
+            if (v.empty()) continue;
+            groups_.push_back({c, static_cast<int>(host_tiles_.size()), static_cast<int>(v.size())});
+            host_tiles_.insert(host_tiles_.end(), v.begin(), v.end());
+            stats_.tiles_by_class[c] += static_cast<std::int64_t>(v.size());
+        }
     stats_.tiles = static_cast<std::int64_t>(host_tiles_.size());
-    for (int c = 0; c < 5; ++c) stats_.tiles_by_class[c] = class_count_[c];
+    stats_.launches = static_cast<std::int64_t>(groups_.size());
     if (d_tiles_) cudaFree(d_tiles_);
     d_tiles_ = nullptr;
     if (!host_tiles_.empty()) {
@@ -417,12 +440,11 @@ int Executor::run(cudaStream_t stream) {
     int launches = 0;
     const int grid_cap = sms_ * (cfg_.ctas_per_sm > 0 ? cfg_.ctas_per_sm : 4);
     const Tile* base = static_cast<const Tile*>(d_tiles_);
-    for (int c = 0; c < 5; ++c) {
-        const int n = class_count_[c];
-        if (!n) continue;
+    for (const Group& g : groups_) {
+        const int n = g.count;
         const int grid = std::min(n, grid_cap);
-        const Tile* t = base + class_begin_[c];
-        switch (c) {
+        const Tile* t = base + g.begin;
+        switch (g.cls) {
             case 0: copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n); break;
             case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n); break;
             case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n); break;
@@ -529,6 +551,7 @@ std::int64_t Executor::verify(int side, std::uint64_t seed, cudaStream_t stream,
     RS_CUDA(cudaSetDevice(cfg_.device));
     const std::vector<FillTask> tasks = fill_tasks(side);
     upload_tasks(tasks);
+    if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
     unsigned long long* bad = static_cast<unsigned long long*>(d_counters_);
     long long* first = reinterpret_cast<long long*>(static_cast<char*>(d_counters_) + 8);
     const long long big = 0x7fffffffffffffffll;

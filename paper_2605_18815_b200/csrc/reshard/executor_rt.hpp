@@ -18,6 +18,12 @@ public:
     explicit CudaError(const std::string& m) : std::runtime_error(m) {}
 };
 
+/// Memory-aware schedule infeasible under the HBM cap (C ABI RS_ERR_BUDGET).
+class BudgetError : public std::runtime_error {
+public:
+    explicit BudgetError(const std::string& m) : std::runtime_error(m) {}
+};
+
 struct ExecConfig {
     int n_gpus = 1;       // GPUs the physical devices of the plan are placed on
     int gpu = 0;          // this process's GPU index in [0, n_gpus)
@@ -32,6 +38,7 @@ struct ExecStats {
     std::int64_t remote_bytes = 0;  // bytes this GPU stores into peers' HBM
     std::int64_t tiles = 0;
     std::int64_t tiles_by_class[5] = {0, 0, 0, 0, 0};  // 16/8/4/2/1-byte vectors
+    std::int64_t launches = 0;                         // kernel launches per run()
 };
 
 struct RankBufs {
@@ -48,6 +55,9 @@ public:
     Executor& operator=(const Executor&) = delete;
 
     int gpu_of_phys(int phys) const;
+    /// memory-aware stages: destination ranks in execution order, one launch group
+    /// per stage (a stage starts after all reads of earlier stages completed)
+    void set_stage_order(const std::vector<int>& dst_order);
     /// cudaMalloc every unbound buffer of the virtual ranks placed on this GPU
     void alloc();
     /// use a caller-owned device buffer (side 0 src / 1 dst)
@@ -82,9 +92,12 @@ private:
     std::vector<void*> owned_;
     std::vector<void*> ipc_opened_;
     std::map<std::string, void*> ipc_map_;
+    struct Group {
+        int cls, begin, count;
+    };
     std::vector<Tile> host_tiles_;
-    int class_begin_[5] = {0, 0, 0, 0, 0};
-    int class_count_[5] = {0, 0, 0, 0, 0};
+    std::vector<Group> groups_;
+    std::vector<int> stage_of_dst_;
     void* d_tiles_ = nullptr;
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;

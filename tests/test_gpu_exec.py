@@ -155,3 +155,28 @@ def test_no_gpu_no_fallback_message():
     plan = RoutingPlan.from_scenario(S.config1())
     with pytest.raises(A.ConfigError):
         Executor(plan, n_gpus=2, gpu=5)
+
+
+def test_arena_round_trip_aliased():
+    """Memory-aware arena: new-layout chunks alias dead old-layout chunks; a round
+    trip through stages is still bit-exact."""
+    from paper_2605_18815_b200.api import Arena
+    sc = S.config2(2)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    arena = Arena(ab, ba, chunk_bytes=2 << 20)
+    st = arena.stats()
+    assert st.aliased_bytes > 0
+    assert st.physical_bytes < st.a_bytes + st.b_bytes
+    e1, e2 = Executor(ab), Executor(ba)
+    arena.bind(e1, e2)
+    e1.fill(0, SEED)
+    e1.prepare()
+    e2.prepare()
+    for _ in range(2):
+        e1.run()
+        torch.cuda.synchronize()
+        assert e1.verify(1, SEED)[0] == 0
+        e2.run()
+        torch.cuda.synchronize()
+        assert e2.verify(1, SEED)[0] == 0
