@@ -41,43 +41,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """`nvidia-smi -lms 100` (clocks + throttle reasons) running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu, self.samples, self._stop = gpu, [], threading.Event()
-        self.t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        self.gpu, self.samples, self.p = gpu, [], None
 
     def __enter__(self):
-        self.t.start()
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.3)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self.t.join(timeout=10)
+        if self.p is None:
+            return
+        time.sleep(0.2)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        self.samples = [[x.strip() for x in l.split(",")] for l in out.splitlines() if l.strip()]
 
     def summary(self):
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        pw = [num(s[2]) for s in self.samples if len(s) > 2 and num(s[2]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.samples[0][1]) if self.samples[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        loaded = [x for x in sm if x > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": num(self.samples[0][1]),
+                "power_w_max": max(pw) if pw else None, "reasons": reasons, "samples": len(self.samples)}
 
 
 class CpuBaseline:
@@ -225,8 +234,15 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     barrier()
-    # correctness of the measured configuration (outside the timed region)
+    # correctness of the measured configuration (outside the timed region): B right
+    # after A->B, A right after B->A (with the arena, B is dead once A is rebuilt)
+    fwd.run(sp)
+    torch.cuda.synchronize()
+    barrier()
     bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
+    bwd.run(sp)
+    torch.cuda.synchronize()
+    barrier()
     bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
