@@ -136,6 +136,12 @@ int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64
 /* project / local_layout / project_optimizer of every rank of one side
  * (project.hpp:44, :94, :146), text lines */
 int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len);
+/* per-GPU byte accounting under contiguous-block placement of the plan's devices on
+ * n_gpus GPUs (host only): local copies, bytes pushed to / received from peers */
+typedef struct {
+    int64_t local_bytes, out_bytes, in_bytes, ops;
+} rs_placement_stats_t;
+int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
 

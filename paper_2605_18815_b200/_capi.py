@@ -21,7 +21,7 @@ EXPORTED = [
     "rs_plan_regions", "rs_plan_dump_rows_host", "rs_exec_create", "rs_exec_destroy", "rs_exec_alloc",
     "rs_exec_bind", "rs_exec_buffer", "rs_exec_ipc_export", "rs_exec_ipc_import", "rs_exec_prepare",
     "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats", "rs_exec_set_stages",
-    "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
+    "rs_plan_placement", "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
 ]
 
 
@@ -72,6 +72,10 @@ class ExecStats_t(C.Structure):
                 ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64)]
 
 
+class PlacementStats_t(C.Structure):
+    _fields_ = [("local_bytes", C.c_int64), ("out_bytes", C.c_int64), ("in_bytes", C.c_int64), ("ops", C.c_int64)]
+
+
 class ArenaStats_t(C.Structure):
     _fields_ = [("physical_bytes", C.c_int64), ("a_bytes", C.c_int64), ("b_bytes", C.c_int64),
                 ("aliased_bytes", C.c_int64), ("chunks", C.c_int64)]
@@ -116,6 +120,7 @@ def lib():
     L.rs_exec_verify.argtypes = [vp, C.c_int, C.c_uint64, vp, P(i64), P(i64)]
     L.rs_exec_stats.argtypes = [vp, P(ExecStats_t)]
     L.rs_exec_set_stages.argtypes = [vp, P(C.c_int), C.c_int]
+    L.rs_plan_placement.argtypes = [vp, C.c_int, C.c_int, P(PlacementStats_t)]
     L.rs_arena_create.argtypes = [vp, vp, C.c_int, i64, i64, C.c_int, P(vp)]
     L.rs_arena_destroy.argtypes = [vp]
     L.rs_arena_buffer.argtypes = [vp, C.c_int, C.c_int, C.c_int, P(vp), P(i64)]

@@ -69,6 +69,12 @@ class RoutingPlan:
         A.check(A.lib().rs_plan_regions(self.h, side, C.byref(p), C.byref(n)))
         return A.take_string(p, n)
 
+    def placement(self, n_gpus: int, gpu: int) -> A.PlacementStats_t:
+        """Bytes GPU `gpu` copies locally / pushes to peers / receives (host-side)."""
+        s = A.PlacementStats_t()
+        A.check(A.lib().rs_plan_placement(self.h, n_gpus, gpu, C.byref(s)))
+        return s
+
     def transfers(self, device: int = -1) -> List[A.Transfer_t]:
         p, n = C.c_void_p(), C.c_int64()
         A.check(A.lib().rs_plan_transfers(self.h, device, C.byref(p), C.byref(n)))

@@ -359,6 +359,18 @@ int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64
     });
 }
 
+int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out) {
+    return guarded([&] {
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad placement");
+        const exec::PlacementStats s = exec::placement_stats(p->core, n_gpus, gpu);
+        out->local_bytes = s.local_bytes;
+        out->out_bytes = s.out_bytes;
+        out->in_bytes = s.in_bytes;
+        out->ops = s.ops;
+        return RS_OK;
+    });
+}
+
 int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len) {
     return guarded([&] {
         const ModelSpace& space = *p->core.space;

@@ -157,6 +157,26 @@ std::vector<CopyOp> build_ops(const PlanCore& P) {
     return ops;
 }
 
+PlacementStats placement_stats(const PlanCore& P, int n_gpus, int gpu) {
+    int max_phys = 0;
+    for (const auto& r : P.routes) max_phys = std::max(max_phys, r.phys);
+    const int per = (max_phys + 1 + n_gpus - 1) / n_gpus;
+    auto gpu_src = [&](int rank) { return P.wm.src_phys[static_cast<size_t>(rank)] / per; };
+    auto gpu_dst = [&](int rank) { return P.wm.dst_phys[static_cast<size_t>(rank)] / per; };
+    PlacementStats s;
+    for (const CopyOp& op : build_ops(P)) {
+        const std::int64_t b = op.rows * op.row_bytes;
+        const int gs = gpu_src(op.src_side_rank), gd = gpu_dst(op.dst_rank);
+        if (gs == gpu) {
+            ++s.ops;
+            (gd == gpu ? s.local_bytes : s.out_bytes) += b;
+        } else if (gd == gpu) {
+            s.in_bytes += b;
+        }
+    }
+    return s;
+}
+
 void buffer_sizes(const PlanCore& P, int side, int rank, bool with_grads, std::int64_t out[kNumBufs]) {
     const RankGeom& g = (side == 0 ? P.src : P.dst).ranks[static_cast<size_t>(rank)];
     out[kParam] = g.param_bytes;

@@ -46,6 +46,13 @@ struct FillTask {
 /// Build every CopyOp of the transition (all GPUs), grouped by nothing.
 std::vector<CopyOp> build_ops(const core::PlanCore& P);
 
+/// Byte accounting of one GPU under contiguous-block placement (host only): what it
+/// copies locally, pushes to peers (out) and receives from peers (in).
+struct PlacementStats {
+    std::int64_t local_bytes = 0, out_bytes = 0, in_bytes = 0, ops = 0;
+};
+PlacementStats placement_stats(const core::PlanCore& P, int n_gpus, int gpu);
+
 /// Buffer sizes of a rank (bytes) for one side.
 void buffer_sizes(const core::PlanCore& P, int side, int rank, bool with_grads, std::int64_t out[kNumBufs]);
 

@@ -1,0 +1,74 @@
+"""Multi-GPU correctness (run under torchrun, one process per GPU, NCCL plumbing):
+push-model transition over cudaIpc-mapped peer HBM, bit-exact on every GPU.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_check.py [layers]
+"""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+
+
+def main():
+    layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seed = 0xBEEF
+    failures = 0
+    scenarios = [S.config2(layers), S.config4(1), S.config3(2)[0], S.config3(2)[1]]
+    for sc in scenarios:
+        ab = RoutingPlan.from_scenario(sc)
+        ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+        fwd = Transition(ab, world, rank, local, alloc=False)
+        bwd = Transition(ba, world, rank, local, alloc=False)
+        keep = []
+        for side_ab in (A.SIDE_SRC, A.SIDE_DST):
+            nr = ab.summary.src_world if side_ab == A.SIDE_SRC else ab.summary.dst_world
+            for r in range(nr):
+                for b in range(6):
+                    _, n, g = fwd.ex.buffer(side_ab, r, b)
+                    if n and g == rank:
+                        t = torch.zeros(n, dtype=torch.uint8, device="cuda")
+                        keep.append(t)
+                        fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
+                        bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
+        fwd.connect()
+        bwd.connect()
+        fwd.ex.fill(A.SIDE_SRC, seed)
+        torch.cuda.synchronize()
+        dist.barrier()
+        fwd.run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
+        bwd.run()
+        torch.cuda.synchronize()
+        dist.barrier()
+        bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
+        st = fwd.ex.stats()
+        print(f"[rank {rank}] {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+              f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
+        failures += int(bad_a != 0) + int(bad_b != 0)
+        del fwd, bwd, keep
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([failures], device="cuda")
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    if rank == 0:
+        print("MGPU_OK" if t.item() == 0 else f"MGPU_FAIL {t.item()}", flush=True)
+    sys.exit(0 if t.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()
