@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -28,6 +29,9 @@ namespace exec {
 
 constexpr int kThreads = 512;
 constexpr int kUnroll = 4;
+constexpr int kBulkStages = 4;        // smem stages per CTA
+constexpr int kBulkStage = 32 << 10;  // bytes per stage
+constexpr int kBulkCtasPerSm = 1;
 
 template <int V>
 struct VecT;
@@ -95,6 +99,107 @@ __global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __rest
             }
         }
     }
+}
+
+// ---- TMA bulk-copy pipeline (cp.async.bulk global -> smem -> global), 16-B class
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive_expect(std::uint64_t* b, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n RS_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra RS_WAIT_%=;\n}" ::"r"(
+            smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* s, const void* g, std::uint32_t bytes, std::uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(s)),
+                 "l"(g), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* g, const void* s, std::uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(s)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+struct BulkStage {
+    std::uint64_t dst;    // first row's destination
+    std::uint64_t pitch;  // destination pitch
+    std::uint32_t rows, bytes;
+};
+
+/// One warp per CTA streams its tiles through S shared-memory stages of kStage
+/// bytes: a stage holds up to kStage/row_bytes rows of one tile (or a piece of one
+/// long row). Per iteration c: wait stage c's loads (mbarrier tx count), issue its
+/// bulk stores, then refill the slot freed by stage c-1 once those stores have read
+/// it (wait_group.read 1), keeping S-1 stages of loads in flight. Every lane commits
+/// one bulk group per stage so the per-thread group counts stay in lockstep.
+template <int S, int kStage>
+__global__ void __launch_bounds__(32) bulk_tiles_kernel(const Tile* __restrict__ tiles, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ std::uint64_t bar[S];
+    __shared__ BulkStage rec[S];
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+        for (int i = 0; i < S; ++i) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    int t = blockIdx.x;
+    std::uint32_t row = 0, off = 0;
+    // issue loads for the next stage into slot; false when the CTA has no more work
+    auto load_next = [&](int slot) -> bool {
+        if (t >= ntiles) return false;
+        const Tile tl = tiles[t];
+        std::uint32_t nr, n, r0 = row, o = off;
+        if (tl.row_bytes <= static_cast<std::uint32_t>(kStage)) {
+            nr = min(static_cast<std::uint32_t>(kStage) / tl.row_bytes, tl.rows - row);
+            n = tl.row_bytes;
+            row += nr;
+        } else {
+            nr = 1;
+            n = min(static_cast<std::uint32_t>(kStage), tl.row_bytes - off);
+            off += n;
+            if (off == tl.row_bytes) off = 0, ++row;
+        }
+        if (row == tl.rows) row = 0, off = 0, t += gridDim.x;
+        if (lane == 0) {
+            rec[slot] = BulkStage{tl.dst + r0 * tl.dst_pitch + o, tl.dst_pitch, nr, n};
+            mbar_arrive_expect(&bar[slot], nr * n);
+        }
+        __syncwarp();
+        unsigned char* buf = smem + slot * kStage;
+        for (std::uint32_t r = lane; r < nr; r += 32)
+            bulk_load(buf + r * n, reinterpret_cast<const void*>(tl.src + (r0 + r) * tl.src_pitch + o), n, &bar[slot]);
+        return true;
+    };
+    int issued = 0;
+    while (issued < S - 1 && load_next(issued % S)) ++issued;
+    std::uint32_t parity = 0;  // bit s: parity to wait for on slot s
+    for (int c = 0; c < issued; ++c) {
+        const int slot = c % S;
+        mbar_wait(&bar[slot], (parity >> slot) & 1u);
+        parity ^= 1u << slot;
+        const BulkStage st = rec[slot];
+        const unsigned char* buf = smem + slot * kStage;
+        for (std::uint32_t r = lane; r < st.rows; r += 32)
+            bulk_store(reinterpret_cast<void*>(st.dst + r * st.pitch), buf + r * st.bytes, st.bytes);
+        bulk_commit();
+        // slot (c+S-1) % S held stage c-1, whose stores were the previous group
+        bulk_wait_read1();
+        __syncwarp();
+        if (load_next((c + S - 1) % S)) ++issued;
+    }
+    bulk_wait_all();
 }
 
 /// value of element with global flat index k for buffer kind
@@ -431,6 +536,11 @@ void Executor::prepare() {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device);
     sms_ = sms;
+    const char* kern = std::getenv("RS_COPY_KERNEL");
+    use_bulk_ = !(kern && std::string(kern) == "vector");
+    if (use_bulk_)
+        RS_CUDA(cudaFuncSetAttribute(bulk_tiles_kernel<kBulkStages, kBulkStage>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkStage));
     prepared_ = true;
 }
 
@@ -445,7 +555,14 @@ int Executor::run(cudaStream_t stream) {
         const int grid = std::min(n, grid_cap);
         const Tile* t = base + g.begin;
         switch (g.cls) {
-            case 0: copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n); break;
+            case 0:
+                if (use_bulk_) {
+                    const int g2 = std::min(n, sms_ * kBulkCtasPerSm);
+                    bulk_tiles_kernel<kBulkStages, kBulkStage><<<g2, 32, kBulkStages * kBulkStage, stream>>>(t, n);
+                } else {
+                    copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n);
+                }
+                break;
             case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n); break;
             case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n); break;
             case 3: copy_tiles_kernel<2><<<grid, kThreads, 0, stream>>>(t, n); break;

@@ -102,6 +102,7 @@ private:
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;
     bool prepared_ = false;
+    bool use_bulk_ = true;  // TMA bulk pipeline for 16-byte-class tiles (RS_COPY_KERNEL=vector to disable)
     ExecStats stats_;
 };
 
