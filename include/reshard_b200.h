@@ -145,6 +145,40 @@ int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stat
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
 
+/* ---- transition schedule: Algorithm 1 */
+typedef struct rs_schedule rs_schedule_t;
+typedef struct {
+    int num_devices;       /* N = participants */
+    int num_stages;
+    int num_collectives;
+    int num_steps;         /* steps with traffic */
+    int64_t budget;        /* M_global_min = min(mem_avail) */
+    int64_t p2p_bytes, collective_bytes;
+    int64_t num_fragments;
+} rs_schedule_summary_t;
+#define RS_COMM_P2P 0
+#define RS_COMM_BROADCAST 1
+#define RS_COMM_SCATTER 2
+#define RS_COMM_GATHER 3
+/* xor_schedule: peer of device i at step s, or -1 */
+int rs_xor_peer(int i, int s, int n);
+/* MemoryAwareChunk: stage index per step (steps ascending, cost[k]
+ * for steps[k]); RS_ERR_BUDGET if one step exceeds min(mem_avail) */
+int rs_memory_aware_chunk(const int* steps, const int64_t* cost, int n_steps, const int64_t* mem_avail, int n_ranks,
+                          int* stage_of_step, int64_t* budget);
+/* build_schedule. mem_avail: per device (NULL = unbounded). */
+int rs_schedule_build(const rs_plan_t* p, const int64_t* mem_avail, int n, int promote, rs_schedule_t** out);
+void rs_schedule_destroy(rs_schedule_t* s);
+int rs_schedule_summary(const rs_schedule_t* s, rs_schedule_summary_t* out);
+/* stage k: its steps and mem_cost */
+int rs_schedule_stage(const rs_schedule_t* s, int k, int* steps, int cap, int* n, int64_t* mem_cost);
+/* device dev in stage k, step index q: peer (-1 inactive) and buffer sizes */
+int rs_schedule_peer(const rs_schedule_t* s, int k, int q, int dev, int* peer, int64_t* send_bytes, int64_t* recv_bytes);
+/* collective c: kind, root, bytes, participants */
+int rs_schedule_collective(const rs_schedule_t* s, int c, int* kind, int* root, int64_t* bytes, int* participants, int cap,
+                           int* n);
+int rs_schedule_dump(const rs_schedule_t* s, char** out, size_t* len);
+
 /* ---- executor: Algorithm 1 ExecuteSwitch / SPEC execute
  * (SPEC.md:375-383), push model over NVLink. One rs_exec_t per GPU/process. */
 typedef struct {

@@ -21,7 +21,9 @@ EXPORTED = [
     "rs_plan_regions", "rs_plan_dump_rows_host", "rs_exec_create", "rs_exec_destroy", "rs_exec_alloc",
     "rs_exec_bind", "rs_exec_buffer", "rs_exec_ipc_export", "rs_exec_ipc_import", "rs_exec_prepare",
     "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats", "rs_exec_set_stages",
-    "rs_plan_placement", "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
+    "rs_plan_placement", "rs_xor_peer", "rs_memory_aware_chunk", "rs_schedule_build", "rs_schedule_destroy",
+    "rs_schedule_summary", "rs_schedule_stage", "rs_schedule_peer", "rs_schedule_collective", "rs_schedule_dump",
+    "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
 ]
 
 
@@ -76,6 +78,12 @@ class PlacementStats_t(C.Structure):
     _fields_ = [("local_bytes", C.c_int64), ("out_bytes", C.c_int64), ("in_bytes", C.c_int64), ("ops", C.c_int64)]
 
 
+class ScheduleSummary_t(C.Structure):
+    _fields_ = [("num_devices", C.c_int), ("num_stages", C.c_int), ("num_collectives", C.c_int), ("num_steps", C.c_int),
+                ("budget", C.c_int64), ("p2p_bytes", C.c_int64), ("collective_bytes", C.c_int64),
+                ("num_fragments", C.c_int64)]
+
+
 class ArenaStats_t(C.Structure):
     _fields_ = [("physical_bytes", C.c_int64), ("a_bytes", C.c_int64), ("b_bytes", C.c_int64),
                 ("aliased_bytes", C.c_int64), ("chunks", C.c_int64)]
@@ -121,6 +129,15 @@ def lib():
     L.rs_exec_stats.argtypes = [vp, P(ExecStats_t)]
     L.rs_exec_set_stages.argtypes = [vp, P(C.c_int), C.c_int]
     L.rs_plan_placement.argtypes = [vp, C.c_int, C.c_int, P(PlacementStats_t)]
+    L.rs_xor_peer.argtypes = [C.c_int, C.c_int, C.c_int]
+    L.rs_memory_aware_chunk.argtypes = [P(C.c_int), P(i64), C.c_int, P(i64), C.c_int, P(C.c_int), P(i64)]
+    L.rs_schedule_build.argtypes = [vp, P(i64), C.c_int, C.c_int, P(vp)]
+    L.rs_schedule_destroy.argtypes = [vp]
+    L.rs_schedule_summary.argtypes = [vp, P(ScheduleSummary_t)]
+    L.rs_schedule_stage.argtypes = [vp, C.c_int, P(C.c_int), C.c_int, P(C.c_int), P(i64)]
+    L.rs_schedule_peer.argtypes = [vp, C.c_int, C.c_int, C.c_int, P(C.c_int), P(i64), P(i64)]
+    L.rs_schedule_collective.argtypes = [vp, C.c_int, P(C.c_int), P(C.c_int), P(i64), P(C.c_int), C.c_int, P(C.c_int)]
+    L.rs_schedule_dump.argtypes = [vp, P(vp), P(sz)]
     L.rs_arena_create.argtypes = [vp, vp, C.c_int, i64, i64, C.c_int, P(vp)]
     L.rs_arena_destroy.argtypes = [vp]
     L.rs_arena_buffer.argtypes = [vp, C.c_int, C.c_int, C.c_int, P(vp), P(i64)]
@@ -129,7 +146,7 @@ def lib():
     for name in EXPORTED:
         fn = getattr(L, name)
         if fn.restype is None and name not in ("rs_free", "rs_model_destroy", "rs_plan_destroy", "rs_exec_destroy",
-                                                      "rs_arena_destroy"):
+                                                      "rs_arena_destroy", "rs_schedule_destroy"):
             fn.restype = C.c_int
     _lib = L
     return L

@@ -240,3 +240,78 @@ class Arena:
         fwd.set_stages(self.stage_order(0))
         if bwd is not None:
             bwd.set_stages(self.stage_order(1))
+
+
+def xor_peer(i: int, s: int, n: int) -> int:
+    """Peer(i, s) = i XOR s, or -1 when outside the device set."""
+    return A.lib().rs_xor_peer(i, s, n)
+
+
+def memory_aware_chunk(steps: Sequence[int], costs: Sequence[int], mem_avail: Sequence[int]):
+    """MemoryAwareChunk: returns (stages as lists of steps, budget)."""
+    n = len(steps)
+    st = (C.c_int * max(1, n))(*steps)
+    co = (C.c_int64 * max(1, n))(*costs)
+    av = (C.c_int64 * max(1, len(mem_avail)))(*mem_avail)
+    out = (C.c_int * max(1, n))()
+    budget = C.c_int64()
+    A.check(A.lib().rs_memory_aware_chunk(st, co, n, av, len(mem_avail), out, C.byref(budget)))
+    stages: List[List[int]] = []
+    for k in range(n):
+        g = out[k]
+        while len(stages) <= g:
+            stages.append([])
+        stages[g].append(steps[k])
+    return stages, budget.value
+
+
+class Schedule:
+    """build_schedule over a RoutingPlan."""
+
+    KINDS = {0: "p2p", 1: "broadcast", 2: "scatter", 3: "gather"}
+
+    def __init__(self, plan: RoutingPlan, mem_avail: Optional[Sequence[int]] = None, promote: bool = True):
+        h = C.c_void_p()
+        av = (C.c_int64 * max(1, len(mem_avail)))(*mem_avail) if mem_avail else None
+        A.check(A.lib().rs_schedule_build(plan.h, av, len(mem_avail) if mem_avail else 0, int(promote), C.byref(h)))
+        self.h = h.value
+        self.plan = plan
+        s = A.ScheduleSummary_t()
+        A.check(A.lib().rs_schedule_summary(self.h, C.byref(s)))
+        self.summary = s
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            A.lib().rs_schedule_destroy(self.h)
+            self.h = None
+
+    def stages(self):
+        out = []
+        for k in range(self.summary.num_stages):
+            steps = (C.c_int * 4096)()
+            n, cost = C.c_int(), C.c_int64()
+            A.check(A.lib().rs_schedule_stage(self.h, k, steps, 4096, C.byref(n), C.byref(cost)))
+            out.append((list(steps[: n.value]), cost.value))
+        return out
+
+    def peer(self, stage: int, q: int, dev: int):
+        p, sb, rb = C.c_int(), C.c_int64(), C.c_int64()
+        A.check(A.lib().rs_schedule_peer(self.h, stage, q, dev, C.byref(p), C.byref(sb), C.byref(rb)))
+        return p.value, sb.value, rb.value
+
+    def collectives(self):
+        out = []
+        for c in range(self.summary.num_collectives):
+            kind, root, n = C.c_int(), C.c_int(), C.c_int()
+            b = C.c_int64()
+            parts = (C.c_int * 4096)()
+            A.check(A.lib().rs_schedule_collective(self.h, c, C.byref(kind), C.byref(root), C.byref(b), parts, 4096,
+                                                   C.byref(n)))
+            out.append({"kind": self.KINDS[kind.value], "root": root.value, "bytes": b.value,
+                        "participants": list(parts[: n.value])})
+        return out
+
+    def dump(self) -> str:
+        p, n = C.c_void_p(), C.c_size_t()
+        A.check(A.lib().rs_schedule_dump(self.h, C.byref(p), C.byref(n)))
+        return A.take_string(p, n)

@@ -14,6 +14,7 @@
 #include "reshard/arena.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
+#include "reshard/schedule.hpp"
 
 namespace reshard {
 namespace gpuplan {
@@ -32,6 +33,11 @@ struct rs_plan {
     std::shared_ptr<rs_model> owned;  // set when created from scenario text
     const rs_model* model = nullptr;
     core::PlanCore core;
+};
+
+struct rs_schedule {
+    const rs_plan* plan = nullptr;
+    sched::TransitionSchedule T;
 };
 
 struct rs_arena {
@@ -392,6 +398,100 @@ int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len) {
                     s += strfmt("rank %d optim %s\n", r, format_interval(iv).c_str());
         }
         *out = dup_string(s, len);
+        return RS_OK;
+    });
+}
+
+int rs_xor_peer(int i, int s, int n) { return sched::xor_peer(i, s, n); }
+
+int rs_memory_aware_chunk(const int* steps, const int64_t* cost, int n_steps, const int64_t* mem_avail, int n_ranks,
+                          int* stage_of_step, int64_t* budget) {
+    return guarded([&] {
+        std::vector<int> st(steps, steps + n_steps);
+        int maxs = 0;
+        for (int x : st) maxs = std::max(maxs, x);
+        std::vector<std::int64_t> c(static_cast<size_t>(maxs) + 1, 0);
+        for (int k = 0; k < n_steps; ++k) c[static_cast<size_t>(steps[k])] = cost[k];
+        std::int64_t M = 0;
+        const auto stages = sched::memory_aware_chunk(st, c, std::vector<std::int64_t>(mem_avail, mem_avail + n_ranks), &M);
+        for (size_t g = 0; g < stages.size(); ++g)
+            for (int x : stages[g])
+                for (int k = 0; k < n_steps; ++k)
+                    if (steps[k] == x) stage_of_step[k] = static_cast<int>(g);
+        if (budget) *budget = M;
+        return RS_OK;
+    });
+}
+
+int rs_schedule_build(const rs_plan_t* p, const int64_t* mem_avail, int n, int promote, rs_schedule_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto s = std::make_unique<rs_schedule>();
+        s->plan = p;
+        std::vector<std::int64_t> avail;
+        if (mem_avail) avail.assign(mem_avail, mem_avail + n);
+        s->T = sched::build_schedule(p->core, core::expand_flat_host(p->core), avail, promote != 0);
+        *out = s.release();
+        return RS_OK;
+    });
+}
+
+void rs_schedule_destroy(rs_schedule_t* s) { delete s; }
+
+int rs_schedule_summary(const rs_schedule_t* s, rs_schedule_summary_t* out) {
+    return guarded([&] {
+        const sched::TransitionSchedule& T = s->T;
+        std::memset(out, 0, sizeof *out);
+        out->num_devices = T.N;
+        out->num_stages = static_cast<int>(T.stages.size());
+        out->num_collectives = static_cast<int>(T.collectives.size());
+        for (const auto& st : T.stages) out->num_steps += static_cast<int>(st.steps.size());
+        out->budget = T.budget;
+        std::int64_t total = 0;
+        for (const auto& f : T.frags) total += f.bytes;
+        for (const auto& c : T.collectives) out->collective_bytes += c.bytes;
+        out->p2p_bytes = total - out->collective_bytes;
+        out->num_fragments = static_cast<int64_t>(T.frags.size());
+        return RS_OK;
+    });
+}
+
+int rs_schedule_stage(const rs_schedule_t* s, int k, int* steps, int cap, int* n, int64_t* mem_cost) {
+    return guarded([&] {
+        const auto& st = s->T.stages.at(static_cast<size_t>(k));
+        *n = static_cast<int>(st.steps.size());
+        for (int i = 0; i < *n && i < cap; ++i) steps[i] = st.steps[static_cast<size_t>(i)];
+        if (mem_cost) *mem_cost = st.mem_cost;
+        return RS_OK;
+    });
+}
+
+int rs_schedule_peer(const rs_schedule_t* s, int k, int q, int dev, int* peer, int64_t* send_bytes, int64_t* recv_bytes) {
+    return guarded([&] {
+        const auto& rs = s->T.stages.at(static_cast<size_t>(k)).ranks.at(static_cast<size_t>(dev)).at(static_cast<size_t>(q));
+        *peer = rs.peer;
+        *send_bytes = rs.send.bytes;
+        *recv_bytes = rs.recv.bytes;
+        return RS_OK;
+    });
+}
+
+int rs_schedule_collective(const rs_schedule_t* s, int c, int* kind, int* root, int64_t* bytes, int* participants, int cap,
+                           int* n) {
+    return guarded([&] {
+        const auto& op = s->T.collectives.at(static_cast<size_t>(c));
+        *kind = static_cast<int>(op.kind);
+        *root = op.root;
+        *bytes = op.bytes;
+        *n = static_cast<int>(op.participants.size());
+        for (int i = 0; i < *n && i < cap; ++i) participants[i] = op.participants[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
+int rs_schedule_dump(const rs_schedule_t* s, char** out, size_t* len) {
+    return guarded([&] {
+        *out = dup_string(sched::dump_schedule(s->plan->core, s->T), len);
         return RS_OK;
     });
 }
