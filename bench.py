@@ -209,8 +209,17 @@ def run_ours(args):
                         keep.append(t)
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), nbytes)
                         bwd.ex.bind(side_ba, r, b, t.data_ptr(), nbytes)
-    fwd.connect()
-    bwd.connect()
+    if args.transport == "nccl" and n > 1:
+        # Algorithm 1 buffered mode over NCCL send/recv: the measured comparison
+        from paper_2605_18815_b200.runtime import StagedTransition
+        fwd_staged = StagedTransition(ab, fwd.ex, n, rank)
+        bwd_staged = StagedTransition(ba, bwd.ex, n, rank)
+        fwd.run, bwd.run = fwd_staged.run, bwd_staged.run
+        reprepare = (fwd.ex.prepare_staged, bwd.ex.prepare_staged)
+    else:
+        fwd.connect()
+        bwd.connect()
+        reprepare = (fwd.ex.prepare, bwd.ex.prepare)
     seed = 0xC0FFEE
     fwd.ex.fill(A.SIDE_SRC, seed)
     stream = torch.cuda.current_stream()
@@ -285,8 +294,8 @@ def run_ours(args):
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        fwd.ex.prepare()
-        bwd.ex.prepare()
+        reprepare[0]()
+        reprepare[1]()
         step()
         torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
@@ -323,6 +332,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u16/u32 payload copy (bf16 params, fp32 master/m/v)",
             "data": "synthetic (canon payloads, bit-exact verified)",
+            "transport": args.transport,
             "config": {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1, round trip per step",
                        "model": "Llama-3-8B", "layers": args.layers, "virtual_ranks": 8,
                        "parallelism": f"tp8 -> dp2xtp4 + zero1 on {n} GPU(s)", "l2": "inputs >> L2 (no flush needed)",
@@ -359,6 +369,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-arena", action="store_true", help="N=1: plain allocations (needs old+new to fit)")
     ap.add_argument("--hbm-cap", type=int, default=0, help="arena physical budget in bytes (0: free HBM - 1 GiB)")
+    ap.add_argument("--transport", default="fused", choices=["fused", "nccl"],
+                    help="fused: one-sided NVLink stores (product); nccl: pack -> NCCL send/recv -> unpack (comparison)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -225,6 +225,14 @@ int rs_exec_buffer(rs_exec_t* e, int side, int rank, int buf, void** dptr, int64
 int rs_exec_ipc_export(rs_exec_t* e, void* out, size_t cap, size_t* len);
 int rs_exec_ipc_import(rs_exec_t* e, const void* blob, size_t len);
 int rs_exec_prepare(rs_exec_t* e);
+/* Algorithm 1 buffered mode (PackData / AsyncSend+Recv / UnpackData):
+ * moves between GPUs go through per-channel contiguous buffers (channel = src phys ->
+ * dst phys; layout derived from the plan, identical on both sides); the transport
+ * (NCCL send/recv, the measured comparison) is the caller's. Same-GPU moves stay fused. */
+int rs_exec_prepare_staged(rs_exec_t* e);
+int rs_exec_channel_bytes(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* bytes);
+int rs_exec_pack(rs_exec_t* e, int src_phys, int dst_phys, void* dbuf, void* stream);
+int rs_exec_unpack(rs_exec_t* e, int src_phys, int dst_phys, const void* dbuf, void* stream);
 /* load_state on this GPU's ranks of one side */
 int rs_exec_fill(rs_exec_t* e, int side, uint64_t seed, void* stream);
 int rs_exec_run(rs_exec_t* e, void* stream, int* launches);

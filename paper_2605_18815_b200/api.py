@@ -315,3 +315,27 @@ class Schedule:
         p, n = C.c_void_p(), C.c_size_t()
         A.check(A.lib().rs_schedule_dump(self.h, C.byref(p), C.byref(n)))
         return A.take_string(p, n)
+
+
+def _exec_staged_methods():
+    def prepare_staged(self) -> None:
+        A.check(A.lib().rs_exec_prepare_staged(self.h))
+
+    def channel_bytes(self, src_phys: int, dst_phys: int) -> int:
+        n = C.c_int64()
+        A.check(A.lib().rs_exec_channel_bytes(self.h, src_phys, dst_phys, C.byref(n)))
+        return n.value
+
+    def pack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_pack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
+
+    def unpack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_unpack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
+
+    Executor.prepare_staged = prepare_staged
+    Executor.channel_bytes = channel_bytes
+    Executor.pack = pack
+    Executor.unpack = unpack
+
+
+_exec_staged_methods()

@@ -572,6 +572,34 @@ int rs_exec_prepare(rs_exec_t* e) {
     });
 }
 
+int rs_exec_prepare_staged(rs_exec_t* e) {
+    return guarded([&] {
+        e->ex->prepare(true);
+        return RS_OK;
+    });
+}
+
+int rs_exec_channel_bytes(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* bytes) {
+    return guarded([&] {
+        *bytes = e->ex->channel_bytes(src_phys, dst_phys);
+        return RS_OK;
+    });
+}
+
+int rs_exec_pack(rs_exec_t* e, int src_phys, int dst_phys, void* dbuf, void* stream) {
+    return guarded([&] {
+        e->ex->pack(src_phys, dst_phys, dbuf, static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
+int rs_exec_unpack(rs_exec_t* e, int src_phys, int dst_phys, const void* dbuf, void* stream) {
+    return guarded([&] {
+        e->ex->unpack(src_phys, dst_phys, dbuf, static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
 int rs_exec_fill(rs_exec_t* e, int side, uint64_t seed, void* stream) {
     return guarded([&] {
         e->ex->fill(side, seed, static_cast<cudaStream_t>(stream));

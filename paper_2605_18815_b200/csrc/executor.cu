@@ -61,10 +61,13 @@ __device__ __forceinline__ uint4 ld_stream<uint4>(const uint4* p) {
 /// multiples of V). Persistent grid: CTA b takes tiles b, b+grid, ... Each thread
 /// keeps kUnroll independent loads in flight before storing.
 template <int V>
-__global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles) {
+__global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles, std::uint64_t sbase,
+                                                              std::uint64_t dbase) {
     using T = typename VecT<V>::T;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const Tile tl = tiles[ti];
+        Tile tl = tiles[ti];
+        tl.src += sbase;
+        tl.dst += dbase;
         const unsigned vpr = tl.row_bytes / V;
         if (tl.rows == 1) {
             const T* __restrict__ s = reinterpret_cast<const T*>(tl.src);
@@ -144,7 +147,8 @@ struct BulkStage {
 /// it (wait_group.read 1), keeping S-1 stages of loads in flight. Every lane commits
 /// one bulk group per stage so the per-thread group counts stay in lockstep.
 template <int S, int kStage>
-__global__ void __launch_bounds__(32) bulk_tiles_kernel(const Tile* __restrict__ tiles, int ntiles) {
+__global__ void __launch_bounds__(32) bulk_tiles_kernel(const Tile* __restrict__ tiles, int ntiles, std::uint64_t sbase,
+                                                      std::uint64_t dbase) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ std::uint64_t bar[S];
     __shared__ BulkStage rec[S];
@@ -159,7 +163,9 @@ __global__ void __launch_bounds__(32) bulk_tiles_kernel(const Tile* __restrict__
     // issue loads for the next stage into slot; false when the CTA has no more work
     auto load_next = [&](int slot) -> bool {
         if (t >= ntiles) return false;
-        const Tile tl = tiles[t];
+        Tile tl = tiles[t];
+        tl.src += sbase;
+        tl.dst += dbase;
         std::uint32_t nr, n, r0 = row, o = off;
         if (tl.row_bytes <= static_cast<std::uint32_t>(kStage)) {
             nr = min(static_cast<std::uint32_t>(kStage) / tl.row_bytes, tl.rows - row);
@@ -334,7 +340,6 @@ Executor::~Executor() {
     cudaSetDevice(cfg_.device);
     for (void* p : ipc_opened_) cudaIpcCloseMemHandle(p);
     for (void* p : owned_) cudaFree(p);
-    if (d_tiles_) cudaFree(d_tiles_);
     if (d_fill_) cudaFree(d_fill_);
     if (d_counters_) cudaFree(d_counters_);
 }
@@ -450,87 +455,164 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
     }
 }
 
-void Executor::prepare() {
+void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
+                  std::int64_t dp, std::int64_t kTile) {
+    if (rows <= 0 || rb <= 0) return;
+    if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
+        rb *= rows;
+        rows = 1;
+    }
+    if (static_cast<int>(buckets.size()) < (key + 1) * 5) buckets.resize(static_cast<size_t>(key + 1) * 5);
+    auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
+        Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
+               static_cast<std::uint32_t>(nb)};
+        std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
+        if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
+        buckets[static_cast<size_t>(key) * 5 + class_index(align_class(a))].push_back(t);
+    };
+    if (rows == 1 || rb >= kTile) {
+        for (std::int64_t r = 0; r < rows; ++r) {
+            std::uint64_t s = src + static_cast<std::uint64_t>(r * sp), d = dst + static_cast<std::uint64_t>(r * dp);
+            std::int64_t left = rb;
+            // peel an unaligned head so the body runs 16-byte vectors when both sides
+            // share the same misalignment (relative offsets keep it: bases are 256-B aligned)
+            if ((s % 16) == (d % 16) && (s % 16) != 0) {
+                const std::int64_t head = std::min<std::int64_t>(left, 16 - static_cast<std::int64_t>(s % 16));
+                emit(s, d, 1, head);
+                s += static_cast<std::uint64_t>(head);
+                d += static_cast<std::uint64_t>(head);
+                left -= head;
+            }
+            while (left > 0) {
+                const std::int64_t n = std::min(left, kTile);
+                const bool aligned = (s % 16) == 0 && (d % 16) == 0;
+                const std::int64_t body = (aligned && n > 16) ? n - n % 16 : n;
+                emit(s, d, 1, body);
+                s += static_cast<std::uint64_t>(body);
+                d += static_cast<std::uint64_t>(body);
+                left -= body;
+            }
+        }
+    } else {
+        const std::int64_t per = std::max<std::int64_t>(1, kTile / rb);
+        for (std::int64_t r = 0; r < rows; r += per) {
+            const std::int64_t nr = std::min(per, rows - r);
+            emit(src + static_cast<std::uint64_t>(r * sp), dst + static_cast<std::uint64_t>(r * dp), nr, rb);
+        }
+    }
+}
+
+void TileSet::finalize(ExecStats* stats) {
+    host.clear();
+    groups.clear();
+    for (size_t b = 0; b < buckets.size(); ++b) {
+        const auto& v = buckets[b];
+        if (v.empty()) continue;
+        const int c = static_cast<int>(b % 5);
+        groups.push_back({c, static_cast<int>(host.size()), static_cast<int>(v.size())});
+        host.insert(host.end(), v.begin(), v.end());
+        if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(v.size());
+    }
+    buckets.clear();
+    if (dev) cudaFree(dev);
+    dev = nullptr;
+    if (!host.empty()) {
+        RS_CUDA(cudaMalloc(&dev, host.size() * sizeof(Tile)));
+        RS_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+    }
+    if (stats) {
+        stats->tiles += static_cast<std::int64_t>(host.size());
+        stats->launches += static_cast<std::int64_t>(groups.size());
+    }
+}
+
+TileSet::~TileSet() {
+    if (dev) cudaFree(dev);
+}
+
+int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm,
+                    bool bulk) const {
+    int launches = 0;
+    const int grid_cap = sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
+    const Tile* base = static_cast<const Tile*>(dev);
+    for (const Group& g : groups) {
+        const int n = g.count;
+        const int grid = std::min(n, grid_cap);
+        const Tile* t = base + g.begin;
+        switch (g.cls) {
+            case 0:
+                if (bulk) {
+                    const int g2 = std::min(n, sms * kBulkCtasPerSm);
+                    bulk_tiles_kernel<kBulkStages, kBulkStage><<<g2, 32, kBulkStages * kBulkStage, stream>>>(t, n, sbase, dbase);
+                } else {
+                    copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase);
+                }
+                break;
+            case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            case 3: copy_tiles_kernel<2><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            default: copy_tiles_kernel<1><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+        }
+        ++launches;
+    }
+    RS_CUDA(cudaGetLastError());
+    return launches;
+}
+
+void Executor::prepare(bool staged) {
     RS_CUDA(cudaSetDevice(cfg_.device));
     const std::vector<CopyOp> ops = build_ops(P_);
-    const int nstage = stage_of_dst_.empty() ? 1 : *std::max_element(stage_of_dst_.begin(), stage_of_dst_.end()) + 1;
-    std::vector<std::vector<Tile>> cls(static_cast<size_t>(nstage) * 5);
     stats_ = ExecStats{};
+    staged_ = staged;
+    channels_.clear();
+    fused_ = std::make_unique<TileSet>();
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
+    std::map<std::pair<int, int>, std::int64_t> chan_off;
     for (const CopyOp& op : ops) {
         const RankBufs& S = bufs_[0][static_cast<size_t>(op.src_side_rank)];
-        if (S.gpu != cfg_.gpu) continue;  // pushed by the source's GPU
         const RankBufs& D = bufs_[1][static_cast<size_t>(op.dst_rank)];
         if (op.rows <= 0 || op.row_bytes <= 0) continue;
+        const bool src_here = S.gpu == cfg_.gpu, dst_here = D.gpu == cfg_.gpu;
+        const std::int64_t total = op.rows * op.row_bytes;
+        if (staged && S.gpu != D.gpu) {
+            // channel between physical devices: ops packed densely in build_ops order,
+            // so sender and receiver derive identical offsets without metadata
+            const int sp = P_.wm.src_phys[static_cast<size_t>(op.src_side_rank)];
+            const int dpp = P_.wm.dst_phys[static_cast<size_t>(op.dst_rank)];
+            const auto key = std::make_pair(sp, dpp);
+            std::int64_t& off = chan_off[key];
+            Channel& ch = channels_[key];
+            if (!ch.pack) ch.pack = std::make_unique<TileSet>(), ch.unpack = std::make_unique<TileSet>();
+            if (src_here) {
+                if (!S.ptr[op.src_buf]) throw ConfigError("prepare: source buffer not bound");
+                ch.pack->add(0, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+                             static_cast<std::uint64_t>(off), op.rows, op.row_bytes, op.src_pitch, op.row_bytes, kTile);
+                stats_.remote_bytes += total;
+            }
+            if (dst_here) {
+                if (!D.ptr[op.dst_buf]) throw ConfigError("prepare: destination buffer not bound");
+                ch.unpack->add(0, static_cast<std::uint64_t>(off),
+                               reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off),
+                               op.rows, op.row_bytes, op.row_bytes, op.dst_pitch, kTile);
+            }
+            off += total;
+            ch.bytes = off;
+            continue;
+        }
+        if (!src_here) continue;  // pushed by the source's GPU
         if (!S.ptr[op.src_buf] || !D.ptr[op.dst_buf])
             throw ConfigError(strfmt("prepare: buffer not bound (src rank %d buf %d -> dst rank %d buf %d)",
                                      op.src_side_rank, op.src_buf, op.dst_rank, op.dst_buf));
-        const bool remote = D.gpu != cfg_.gpu;
-        const std::int64_t total = op.rows * op.row_bytes;
-        (remote ? stats_.remote_bytes : stats_.local_bytes) += total;
-        std::uint64_t src = reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off);
-        std::uint64_t dst = reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off);
-        std::int64_t rows = op.rows, rb = op.row_bytes, sp = op.src_pitch, dp = op.dst_pitch;
-        if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
-            rb *= rows;
-            rows = 1;
-        }
+        (dst_here ? stats_.local_bytes : stats_.remote_bytes) += total;
         const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
-        auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
-            Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
-                   static_cast<std::uint32_t>(nb)};
-            std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
-            if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-            cls[static_cast<size_t>(stage) * 5 + class_index(align_class(a))].push_back(t);
-        };
-        if (rows == 1 || rb >= kTile) {
-            for (std::int64_t r = 0; r < rows; ++r) {
-                std::uint64_t s = src + static_cast<std::uint64_t>(r * sp), d = dst + static_cast<std::uint64_t>(r * dp);
-                std::int64_t left = rb;
-                // peel an unaligned head so the body runs 16-byte vectors when both
-                // sides share the same misalignment
-                if ((s % 16) == (d % 16) && (s % 16) != 0) {
-                    const std::int64_t head = std::min<std::int64_t>(left, 16 - static_cast<std::int64_t>(s % 16));
-                    emit(s, d, 1, head);
-                    s += static_cast<std::uint64_t>(head);
-                    d += static_cast<std::uint64_t>(head);
-                    left -= head;
-                }
-                while (left > 0) {
-                    const std::int64_t n = std::min(left, kTile);
-                    const bool aligned = (s % 16) == 0 && (d % 16) == 0;
-                    const std::int64_t body = (aligned && n > 16) ? n - n % 16 : n;
-                    emit(s, d, 1, body);
-                    s += static_cast<std::uint64_t>(body);
-                    d += static_cast<std::uint64_t>(body);
-                    left -= body;
-                }
-            }
-        } else {
-            const std::int64_t per = std::max<std::int64_t>(1, kTile / rb);
-            for (std::int64_t r = 0; r < rows; r += per) {
-                const std::int64_t nr = std::min(per, rows - r);
-                emit(src + static_cast<std::uint64_t>(r * sp), dst + static_cast<std::uint64_t>(r * dp), nr, rb);
-            }
-        }
+        fused_->add(stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+                    reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
+                    op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
     }
-    host_tiles_.clear();
-    groups_.clear();
-    for (int st = 0; st < nstage; ++st)
-        for (int c = 0; c < 5; ++c) {
-            const auto& v = cls[static_cast<size_t>(st) * 5 + c];
-            if (v.empty()) continue;
-            groups_.push_back({c, static_cast<int>(host_tiles_.size()), static_cast<int>(v.size())});
-            host_tiles_.insert(host_tiles_.end(), v.begin(), v.end());
-            stats_.tiles_by_class[c] += static_cast<std::int64_t>(v.size());
-        }
-    stats_.tiles = static_cast<std::int64_t>(host_tiles_.size());
-    stats_.launches = static_cast<std::int64_t>(groups_.size());
-    if (d_tiles_) cudaFree(d_tiles_);
-    d_tiles_ = nullptr;
-    if (!host_tiles_.empty()) {
-        RS_CUDA(cudaMalloc(&d_tiles_, host_tiles_.size() * sizeof(Tile)));
-        RS_CUDA(cudaMemcpy(d_tiles_, host_tiles_.data(), host_tiles_.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+    fused_->finalize(&stats_);
+    for (auto& kv : channels_) {
+        kv.second.pack->finalize(nullptr);
+        kv.second.unpack->finalize(nullptr);
     }
     if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
     int sms = 148;
@@ -547,31 +629,26 @@ void Executor::prepare() {
 int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     RS_CUDA(cudaSetDevice(cfg_.device));
-    int launches = 0;
-    const int grid_cap = sms_ * (cfg_.ctas_per_sm > 0 ? cfg_.ctas_per_sm : 4);
-    const Tile* base = static_cast<const Tile*>(d_tiles_);
-    for (const Group& g : groups_) {
-        const int n = g.count;
-        const int grid = std::min(n, grid_cap);
-        const Tile* t = base + g.begin;
-        switch (g.cls) {
-            case 0:
-                if (use_bulk_) {
-                    const int g2 = std::min(n, sms_ * kBulkCtasPerSm);
-                    bulk_tiles_kernel<kBulkStages, kBulkStage><<<g2, 32, kBulkStages * kBulkStage, stream>>>(t, n);
-                } else {
-                    copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n);
-                }
-                break;
-            case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n); break;
-            case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n); break;
-            case 3: copy_tiles_kernel<2><<<grid, kThreads, 0, stream>>>(t, n); break;
-            default: copy_tiles_kernel<1><<<grid, kThreads, 0, stream>>>(t, n); break;
-        }
-        ++launches;
-    }
-    RS_CUDA(cudaGetLastError());
-    return launches;
+    return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
+}
+
+std::int64_t Executor::channel_bytes(int src_phys, int dst_phys) const {
+    auto it = channels_.find({src_phys, dst_phys});
+    return it == channels_.end() ? 0 : it->second.bytes;
+}
+
+int Executor::pack(int src_phys, int dst_phys, void* buf, cudaStream_t stream) {
+    auto it = channels_.find({src_phys, dst_phys});
+    if (it == channels_.end()) return 0;
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    return it->second.pack->launch(stream, 0, reinterpret_cast<std::uint64_t>(buf), sms_, cfg_.ctas_per_sm, use_bulk_);
+}
+
+int Executor::unpack(int src_phys, int dst_phys, const void* buf, cudaStream_t stream) {
+    auto it = channels_.find({src_phys, dst_phys});
+    if (it == channels_.end()) return 0;
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    return it->second.unpack->launch(stream, reinterpret_cast<std::uint64_t>(buf), 0, sms_, cfg_.ctas_per_sm, use_bulk_);
 }
 
 std::vector<FillTask> Executor::fill_tasks(int side) const {

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -47,6 +48,26 @@ struct RankBufs {
     std::int64_t bytes[kNumBufs] = {0, 0, 0, 0, 0, 0};
 };
 
+/// Device tiles of one launch group set (fused transition, or one channel's
+/// pack / unpack); kernels add runtime base addresses so staging buffers can move.
+struct TileSet {
+    struct Group {
+        int cls, begin, count;
+    };
+    std::vector<std::vector<Tile>> buckets;  // [key * 5 + class] while building
+    std::vector<Tile> host;
+    std::vector<Group> groups;
+    void* dev = nullptr;
+    TileSet() = default;
+    TileSet(const TileSet&) = delete;
+    TileSet& operator=(const TileSet&) = delete;
+    ~TileSet();
+    void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
+             std::int64_t dp, std::int64_t kTile);
+    void finalize(ExecStats* stats);
+    int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk) const;
+};
+
 class Executor {
 public:
     Executor(const core::PlanCore& P, const ExecConfig& cfg);
@@ -69,10 +90,17 @@ public:
     std::vector<std::uint8_t> export_ipc() const;
     void import_ipc(const std::uint8_t* blob, size_t len);
 
-    /// build device tiles for the moves whose source lives here
-    void prepare();
-    /// launch the transition; returns the number of kernel launches
+    /// build device tiles for the moves whose source lives here. staged: moves between
+    /// GPUs go through per-channel pack/unpack (Algorithm 1 buffered mode) instead of
+    /// direct peer stores; only same-GPU moves stay fused.
+    void prepare(bool staged = false);
+    /// launch the transition (fused part); returns the number of kernel launches
     int run(cudaStream_t stream);
+    /// staged mode: bytes of the (src phys -> dst phys) channel, pack into / unpack from
+    /// a contiguous buffer (same layout on both sides, derived from the plan)
+    std::int64_t channel_bytes(int src_phys, int dst_phys) const;
+    int pack(int src_phys, int dst_phys, void* buf, cudaStream_t stream);
+    int unpack(int src_phys, int dst_phys, const void* buf, cudaStream_t stream);
 
     void fill(int side, std::uint64_t seed, cudaStream_t stream);
     std::int64_t verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad);
@@ -92,13 +120,14 @@ private:
     std::vector<void*> owned_;
     std::vector<void*> ipc_opened_;
     std::map<std::string, void*> ipc_map_;
-    struct Group {
-        int cls, begin, count;
+    struct Channel {
+        std::unique_ptr<TileSet> pack, unpack;
+        std::int64_t bytes = 0;
     };
-    std::vector<Tile> host_tiles_;
-    std::vector<Group> groups_;
+    std::unique_ptr<TileSet> fused_;
+    std::map<std::pair<int, int>, Channel> channels_;
+    bool staged_ = false;
     std::vector<int> stage_of_dst_;
-    void* d_tiles_ = nullptr;
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;
     bool prepared_ = false;

@@ -49,6 +49,59 @@ class Transition:
         return self.ex.run(stream)
 
 
+class StagedTransition:
+    """Algorithm 1 buffered execution (ExecuteSwitch) over NCCL: the
+    measured comparison for the fused push path. Per stage of the memory-aware
+    schedule: PackData into one contiguous buffer per (device -> peer) channel,
+    AsyncSend/AsyncRecv as one NCCL group (batch_isend_irecv), then UnpackData.
+    Channels are enumerated in the global (step, device) order on every rank, so
+    NCCL's per-pair FIFO matching pairs them without metadata."""
+
+    def __init__(self, plan: RoutingPlan, ex: Executor, n_gpus: int, gpu: int, mem_avail=None, group=None):
+        from .api import Schedule, xor_peer
+        self.plan, self.ex, self.n_gpus, self.gpu, self.group = plan, ex, n_gpus, gpu, group
+        n = plan.summary.num_participants
+        self.sched = Schedule(plan, mem_avail or [1 << 62] * n, promote=False)
+        ex.prepare_staged()
+        self.phys = list(range(n))  # device index -> phys (identity world maps in the benches)
+        span = (max(self.phys) + 1 + n_gpus - 1) // n_gpus
+        self.gpu_of = [p // span for p in self.phys]
+        self.plan_stages = []
+        for k, (steps, _) in enumerate(self.sched.stages()):
+            chans = []
+            for s in steps:
+                for i in range(n):
+                    p = xor_peer(i, s, n)
+                    if p < 0 or self.gpu_of[i] == self.gpu_of[p]:
+                        continue
+                    nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
+                    if nbytes:
+                        chans.append((self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes))
+            self.plan_stages.append(chans)
+
+    def run(self, stream: int = 0) -> None:
+        import torch
+        import torch.distributed as dist
+        self.ex.run(stream)  # same-GPU moves, fused
+        for chans in self.plan_stages:
+            ops, unpacks, keep = [], [], []
+            for src, dst, gs, gd, nbytes in chans:
+                if gs == self.gpu:
+                    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                    self.ex.pack(src, dst, buf.data_ptr(), stream)
+                    ops.append(dist.P2POp(dist.isend, buf, gd, group=self.group))
+                    keep.append(buf)
+                elif gd == self.gpu:
+                    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                    ops.append(dist.P2POp(dist.irecv, buf, gs, group=self.group))
+                    unpacks.append((src, dst, buf))
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+            for src, dst, buf in unpacks:
+                self.ex.unpack(src, dst, buf.data_ptr(), stream)
+
+
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:
     n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
     return [r for r in range(n) if ex.buffer(side, r, A.BUF_PARAM)[2] == ex.gpu]

@@ -20,6 +20,7 @@ from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
 
 def main():
     layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    staged = "--staged" in sys.argv
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -42,21 +43,27 @@ def main():
                         keep.append(t)
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
                         bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
-        fwd.connect()
-        bwd.connect()
+        if staged:
+            from paper_2605_18815_b200.runtime import StagedTransition
+            fwd_run = StagedTransition(ab, fwd.ex, world, rank).run
+            bwd_run = StagedTransition(ba, bwd.ex, world, rank).run
+        else:
+            fwd.connect()
+            bwd.connect()
+            fwd_run, bwd_run = fwd.run, bwd.run
         fwd.ex.fill(A.SIDE_SRC, seed)
         torch.cuda.synchronize()
         dist.barrier()
-        fwd.run()
+        fwd_run()
         torch.cuda.synchronize()
         dist.barrier()
         bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
-        bwd.run()
+        bwd_run()
         torch.cuda.synchronize()
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'staged' if staged else 'fused'} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep
