@@ -145,6 +145,18 @@ int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stat
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
 
+/* ---- Elastic Device Manager support */
+#define RS_GROUP_DP 0
+#define RS_GROUP_TP 1
+#define RS_GROUP_PP 2
+#define RS_GROUP_EP 3
+#define RS_GROUP_EDP 4
+/* get_or_create_groups' pure derivation: communicator groups of cfg
+ * along one dimension; out[g * group_size + k] = k-th rank of group g. */
+int rs_config_groups(const rs_cfg_t* cfg, int dim, int* out, int cap, int* n_groups, int* group_size);
+/* rank_coord (parallel.hpp:88-106): {pp, dp, tp, ep, edp} */
+int rs_rank_coord(const rs_cfg_t* cfg, int rank, int coord[5]);
+
 /* ---- transition schedule: Algorithm 1 */
 typedef struct rs_schedule rs_schedule_t;
 typedef struct {

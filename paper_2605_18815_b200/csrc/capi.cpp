@@ -402,6 +402,30 @@ int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len) {
     });
 }
 
+int rs_config_groups(const rs_cfg_t* cfg, int dim, int* out, int cap, int* n_groups, int* group_size) {
+    return guarded([&] {
+        if (dim < 0 || dim > 4) throw ConfigError("bad group dimension");
+        const auto g = parallel_groups(to_cfg(*cfg), static_cast<GroupDim>(dim));
+        *n_groups = static_cast<int>(g.size());
+        *group_size = g.empty() ? 0 : static_cast<int>(g[0].size());
+        int k = 0;
+        for (const auto& grp : g)
+            for (int r : grp) {
+                if (k < cap) out[k] = r;
+                ++k;
+            }
+        return RS_OK;
+    });
+}
+
+int rs_rank_coord(const rs_cfg_t* cfg, int rank, int coord[5]) {
+    return guarded([&] {
+        const RankCoord c = rank_coord(to_cfg(*cfg), rank);
+        coord[0] = c.pp_rank, coord[1] = c.dp_rank, coord[2] = c.tp_rank, coord[3] = c.ep_rank, coord[4] = c.edp_rank;
+        return RS_OK;
+    });
+}
+
 int rs_xor_peer(int i, int s, int n) { return sched::xor_peer(i, s, n); }
 
 int rs_memory_aware_chunk(const int* steps, const int64_t* cost, int n_steps, const int64_t* mem_avail, int n_ranks,

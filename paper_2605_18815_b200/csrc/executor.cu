@@ -342,6 +342,7 @@ Executor::~Executor() {
     for (void* p : owned_) cudaFree(p);
     if (d_fill_) cudaFree(d_fill_);
     if (d_counters_) cudaFree(d_counters_);
+    if (upload_) cudaStreamDestroy(upload_);
 }
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
@@ -502,7 +503,7 @@ void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t ro
     }
 }
 
-void TileSet::finalize(ExecStats* stats) {
+void TileSet::finalize(ExecStats* stats, cudaStream_t upload) {
     host.clear();
     groups.clear();
     for (size_t b = 0; b < buckets.size(); ++b) {
@@ -518,7 +519,10 @@ void TileSet::finalize(ExecStats* stats) {
     dev = nullptr;
     if (!host.empty()) {
         RS_CUDA(cudaMalloc(&dev, host.size() * sizeof(Tile)));
-        RS_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(Tile), cudaMemcpyHostToDevice));
+        // private non-blocking stream: descriptor uploads never serialize with the
+        // caller's (training) streams, so the EDM can prepare in the background
+        RS_CUDA(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(Tile), cudaMemcpyHostToDevice, upload));
+        RS_CUDA(cudaStreamSynchronize(upload));
     }
     if (stats) {
         stats->tiles += static_cast<std::int64_t>(host.size());
@@ -609,10 +613,11 @@ void Executor::prepare(bool staged) {
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
                     op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
     }
-    fused_->finalize(&stats_);
+    if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
+    fused_->finalize(&stats_, upload_);
     for (auto& kv : channels_) {
-        kv.second.pack->finalize(nullptr);
-        kv.second.unpack->finalize(nullptr);
+        kv.second.pack->finalize(nullptr, upload_);
+        kv.second.unpack->finalize(nullptr, upload_);
     }
     if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
     int sms = 148;

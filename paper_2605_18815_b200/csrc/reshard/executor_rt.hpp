@@ -64,7 +64,7 @@ struct TileSet {
     ~TileSet();
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
              std::int64_t dp, std::int64_t kTile);
-    void finalize(ExecStats* stats);
+    void finalize(ExecStats* stats, cudaStream_t upload);
     int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk) const;
 };
 
@@ -127,6 +127,7 @@ private:
     std::unique_ptr<TileSet> fused_;
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;
+    cudaStream_t upload_ = nullptr;
     std::vector<int> stage_of_dst_;
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;

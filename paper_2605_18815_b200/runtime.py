@@ -78,6 +78,21 @@ class StagedTransition:
                     if nbytes:
                         chans.append((self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes))
             self.plan_stages.append(chans)
+        # channels outside the plan's transfer list (the scalar broadcast, routing.hpp:341-353)
+        # may fall in steps the schedule elided: one final phase in the same global order
+        done = {(c[0], c[1]) for st in self.plan_stages for c in st}
+        rest = []
+        steps_all = range(1, 1 << max(1, (n - 1).bit_length()))
+        for s in steps_all:
+            for i in range(n):
+                p = xor_peer(i, s, n)
+                if p < 0 or self.gpu_of[i] == self.gpu_of[p] or (self.phys[i], self.phys[p]) in done:
+                    continue
+                nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
+                if nbytes:
+                    rest.append((self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes))
+        if rest:
+            self.plan_stages.append(rest)
 
     def run(self, stream: int = 0) -> None:
         import torch

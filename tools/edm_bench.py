@@ -1,0 +1,160 @@
+"""BASELINE config 3: Llama-3-8B elastic shrink / grow DP8 -> DP4 -> DP8 with the
+Elastic Device Manager overlapping new-world preparation with old-layout training.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/edm_bench.py [--layers L]
+
+Per direction: (1) blocking mode: prepare, then switch (nothing overlapped);
+(2) overlapped mode: prepare on the EDM side thread while the training loop keeps
+running bf16 GEMM steps on its own stream; switch when ready. Prints one JSON line
+with the SPEC accounting (exposed, overlapped, ratio) for both modes.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
+from paper_2605_18815_b200.edm import ElasticDeviceManager, overlap_accounting  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--gemm", type=int, default=8192)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    shrink, grow = S.config3(args.layers)
+    edm = ElasticDeviceManager()
+    train_stream = torch.cuda.Stream()
+    a = torch.randn(args.gemm, args.gemm, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(args.gemm, args.gemm, device="cuda", dtype=torch.bfloat16)
+
+    def train_step():
+        with torch.cuda.stream(train_stream):
+            for _ in range(4):
+                torch.matmul(a, b)
+        train_stream.synchronize()
+
+    # step cost of the old layout's training loop
+    for _ in range(3):
+        train_step()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        train_step()
+    step_s = (time.perf_counter() - t0) / 5
+
+    state = {}
+
+    def build_for(sc):
+        def build(ctrl):
+            t = {}
+            t0 = time.perf_counter()
+            edm.get_or_create_groups(sc.dst)
+            plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+            t["plan_s"] = time.perf_counter() - t0
+            tr = Transition(plan, world, rank, local, alloc=False)
+            keep = []
+            for side in (A.SIDE_SRC, A.SIDE_DST):
+                nr = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
+                for r in range(nr):
+                    for bb in range(6):
+                        _, n, g = tr.ex.buffer(side, r, bb)
+                        if not n or g != rank:
+                            continue
+                        key = (id(sc), side, r, bb)
+                        if side == A.SIDE_SRC and ("cur", r, bb) in state:
+                            buf = state[("cur", r, bb)]
+                        else:
+                            buf = torch.empty(n, dtype=torch.uint8, device="cuda")
+                        keep.append(buf)
+                        tr.ex.bind(side, r, bb, buf.data_ptr(), n)
+            t["alloc_s"] = time.perf_counter() - t0 - t["plan_s"]
+            if world > 1:
+                blob = tr.ex.ipc_export()
+                blobs = [None] * world
+                dist.all_gather_object(blobs, blob, group=ctrl)
+                for x in blobs:
+                    tr.ex.ipc_import(x)
+            tr.ex.prepare()
+            t["total_s"] = time.perf_counter() - t0
+            return tr, keep, t
+        return build
+
+    results = {}
+    seed = 0xED
+    # the DP8 state lives in its own buffers first
+    first = RoutingPlan.from_scenario(shrink)
+    ex0 = Transition(first, world, rank, local, alloc=False).ex
+    for r in range(first.summary.src_world):
+        for bb in range(6):
+            _, n, g = ex0.buffer(A.SIDE_SRC, r, bb)
+            if n and g == rank:
+                state[("cur", r, bb)] = torch.empty(n, dtype=torch.uint8, device="cuda")
+                ex0.bind(A.SIDE_SRC, r, bb, state[("cur", r, bb)].data_ptr(), n)
+    ex0.fill(A.SIDE_SRC, seed)
+    del ex0
+    for name, sc in (("shrink_dp8_to_dp4", shrink), ("grow_dp4_to_dp8", grow)):
+        out = {}
+        for mode in ("blocking", "overlapped"):
+            torch.cuda.synchronize()
+            dist.barrier()
+            edm.prepare_async(build_for(sc))
+            window_steps = 0
+            t_win = time.perf_counter()
+            if mode == "overlapped":
+                while not edm.ready():
+                    train_step()
+                    window_steps += 1
+            tr, keep, tprep = edm.wait()
+            window_s = time.perf_counter() - t_win if mode == "overlapped" else 0.0
+            # all ranks must have finished preparing before anyone writes into peers
+            flag = torch.ones(1, device="cuda")
+            dist.all_reduce(flag)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tr.run()
+            torch.cuda.synchronize()
+            dist.barrier()
+            switch_s = time.perf_counter() - t0
+            bad = tr.ex.verify(A.SIDE_DST, seed)[0]
+            init = torch.tensor([edm.init_s, window_s, switch_s, float(bad)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(init, op=dist.ReduceOp.MAX)
+            init_s, window_s, switch_s, bad = init.tolist()
+            acc = overlap_accounting(init_s, switch_s, window_s=window_s, mode=mode)
+            acc.update(window_train_steps=window_steps, train_step_s=step_s, verified_mismatches=int(bad),
+                       bytes_moved=tr.plan.bytes_moved(), prepare_breakdown_rank0=tprep)
+            out[mode] = acc
+            last = (tr, keep)
+        # the new layout becomes the current state for the next event
+        tr, keep = last
+        state.clear()
+        for r in range(tr.plan.summary.dst_world):
+            for bb in range(6):
+                p, n, g = tr.ex.buffer(A.SIDE_DST, r, bb)
+                if n and g == rank:
+                    for t in keep:
+                        if t.data_ptr() == p:
+                            state[("cur", r, bb)] = t
+        results[name] = out
+        del tr
+    if rank == 0:
+        print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
+                          "n_gpus": world, "results": results}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
