@@ -316,14 +316,22 @@ def run_ours(args):
         if n == 1:
             roof = {"bound": "hbm", "achieved": round(achieved_hbm, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved_hbm / pk["hbm_gbs"], 4), "traffic": None, "peak_source": pk["source"],
-                    "kernel": "copy_tiles_kernel<16> (forward transition)",
+                    "kernel": "bulk_tiles_kernel<4,32K> (TMA bulk, forward transition)",
                     "algorithmic_bytes_per_launch": local_rw}
         else:
-            nv = st_f.remote_bytes / (fwd_avg / 1e3) / 1e9
+            # T_roof = max_g max(out_g / NVLink, in_g / NVLink, HBM_g / B_HBM); the
+            # binding GPU's NVLink bytes over the measured (max over ranks) transition time
+            pl = [ab.placement(n, g) for g in range(n)]
+            link = max(max(p.out_bytes, p.in_bytes) for p in pl)
+            hbm = max(2 * p.local_bytes + p.out_bytes + p.in_bytes for p in pl)
+            t_roof = max(link / (NVLINK_GBS * 1e9), hbm / (pk["hbm_gbs"] * 1e9))
+            nv = link / (fwd_avg / 1e3) / 1e9
             roof = {"bound": "nvlink", "achieved": round(nv, 1), "peak": NVLINK_GBS, "unit": "GB/s",
-                    "frac": round(nv / NVLINK_GBS, 4), "frac_of_measured_peer_copy": round(nv / NVLINK_MEASURED_GBS, 4),
-                    "traffic": None, "kernel": "copy_tiles_kernel<16> (forward transition, rank 0)",
-                    "algorithmic_bytes_per_launch": st_f.remote_bytes, "hbm_achieved_gbs": round(achieved_hbm, 1)}
+                    "frac": round(t_roof / (fwd_avg / 1e3), 4), "frac_of_measured_peer_copy": round(nv / NVLINK_MEASURED_GBS, 4),
+                    "traffic": None, "kernel": "bulk_tiles_kernel / copy_tiles_kernel (forward transition, binding GPU)",
+                    "algorithmic_bytes_per_launch": link, "t_roof_s": round(t_roof, 5),
+                    "per_gpu_out_in_gb": [[round(p.out_bytes / 1e9, 2), round(p.in_bytes / 1e9, 2)] for p in pl],
+                    "hbm_achieved_gbs_rank0": round(achieved_hbm, 1)}
         cpu = None
         if not args.no_cpu_baseline:
             cpu = cpu_baseline(layers_sample=args.cpu_layers)

@@ -226,6 +226,10 @@ int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** d
 /* destination-rank stage order of direction 0 (A->B) or 1 (B->A) */
 int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n);
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out);
+/* host-only memory plan (no GPU): stats and the execution-simulation check
+ * (violations == 0 means every read sees its own data) */
+int rs_memory_plan(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
+                   rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap);
 /* run the plan as memory-aware stages: dst ranks in the given order */
 int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n);
 

@@ -21,7 +21,7 @@ EXPORTED = [
     "rs_plan_regions", "rs_plan_dump_rows_host", "rs_exec_create", "rs_exec_destroy", "rs_exec_alloc",
     "rs_exec_bind", "rs_exec_buffer", "rs_exec_ipc_export", "rs_exec_ipc_import", "rs_exec_prepare",
     "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats", "rs_exec_set_stages",
-    "rs_config_groups", "rs_rank_coord", "rs_exec_prepare_staged", "rs_exec_channel_bytes", "rs_exec_pack", "rs_exec_unpack", "rs_plan_placement", "rs_xor_peer", "rs_memory_aware_chunk", "rs_schedule_build", "rs_schedule_destroy",
+    "rs_memory_plan", "rs_config_groups", "rs_rank_coord", "rs_exec_prepare_staged", "rs_exec_channel_bytes", "rs_exec_pack", "rs_exec_unpack", "rs_plan_placement", "rs_xor_peer", "rs_memory_aware_chunk", "rs_schedule_build", "rs_schedule_destroy",
     "rs_schedule_summary", "rs_schedule_stage", "rs_schedule_peer", "rs_schedule_collective", "rs_schedule_dump",
     "rs_arena_create", "rs_arena_destroy", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
 ]
@@ -129,6 +129,7 @@ def lib():
     L.rs_exec_stats.argtypes = [vp, P(ExecStats_t)]
     L.rs_exec_set_stages.argtypes = [vp, P(C.c_int), C.c_int]
     L.rs_plan_placement.argtypes = [vp, C.c_int, C.c_int, P(PlacementStats_t)]
+    L.rs_memory_plan.argtypes = [vp, vp, i64, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int), P(C.c_int), C.c_int]
     L.rs_config_groups.argtypes = [P(Cfg_t), C.c_int, P(C.c_int), C.c_int, P(C.c_int), P(C.c_int)]
     L.rs_rank_coord.argtypes = [P(Cfg_t), C.c_int, P(C.c_int)]
     L.rs_exec_prepare_staged.argtypes = [vp]

@@ -339,3 +339,12 @@ def _exec_staged_methods():
 
 
 _exec_staged_methods()
+
+
+def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False):
+    """Host-only arena plan: (stats, simulated violations, stage orders)."""
+    st, viol = A.ArenaStats_t(), C.c_int64()
+    oa, ob = (C.c_int * 1024)(), (C.c_int * 1024)()
+    A.check(A.lib().rs_memory_plan(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), C.byref(st), C.byref(viol),
+                                   oa, ob, 1024))
+    return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]

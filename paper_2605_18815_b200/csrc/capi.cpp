@@ -708,6 +708,26 @@ int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n
     });
 }
 
+int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, rs_arena_stats_t* stats,
+                   int64_t* violations, int* order_ab, int* order_ba, int cap) {
+    return guarded([&] {
+        const mem::MemoryPlan mp = mem::plan_memory(ab->core, ba ? &ba->core : nullptr,
+                                                    chunk_bytes > 0 ? chunk_bytes : (32ll << 20), with_grads != 0);
+        stats->physical_bytes = mp.stats.physical_bytes;
+        stats->a_bytes = mp.stats.a_bytes;
+        stats->b_bytes = mp.stats.b_bytes;
+        stats->aliased_bytes = mp.stats.aliased_bytes;
+        stats->chunks = mp.stats.chunks;
+        *violations = mem::simulate_memory_plan(mp, ab->core, ba ? &ba->core : nullptr);
+        for (int d = 0; d < 2; ++d) {
+            int* o = d == 0 ? order_ab : order_ba;
+            if (!o) continue;
+            for (int i = 0; i < cap; ++i) o[i] = i < static_cast<int>(mp.order[d].size()) ? mp.order[d][static_cast<size_t>(i)] : -1;
+        }
+        return RS_OK;
+    });
+}
+
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
     return guarded([&] {
         const mem::ArenaStats& s = a->a->stats();

@@ -41,6 +41,25 @@ struct ArenaStats {
 /// Stage order of a direction: destination ranks, greedy so sources die early.
 std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops);
 
+/// Host-side memory plan (no driver calls; CPU-testable).
+struct BufPlan {
+    std::int64_t bytes = 0, reserved = 0;
+    bool direct = false;     // small buffer: plain allocation, never aliased
+    std::vector<int> phys;   // physical chunk per VA chunk
+};
+struct MemoryPlan {
+    std::int64_t chunk = 0;
+    std::vector<BufPlan> bufs[2];  // [layout][rank * kNumBufs + buf]
+    std::vector<int> order[2];     // stage orders (dst ranks) A->B, B->A
+    int nphys = 0;
+    ArenaStats stats;
+};
+MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads);
+/// Replays the staged execution chunk by chunk (A->B, then B->A) tracking which
+/// logical chunk each physical chunk holds; counts reads of clobbered data and
+/// same-stage read/write races. 0 == the aliasing is safe.
+std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba);
+
 class Arena {
 public:
     /// ab: A->B; ba: B->A on the same buffers (or nullptr for one-way). All virtual

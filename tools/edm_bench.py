@@ -136,7 +136,11 @@ def main():
             acc.update(window_train_steps=window_steps, train_step_s=step_s, verified_mismatches=int(bad),
                        bytes_moved=tr.plan.bytes_moved(), prepare_breakdown_rank0=tprep)
             out[mode] = acc
-            last = (tr, keep)
+            if mode == "blocking":  # free the blocking run's new layout before the overlapped one
+                del tr, keep
+                torch.cuda.synchronize()
+            else:
+                last = (tr, keep)
         # the new layout becomes the current state for the next event
         tr, keep = last
         state.clear()
