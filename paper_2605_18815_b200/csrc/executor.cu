@@ -343,6 +343,9 @@ Executor::~Executor() {
     if (d_fill_) cudaFree(d_fill_);
     if (d_counters_) cudaFree(d_counters_);
     if (upload_) cudaStreamDestroy(upload_);
+    if (aux_) cudaStreamDestroy(aux_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
 }
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
@@ -510,7 +513,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload) {
         const auto& v = buckets[b];
         if (v.empty()) continue;
         const int c = static_cast<int>(b % 5);
-        groups.push_back({c, static_cast<int>(host.size()), static_cast<int>(v.size())});
+        groups.push_back({c, static_cast<int>(host.size()), static_cast<int>(v.size()), static_cast<int>(b / 5)});
         host.insert(host.end(), v.begin(), v.end());
         if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(v.size());
     }
@@ -535,11 +538,12 @@ TileSet::~TileSet() {
 }
 
 int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm,
-                    bool bulk) const {
+                    bool bulk, int key_mod, int key_rem) const {
     int launches = 0;
     const int grid_cap = sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
     const Tile* base = static_cast<const Tile*>(dev);
     for (const Group& g : groups) {
+        if (key_mod > 0 && g.key % key_mod != key_rem) continue;
         const int n = g.count;
         const int grid = std::min(n, grid_cap);
         const Tile* t = base + g.begin;
@@ -568,6 +572,7 @@ void Executor::prepare(bool staged) {
     const std::vector<CopyOp> ops = build_ops(P_);
     stats_ = ExecStats{};
     staged_ = staged;
+    has_remote_ = false;
     channels_.clear();
     fused_ = std::make_unique<TileSet>();
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
@@ -609,7 +614,10 @@ void Executor::prepare(bool staged) {
                                      op.src_side_rank, op.src_buf, op.dst_rank, op.dst_buf));
         (dst_here ? stats_.local_bytes : stats_.remote_bytes) += total;
         const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
-        fused_->add(stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+        if (!dst_here) has_remote_ = true;
+        // key = stage * 2 + remote: peer-bound tiles run as their own launch so they can
+        // overlap with the local HBM copies on a second stream
+        fused_->add(stage * 2 + (dst_here ? 0 : 1), reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
                     op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
     }
@@ -625,6 +633,10 @@ void Executor::prepare(bool staged) {
     sms_ = sms;
     const char* kern = std::getenv("RS_COPY_KERNEL");
     use_bulk_ = !(kern && std::string(kern) == "vector");
+    const char* rk = std::getenv("RS_REMOTE_KERNEL");
+    remote_bulk_ = rk && std::string(rk) == "bulk";
+    const char* rc = std::getenv("RS_REMOTE_CTAS_PER_SM");
+    remote_ctas_per_sm_ = rc ? std::atoi(rc) : 2;
     if (use_bulk_)
         RS_CUDA(cudaFuncSetAttribute(bulk_tiles_kernel<kBulkStages, kBulkStage>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkStage));
@@ -634,7 +646,21 @@ void Executor::prepare(bool staged) {
 int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     RS_CUDA(cudaSetDevice(cfg_.device));
-    return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
+    if (!has_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
+    // NVLink-bound part (vector stores: full 16-B warps to peer HBM) on the caller's
+    // stream; local HBM copies (TMA bulk) concurrently on an auxiliary stream
+    if (!aux_) {
+        RS_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+        RS_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        RS_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    }
+    RS_CUDA(cudaEventRecord(ev_fork_, stream));
+    RS_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    int n = fused_->launch(stream, 0, 0, sms_, remote_ctas_per_sm_, remote_bulk_, 2, 1);
+    n += fused_->launch(aux_, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_, 2, 0);
+    RS_CUDA(cudaEventRecord(ev_join_, aux_));
+    RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
+    return n;
 }
 
 std::int64_t Executor::channel_bytes(int src_phys, int dst_phys) const {

@@ -52,7 +52,7 @@ struct RankBufs {
 /// pack / unpack); kernels add runtime base addresses so staging buffers can move.
 struct TileSet {
     struct Group {
-        int cls, begin, count;
+        int cls, begin, count, key;
     };
     std::vector<std::vector<Tile>> buckets;  // [key * 5 + class] while building
     std::vector<Tile> host;
@@ -65,7 +65,9 @@ struct TileSet {
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
              std::int64_t dp, std::int64_t kTile);
     void finalize(ExecStats* stats, cudaStream_t upload);
-    int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk) const;
+    /// launch groups in key order; key_mod > 0 restricts to keys with key % key_mod == key_rem
+    int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk,
+               int key_mod = 0, int key_rem = 0) const;
 };
 
 class Executor {
@@ -128,6 +130,11 @@ private:
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;
     cudaStream_t upload_ = nullptr;
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    bool has_remote_ = false;
+    bool remote_bulk_ = false;     // RS_REMOTE_KERNEL=bulk: TMA bulk stores to peers
+    int remote_ctas_per_sm_ = 2;   // RS_REMOTE_CTAS_PER_SM
     std::vector<int> stage_of_dst_;
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;
