@@ -569,6 +569,8 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
 
 void Executor::prepare(bool staged) {
     RS_CUDA(cudaSetDevice(cfg_.device));
+    const char* sr = std::getenv("RS_SPLIT_REMOTE");
+    split_remote_ = sr && std::string(sr) == "1";
     const std::vector<CopyOp> ops = build_ops(P_);
     stats_ = ExecStats{};
     staged_ = staged;
@@ -615,9 +617,9 @@ void Executor::prepare(bool staged) {
         (dst_here ? stats_.local_bytes : stats_.remote_bytes) += total;
         const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
         if (!dst_here) has_remote_ = true;
-        // key = stage * 2 + remote: peer-bound tiles run as their own launch so they can
-        // overlap with the local HBM copies on a second stream
-        fused_->add(stage * 2 + (dst_here ? 0 : 1), reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+        // key = stage * 2 + remote when split_remote_ (peer-bound tiles as their own launch on
+        // the caller's stream, local HBM tiles on an aux stream); otherwise one mixed launch
+        fused_->add(split_remote_ ? stage * 2 + (dst_here ? 0 : 1) : stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
                     op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
     }
@@ -647,6 +649,9 @@ int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     RS_CUDA(cudaSetDevice(cfg_.device));
     if (!has_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
+    // measured on B200 (profiles/r01_nvlink.md): with peer-bound tiles, one mixed launch
+    // of the 16-B vector kernel keeps NVLink busiest (685 GB/s at N=2, 620 at N=4)
+    if (!split_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, remote_bulk_);
     // NVLink-bound part (vector stores: full 16-B warps to peer HBM) on the caller's
     // stream; local HBM copies (TMA bulk) concurrently on an auxiliary stream
     if (!aux_) {

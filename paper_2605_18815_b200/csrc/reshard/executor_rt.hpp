@@ -134,6 +134,7 @@ private:
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     bool has_remote_ = false;
     bool remote_bulk_ = false;     // RS_REMOTE_KERNEL=bulk: TMA bulk stores to peers
+    bool split_remote_ = false;    // RS_SPLIT_REMOTE=1: peer tiles and local tiles on two streams
     int remote_ctas_per_sm_ = 2;   // RS_REMOTE_CTAS_PER_SM
     std::vector<int> stage_of_dst_;
     void* d_fill_ = nullptr;
