@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -568,6 +570,7 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
 }
 
 void Executor::prepare(bool staged) {
+    const auto t_begin = std::chrono::steady_clock::now();
     RS_CUDA(cudaSetDevice(cfg_.device));
     const char* sr = std::getenv("RS_SPLIT_REMOTE");
     split_remote_ = sr && std::string(sr) == "1";
@@ -623,11 +626,19 @@ void Executor::prepare(bool staged) {
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
                     op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
     }
+    const auto t_tiles = std::chrono::steady_clock::now();
     if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
     fused_->finalize(&stats_, upload_);
     for (auto& kv : channels_) {
         kv.second.pack->finalize(nullptr, upload_);
         kv.second.unpack->finalize(nullptr, upload_);
+    }
+    if (std::getenv("RS_TIMING")) {
+        const auto t_end = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[reshard] prepare: ops+tiles %.1f ms, upload %.1f ms, %lld tiles\n",
+                     std::chrono::duration<double, std::milli>(t_tiles - t_begin).count(),
+                     std::chrono::duration<double, std::milli>(t_end - t_tiles).count(),
+                     static_cast<long long>(stats_.tiles));
     }
     if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
     int sms = 148;
