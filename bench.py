@@ -332,6 +332,19 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": link, "t_roof_s": round(t_roof, 5),
                     "per_gpu_out_in_gb": [[round(p.out_bytes / 1e9, 2), round(p.in_bytes / 1e9, 2)] for p in pl],
                     "hbm_achieved_gbs_rank0": round(achieved_hbm, 1)}
+        # planner: ZeRO transfer-list expansion (1.84 M reference SliceTransfers at L=32) on the
+        # GPU planner vs the host sweep; the reference's own O(n*m) planner needs hours at L=32
+        g_ms, g_runs = ab.expand_timed(dev)
+        h_ms, h_runs = ab.expand_timed(-1)
+        planner = {"gpu_planner_ms": round(g_ms, 3), "host_sweep_ms": round(h_ms, 2), "runs": g_runs,
+                   "gpu_equals_host": g_runs == h_runs, "plan_build_s": round(plan_s, 4)}
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", "ref_plans.json")) as f:
+                ref = {e["name"]: e["ref_seconds"] for e in json.load(f)["entries"]}
+            planner["reference_planner_s_build_host"] = {"L=1": ref.get("llama3-8b-L1.tp8-to-dp2tp4-zero1"),
+                                                         "L=2": ref.get("llama3-8b-L2.tp8-to-dp2tp4-zero1")}
+        except Exception:
+            pass
         cpu = None
         if not args.no_cpu_baseline:
             cpu = cpu_baseline(layers_sample=args.cpu_layers)
@@ -348,7 +361,7 @@ def run_ours(args):
             "reconfig_s": round(fwd_avg / 1e3, 5), "reconfig_back_s": round(bwd_avg / 1e3, 5),
             "gbs_per_gpu": round(ab.bytes_moved() / (fwd_avg / 1e3) / 1e9 / n, 2),
             "plan_s": round(plan_s, 4), "verified_mismatches": int(bad),
-            "roofline": roof, "cpu_baseline": cpu,
+            "roofline": roof, "cpu_baseline": cpu, "planner": planner,
             "e2e": {"value": round(bytes_step / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "seconds_per_step": round(e2e_s, 4),
                     "what": "descriptor rebuild + upload, both transitions, result readback"},

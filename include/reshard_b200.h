@@ -144,6 +144,9 @@ typedef struct {
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
+/* expand the ZeRO optimizer transfers (1.84 M runs for Llama-3-8B) and report the
+ * time: device >= 0 -> GPU planner kernels (ms of device time), < 0 -> host sweep */
+int rs_plan_expand_timed(const rs_plan_t* p, int device, double* ms, int64_t* n_runs);
 
 /* ---- Elastic Device Manager support */
 #define RS_GROUP_DP 0

@@ -155,7 +155,7 @@ def lib():
         if fn.restype is None and name not in ("rs_free", "rs_model_destroy", "rs_plan_destroy", "rs_exec_destroy",
                                                       "rs_arena_destroy", "rs_schedule_destroy"):
             fn.restype = C.c_int
-    _lib = L
+    _lib = _late_bindings(L)
     return L
 
 
@@ -189,3 +189,9 @@ def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
     s = C.string_at(ptr.value, n.value).decode() if ptr.value else ""
     lib().rs_free(ptr)
     return s
+
+
+def _late_bindings(L):
+    L.rs_plan_expand_timed.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.rs_plan_expand_timed.restype = C.c_int
+    return L

@@ -40,7 +40,7 @@ class RoutingPlan:
         return cls(h.value)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_plan_destroy(self.h)
             self.h = None
 
@@ -102,7 +102,7 @@ class ModelSpace:
         self.model = model
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_model_destroy(self.h)
             self.h = None
 
@@ -141,7 +141,7 @@ class Executor:
         self.n_gpus, self.gpu, self.device = n_gpus, gpu, device
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_exec_destroy(self.h)
             self.h = None
 
@@ -206,7 +206,7 @@ class Arena:
         self.ab, self.ba = ab, ba
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_arena_destroy(self.h)
             self.h = None
 
@@ -281,7 +281,7 @@ class Schedule:
         self.summary = s
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_schedule_destroy(self.h)
             self.h = None
 
@@ -348,3 +348,13 @@ def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: 
     A.check(A.lib().rs_memory_plan(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), C.byref(st), C.byref(viol),
                                    oa, ob, 1024))
     return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
+
+
+def _plan_expand_timed(self, device: int = 0):
+    """(milliseconds, runs) of expanding the ZeRO transfer list: GPU planner or host."""
+    ms, n = C.c_double(), C.c_int64()
+    A.check(A.lib().rs_plan_expand_timed(self.h, device, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+RoutingPlan.expand_timed = _plan_expand_timed

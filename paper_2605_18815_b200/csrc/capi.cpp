@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -303,6 +304,23 @@ int rs_plan_summary(const rs_plan_t* p, rs_plan_summary_t* out) {
 int rs_plan_dump(const rs_plan_t* p, int device, char** out, size_t* len) {
     return guarded([&] {
         *out = dup_string(core::dump(p->core, expand(p, device)), len);
+        return RS_OK;
+    });
+}
+
+int rs_plan_expand_timed(const rs_plan_t* p, int device, double* ms, int64_t* n_runs) {
+    return guarded([&] {
+        double t = 0;
+        std::vector<core::FlatXfer> v;
+        if (device >= 0) {
+            v = gpuplan::expand_flat_gpu(p->core, device, &t);
+        } else {
+            const auto t0 = std::chrono::steady_clock::now();
+            v = core::expand_flat_host(p->core);
+            t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+        *ms = t;
+        *n_runs = static_cast<int64_t>(v.size());
         return RS_OK;
     });
 }

@@ -508,7 +508,19 @@ void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t ro
     }
 }
 
-void TileSet::finalize(ExecStats* stats, cudaStream_t upload) {
+void PinnedBuf::grow(size_t bytes) {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+    RS_CUDA(cudaHostAlloc(&ptr, bytes, cudaHostAllocDefault));
+    cap = bytes;
+}
+
+PinnedBuf::~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+}
+
+void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging) {
     host.clear();
     groups.clear();
     for (size_t b = 0; b < buckets.size(); ++b) {
@@ -526,7 +538,14 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload) {
         RS_CUDA(cudaMalloc(&dev, host.size() * sizeof(Tile)));
         // private non-blocking stream: descriptor uploads never serialize with the
         // caller's (training) streams, so the EDM can prepare in the background
-        RS_CUDA(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(Tile), cudaMemcpyHostToDevice, upload));
+        const size_t bytes = host.size() * sizeof(Tile);
+        if (staging && staging->size() < bytes) staging->grow(bytes);
+        if (staging) {  // pinned staging: DMA at PCIe speed instead of a pageable bounce
+            std::memcpy(staging->ptr, host.data(), bytes);
+            RS_CUDA(cudaMemcpyAsync(dev, staging->ptr, bytes, cudaMemcpyHostToDevice, upload));
+        } else {
+            RS_CUDA(cudaMemcpyAsync(dev, host.data(), bytes, cudaMemcpyHostToDevice, upload));
+        }
         RS_CUDA(cudaStreamSynchronize(upload));
     }
     if (stats) {
@@ -628,10 +647,10 @@ void Executor::prepare(bool staged) {
     }
     const auto t_tiles = std::chrono::steady_clock::now();
     if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
-    fused_->finalize(&stats_, upload_);
+    fused_->finalize(&stats_, upload_, &staging_);
     for (auto& kv : channels_) {
-        kv.second.pack->finalize(nullptr, upload_);
-        kv.second.unpack->finalize(nullptr, upload_);
+        kv.second.pack->finalize(nullptr, upload_, &staging_);
+        kv.second.unpack->finalize(nullptr, upload_, &staging_);
     }
     if (std::getenv("RS_TIMING")) {
         const auto t_end = std::chrono::steady_clock::now();

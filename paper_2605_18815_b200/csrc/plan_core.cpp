@@ -248,7 +248,7 @@ D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Tripl
         return a.lo != b.lo ? a.lo < b.lo : (a.hi != b.hi ? a.hi < b.hi : a.src < b.src);
     });
     // recv ivs = union of pieces (every recv element is covered by >= 1 source)
-    std::vector<Interval> ivs;
+    std::vector<Interval> ivs, multi;
     for (const Piece& p : pieces) {
         if (!ivs.empty() && p.lo <= ivs.back().hi) ivs.back().hi = std::max(ivs.back().hi, p.hi);
         else ivs.push_back({p.lo, p.hi});
@@ -301,6 +301,7 @@ D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Tripl
                 if (chosen < 0) chosen = run_c.front();
             }
             R.final_runs.push_back({run_lo, run_hi, chosen, -1});
+            if (run_c.size() > 1) multi.push_back({run_lo, run_hi});
         };
         for (size_t b = 0; b + 1 < bounds.size(); ++b) {
             const std::int64_t lo = bounds[b], hi = bounds[b + 1];
@@ -319,12 +320,18 @@ D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Tripl
             }
         }
         flush();
-        // tensors touched by this iv
-        for (const stair::Triple* T : trip) {
-            const std::int64_t tlo = T->t.off;
-            const auto& e = P.space->entries()[static_cast<size_t>(T->tensor)];
-            if (tlo < iv.hi && iv.lo < tlo + e.spec.numel()) R.flagged_tensors.push_back(T->tensor);
-        }
+    }
+    // tensors holding over-sourced elements: the executor takes their optimizer moves from
+    // the resolved runs (a choice among replicas); elsewhere every element has a single
+    // source, exactly as in the triples
+    for (const stair::Triple* T : trip) {
+        const std::int64_t tlo = T->t.off;
+        const std::int64_t thi = tlo + P.space->entries()[static_cast<size_t>(T->tensor)].spec.numel();
+        for (const Interval& m : multi)
+            if (m.lo < thi && tlo < m.hi) {
+                R.flagged_tensors.push_back(T->tensor);
+                break;
+            }
     }
     return R;
 }

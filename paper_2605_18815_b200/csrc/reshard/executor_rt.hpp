@@ -48,6 +48,18 @@ struct RankBufs {
     std::int64_t bytes[kNumBufs] = {0, 0, 0, 0, 0, 0};
 };
 
+/// Pinned host staging for descriptor uploads (reused across prepares).
+struct PinnedBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf();
+    size_t size() const { return cap; }
+    void grow(size_t bytes);
+};
+
 /// Device tiles of one launch group set (fused transition, or one channel's
 /// pack / unpack); kernels add runtime base addresses so staging buffers can move.
 struct TileSet {
@@ -64,7 +76,7 @@ struct TileSet {
     ~TileSet();
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
              std::int64_t dp, std::int64_t kTile);
-    void finalize(ExecStats* stats, cudaStream_t upload);
+    void finalize(ExecStats* stats, cudaStream_t upload, struct PinnedBuf* staging);
     /// launch groups in key order; key_mod > 0 restricts to keys with key % key_mod == key_rem
     int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk,
                int key_mod = 0, int key_rem = 0) const;
@@ -130,6 +142,7 @@ private:
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;
     cudaStream_t upload_ = nullptr;
+    PinnedBuf staging_;
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     bool has_remote_ = false;
