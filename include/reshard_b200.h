@@ -250,6 +250,8 @@ int rs_exec_prepare(rs_exec_t* e);
  * (NCCL send/recv, the measured comparison) is the caller's. Same-GPU moves stay fused. */
 int rs_exec_prepare_staged(rs_exec_t* e);
 int rs_exec_channel_bytes(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* bytes);
+/* per-op packed sizes of a channel (SPEC execute "naive" mode: one message per fragment) */
+int rs_exec_channel_ops(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* sizes, int64_t cap, int64_t* n);
 int rs_exec_pack(rs_exec_t* e, int src_phys, int dst_phys, void* dbuf, void* stream);
 int rs_exec_unpack(rs_exec_t* e, int src_phys, int dst_phys, const void* dbuf, void* stream);
 /* load_state on this GPU's ranks of one side */

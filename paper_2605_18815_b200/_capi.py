@@ -192,6 +192,9 @@ def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
 
 
 def _late_bindings(L):
+    L.rs_exec_channel_ops.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_int64,
+                                      C.POINTER(C.c_int64)]
+    L.rs_exec_channel_ops.restype = C.c_int
     L.rs_plan_expand_timed.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     L.rs_plan_expand_timed.restype = C.c_int
     return L

@@ -628,6 +628,15 @@ int rs_exec_channel_bytes(const rs_exec_t* e, int src_phys, int dst_phys, int64_
     });
 }
 
+int rs_exec_channel_ops(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* sizes, int64_t cap, int64_t* n) {
+    return guarded([&] {
+        const std::vector<std::int64_t> v = e->ex->channel_ops(src_phys, dst_phys);
+        *n = static_cast<int64_t>(v.size());
+        for (int64_t i = 0; i < *n && i < cap; ++i) sizes[i] = v[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
 int rs_exec_pack(rs_exec_t* e, int src_phys, int dst_phys, void* dbuf, void* stream) {
     return guarded([&] {
         e->ex->pack(src_phys, dst_phys, dbuf, static_cast<cudaStream_t>(stream));

@@ -630,6 +630,7 @@ void Executor::prepare(bool staged) {
             }
             off += total;
             ch.bytes = off;
+            ch.op_bytes.push_back(total);
             continue;
         }
         if (!src_here) continue;  // pushed by the source's GPU

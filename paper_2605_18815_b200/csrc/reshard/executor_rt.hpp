@@ -137,7 +137,18 @@ private:
     struct Channel {
         std::unique_ptr<TileSet> pack, unpack;
         std::int64_t bytes = 0;
+        std::vector<std::int64_t> op_bytes;  // packed size of each op, channel order
     };
+
+public:
+    /// staged mode: sizes of the channel's ops in packing order (the "naive" mode sends
+    /// one message per op)
+    std::vector<std::int64_t> channel_ops(int src_phys, int dst_phys) const {
+        auto it = channels_.find({src_phys, dst_phys});
+        return it == channels_.end() ? std::vector<std::int64_t>{} : it->second.op_bytes;
+    }
+
+private:
     std::unique_ptr<TileSet> fused_;
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;

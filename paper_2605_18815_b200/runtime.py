@@ -51,70 +51,102 @@ class Transition:
 
 class StagedTransition:
     """Algorithm 1 buffered execution (ExecuteSwitch) over NCCL: the
-    measured comparison for the fused push path. Per stage of the memory-aware
-    schedule: PackData into one contiguous buffer per (device -> peer) channel,
-    AsyncSend/AsyncRecv as one NCCL group (batch_isend_irecv), then UnpackData.
-    Channels are enumerated in the global (step, device) order on every rank, so
-    NCCL's per-pair FIFO matching pairs them without metadata."""
+    measured comparison for the fused push path, with SPEC execute's three modes
+    (SPEC.md:375-383):
+      async : per stage of the memory-aware schedule, PackData into one contiguous buffer
+              per (device -> peer) channel, all steps' AsyncSend/AsyncRecv as one NCCL
+              group (batch_isend_irecv), SynchronizeAll, UnpackData;
+      sync  : the same buffers, one XOR step at a time;
+      naive : no buffering of messages: one NCCL message per op (fragment group), sent
+              and received one after another.
+    Channels are enumerated in the global (step, device) order on every rank, so NCCL's
+    per-pair FIFO matching pairs them without metadata."""
 
-    def __init__(self, plan: RoutingPlan, ex: Executor, n_gpus: int, gpu: int, mem_avail=None, group=None):
+    MODES = ("async", "sync", "naive")
+
+    def __init__(self, plan: RoutingPlan, ex: Executor, n_gpus: int, gpu: int, mem_avail=None, group=None,
+                 mode: str = "async"):
         from .api import Schedule, xor_peer
-        self.plan, self.ex, self.n_gpus, self.gpu, self.group = plan, ex, n_gpus, gpu, group
+        if mode not in self.MODES:
+            raise ValueError(f"mode must be one of {self.MODES}")
+        self.plan, self.ex, self.n_gpus, self.gpu, self.group, self.mode = plan, ex, n_gpus, gpu, group, mode
         n = plan.summary.num_participants
         self.sched = Schedule(plan, mem_avail or [1 << 62] * n, promote=False)
         ex.prepare_staged()
         self.phys = list(range(n))  # device index -> phys (identity world maps in the benches)
         span = (max(self.phys) + 1 + n_gpus - 1) // n_gpus
         self.gpu_of = [p // span for p in self.phys]
+
+        def chan(i, p, s):
+            nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
+            if not nbytes or self.gpu_of[i] == self.gpu_of[p]:
+                return None
+            return (self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes, s)
+
         self.plan_stages = []
-        for k, (steps, _) in enumerate(self.sched.stages()):
-            chans = []
-            for s in steps:
-                for i in range(n):
-                    p = xor_peer(i, s, n)
-                    if p < 0 or self.gpu_of[i] == self.gpu_of[p]:
-                        continue
-                    nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
-                    if nbytes:
-                        chans.append((self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes))
+        for steps, _ in self.sched.stages():
+            chans = [c for s in steps for i in range(n) if xor_peer(i, s, n) >= 0
+                     for c in [chan(i, xor_peer(i, s, n), s)] if c]
             self.plan_stages.append(chans)
         # channels outside the plan's transfer list (the scalar broadcast, routing.hpp:341-353)
         # may fall in steps the schedule elided: one final phase in the same global order
         done = {(c[0], c[1]) for st in self.plan_stages for c in st}
-        rest = []
-        steps_all = range(1, 1 << max(1, (n - 1).bit_length()))
-        for s in steps_all:
-            for i in range(n):
-                p = xor_peer(i, s, n)
-                if p < 0 or self.gpu_of[i] == self.gpu_of[p] or (self.phys[i], self.phys[p]) in done:
-                    continue
-                nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
-                if nbytes:
-                    rest.append((self.phys[i], self.phys[p], self.gpu_of[i], self.gpu_of[p], nbytes))
+        rest = [c for s in range(1, 1 << max(1, (n - 1).bit_length())) for i in range(n)
+                if xor_peer(i, s, n) >= 0 for c in [chan(i, xor_peer(i, s, n), s)] if c and (c[0], c[1]) not in done]
         if rest:
             self.plan_stages.append(rest)
 
-    def run(self, stream: int = 0) -> None:
+    def _ops(self, src, dst):
+        n = A.C.c_int64()
+        A.check(A.lib().rs_exec_channel_ops(self.ex.h, src, dst, None, 0, A.C.byref(n)))
+        arr = (A.C.c_int64 * max(1, n.value))()
+        A.check(A.lib().rs_exec_channel_ops(self.ex.h, src, dst, arr, n.value, A.C.byref(n)))
+        return list(arr[: n.value])
+
+    def _exchange(self, chans, stream, per_op=False):
         import torch
         import torch.distributed as dist
-        self.ex.run(stream)  # same-GPU moves, fused
-        for chans in self.plan_stages:
-            ops, unpacks, keep = [], [], []
-            for src, dst, gs, gd, nbytes in chans:
+        sends, recvs = [], []
+        for src, dst, gs, gd, nbytes, _ in chans:
+            if gs == self.gpu:
+                buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                self.ex.pack(src, dst, buf.data_ptr(), stream)
+                sends.append((buf, gd, src, dst))
+            elif gd == self.gpu:
+                recvs.append((torch.empty(nbytes, dtype=torch.uint8, device="cuda"), gs, src, dst))
+        if per_op:  # naive: one blocking message per op, in the global channel order
+            for src, dst, gs, gd, nbytes, _ in chans:
+                if self.gpu not in (gs, gd):
+                    continue
                 if gs == self.gpu:
-                    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-                    self.ex.pack(src, dst, buf.data_ptr(), stream)
-                    ops.append(dist.P2POp(dist.isend, buf, gd, group=self.group))
-                    keep.append(buf)
-                elif gd == self.gpu:
-                    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-                    ops.append(dist.P2POp(dist.irecv, buf, gs, group=self.group))
-                    unpacks.append((src, dst, buf))
+                    buf = next(b for b, _, s, d in sends if (s, d) == (src, dst))
+                    peer, fn = gd, dist.send
+                else:
+                    buf = next(b for b, _, s, d in recvs if (s, d) == (src, dst))
+                    peer, fn = gs, dist.recv
+                off = 0
+                for sz in self._ops(src, dst):
+                    fn(buf[off:off + sz], peer, group=self.group)
+                    off += sz
+        else:
+            ops = [dist.P2POp(dist.isend, b, g, group=self.group) for b, g, _, _ in sends]
+            ops += [dist.P2POp(dist.irecv, b, g, group=self.group) for b, g, _, _ in recvs]
             if ops:
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
-            for src, dst, buf in unpacks:
-                self.ex.unpack(src, dst, buf.data_ptr(), stream)
+        for buf, _, src, dst in recvs:
+            self.ex.unpack(src, dst, buf.data_ptr(), stream)
+
+    def run(self, stream: int = 0) -> None:
+        self.ex.run(stream)  # same-GPU moves, fused
+        for chans in self.plan_stages:
+            if self.mode == "async":
+                self._exchange(chans, stream)
+            elif self.mode == "sync":
+                for s in sorted({c[5] for c in chans}, key=lambda x: [c[5] for c in chans].index(x)):
+                    self._exchange([c for c in chans if c[5] == s], stream)
+            else:
+                self._exchange(chans, stream, per_op=True)
 
 
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:

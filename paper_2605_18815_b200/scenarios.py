@@ -148,6 +148,33 @@ def llama3_70b(layers: int = 80) -> Model:
     return Model(f"llama3-70b-L{layers}", ts, layers=layers)
 
 
+def llama2_13b(layers: int = 40) -> Model:
+    """LLaMA-2 13B (Table 4 ablation model): h 5120, ffn 13824, MHA, vocab 32000."""
+    h, ffn, vocab = 5120, 13824, 32000
+    ts = [Tensor("embed", (vocab, h), 0, tp=0)]
+    for l in range(layers):
+        p = f"l{l}."
+        ts += [
+            Tensor(p + "attn_norm", (h,), l),
+            Tensor(p + "q", (h, h), l, tp=0),
+            Tensor(p + "k", (h, h), l, tp=0),
+            Tensor(p + "v", (h, h), l, tp=0),
+            Tensor(p + "o", (h, h), l, tp=1),
+            Tensor(p + "mlp_norm", (h,), l),
+            Tensor(p + "gate", (ffn, h), l, tp=0),
+            Tensor(p + "up", (ffn, h), l, tp=0),
+            Tensor(p + "down", (h, ffn), l, tp=1),
+        ]
+    ts += [Tensor("final_norm", (h,), layers - 1), Tensor("lm_head", (vocab, h), layers - 1, tp=0)]
+    return Model(f"llama2-13b-L{layers}", ts, layers=layers)
+
+
+def table4(layers: int = 8) -> Scenario:
+    """PAPER.md Table 4 ablation geometry: (TP,PP,DP) (2,8,1) -> (2,2,4), 16 ranks."""
+    return Scenario(llama2_13b(layers), Cfg(tp=2, pp=8, dp=1, zero=True), Cfg(tp=2, pp=2, dp=4, zero=True),
+                    rpn=16, name=f"llama2-13b-L{layers}.table4")
+
+
 def qwen3_30b_a3b(layers: int = 48, experts: int = 128) -> Model:
     """Qwen3-30B-A3B-style MoE (config 4): 579 tensors at L=48."""
     h, qd, kvd, hd, eff, vocab = 2048, 4096, 512, 128, 768, 151936
