@@ -597,6 +597,9 @@ void Executor::prepare(bool staged) {
     stats_ = ExecStats{};
     staged_ = staged;
     has_remote_ = false;
+    ce_ops_.clear();
+    const char* ce = std::getenv("RS_CE_MIN_BYTES");
+    ce_min_bytes_ = ce ? std::atoll(ce) : (4ll << 20);
     channels_.clear();
     fused_ = std::make_unique<TileSet>();
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
@@ -640,6 +643,16 @@ void Executor::prepare(bool staged) {
         (dst_here ? stats_.local_bytes : stats_.remote_bytes) += total;
         const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
         if (!dst_here) has_remote_ = true;
+        const bool contiguous = op.rows == 1 || (op.src_pitch == op.row_bytes && op.dst_pitch == op.row_bytes);
+        if (!dst_here && ce_min_bytes_ > 0 && contiguous && total >= ce_min_bytes_) {
+            // large contiguous peer-bound block: a copy engine moves it (778 GB/s both ways
+            // vs ~710 for SM stores, profiles/r01_nvlink.md) concurrently with the kernel
+            ce_ops_.push_back({reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+                               reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off),
+                               total});
+            stats_.ce_bytes += total;
+            continue;
+        }
         // key = stage * 2 + remote when split_remote_ (peer-bound tiles as their own launch on
         // the caller's stream, local HBM tiles on an aux stream); otherwise one mixed launch
         fused_->add(split_remote_ ? stage * 2 + (dst_here ? 0 : 1) : stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
@@ -680,20 +693,38 @@ int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     RS_CUDA(cudaSetDevice(cfg_.device));
     if (!has_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
-    // measured on B200 (profiles/r01_nvlink.md): with peer-bound tiles, one mixed launch
-    // of the 16-B vector kernel keeps NVLink busiest (685 GB/s at N=2, 620 at N=4)
-    if (!split_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, remote_bulk_);
-    // NVLink-bound part (vector stores: full 16-B warps to peer HBM) on the caller's
-    // stream; local HBM copies (TMA bulk) concurrently on an auxiliary stream
     if (!aux_) {
         RS_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
         RS_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         RS_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     }
+    if (!ce_ops_.empty()) {
+        // copy-engine part of the push on the aux stream, joined back into the caller's
+        RS_CUDA(cudaEventRecord(ev_fork_, stream));
+        RS_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    }
+    // measured on B200 (profiles/r01_nvlink.md): with peer-bound tiles, one mixed launch
+    // of the 16-B vector kernel keeps NVLink busiest (685 GB/s at N=2, 620 at N=4)
+    if (!split_remote_) {
+        const int n = fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, remote_bulk_);
+        if (!ce_ops_.empty()) {
+            for (const CeOp& c : ce_ops_)
+                RS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dst), reinterpret_cast<const void*>(c.src),
+                                        static_cast<size_t>(c.bytes), cudaMemcpyDeviceToDevice, aux_));
+            RS_CUDA(cudaEventRecord(ev_join_, aux_));
+            RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
+        }
+        return n;
+    }
+    // NVLink-bound part (vector stores: full 16-B warps to peer HBM) on the caller's
+    // stream; local HBM copies (TMA bulk) concurrently on an auxiliary stream
     RS_CUDA(cudaEventRecord(ev_fork_, stream));
     RS_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
     int n = fused_->launch(stream, 0, 0, sms_, remote_ctas_per_sm_, remote_bulk_, 2, 1);
     n += fused_->launch(aux_, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_, 2, 0);
+    for (const CeOp& c : ce_ops_)
+        RS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dst), reinterpret_cast<const void*>(c.src),
+                                static_cast<size_t>(c.bytes), cudaMemcpyDeviceToDevice, aux_));
     RS_CUDA(cudaEventRecord(ev_join_, aux_));
     RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
     return n;

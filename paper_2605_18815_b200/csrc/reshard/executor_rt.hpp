@@ -40,6 +40,7 @@ struct ExecStats {
     std::int64_t tiles = 0;
     std::int64_t tiles_by_class[5] = {0, 0, 0, 0, 0};  // 16/8/4/2/1-byte vectors
     std::int64_t launches = 0;                         // kernel launches per run()
+    std::int64_t ce_bytes = 0;                         // peer-bound bytes moved by copy engines
 };
 
 struct RankBufs {
@@ -159,6 +160,12 @@ private:
     bool has_remote_ = false;
     bool remote_bulk_ = false;     // RS_REMOTE_KERNEL=bulk: TMA bulk stores to peers
     bool split_remote_ = false;    // RS_SPLIT_REMOTE=1: peer tiles and local tiles on two streams
+    struct CeOp {
+        std::uint64_t src, dst;
+        std::int64_t bytes;
+    };
+    std::vector<CeOp> ce_ops_;          // large contiguous peer-bound blocks for the copy engines
+    std::int64_t ce_min_bytes_ = 4 << 20;  // RS_CE_MIN_BYTES (0 disables)
     int remote_ctas_per_sm_ = 2;   // RS_REMOTE_CTAS_PER_SM
     std::vector<int> stage_of_dst_;
     void* d_fill_ = nullptr;

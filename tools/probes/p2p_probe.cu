@@ -91,6 +91,9 @@ int main() {
                 char* remote = dst[1 - g];
                 if (mode == 0) push_vec<512, 4><<<ctas, 512, 0, st[g]>>>((const uint4*)src[g], (uint4*)remote, bytes / 16);
                 else if (mode == 1) push_bulk<4, 32768><<<ctas, 32, 4 * 32768, st[g]>>>(src[g], remote, bytes);
+                else if (mode == 3) push_vec<512, 4><<<ctas, 512, 0, st[g]>>>((const uint4*)src[1 - g], (uint4*)dst[g], bytes / 16);  // pull
+                else if (mode == 4) push_vec<512, 8><<<ctas, 512, 0, st[g]>>>((const uint4*)src[1 - g], (uint4*)dst[g], bytes / 16);  // pull, deeper
+                else if (mode == 5) push_bulk<4, 32768><<<ctas, 32, 4 * 32768, st[g]>>>(src[1 - g], dst[g], bytes);  // TMA pull
                 else cudaMemcpyPeerAsync(remote, 1 - g, src[g], g, bytes, st[g]);
                 cudaEventRecord(e1[g], st[g]);
             }
@@ -112,6 +115,9 @@ int main() {
         for (int ctas : {16, 32, 64, 148, 296, 592}) run(0, dirs, ctas, "SM vec 512x4");
         for (int ctas : {16, 32, 64, 148, 296}) run(1, dirs, ctas, "TMA bulk 4x32K");
         run(2, dirs, 0, "CE cudaMemcpyPeer");
+        for (int ctas : {148, 296, 592}) run(3, dirs, ctas, "SM vec PULL 512x4");
+        for (int ctas : {148, 296}) run(4, dirs, ctas, "SM vec PULL 512x8");
+        for (int ctas : {148, 296}) run(5, dirs, ctas, "TMA bulk PULL 4x32K");
     }
     std::vector<char> h(16);
     CR(cudaSetDevice(1));
