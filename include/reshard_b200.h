@@ -142,6 +142,10 @@ typedef struct {
     int64_t local_bytes, out_bytes, in_bytes, ops;
 } rs_placement_stats_t;
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
+/* validate_plan: invariants + destination coverage; violations are
+ * returned (one per line), not raised. drop >= 0 removes one fragment first (fault
+ * injection: box transfers are indexed first, then ZeRO runs). */
+int rs_plan_validate(const rs_plan_t* p, int64_t drop, char** report, size_t* len, int64_t* n_violations);
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
 /* expand the ZeRO optimizer transfers (1.84 M runs for Llama-3-8B) and report the

@@ -192,6 +192,9 @@ def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
 
 
 def _late_bindings(L):
+    L.rs_plan_validate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                   C.POINTER(C.c_int64)]
+    L.rs_plan_validate.restype = C.c_int
     L.rs_exec_channel_ops.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_int64,
                                       C.POINTER(C.c_int64)]
     L.rs_exec_channel_ops.restype = C.c_int

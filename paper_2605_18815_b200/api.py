@@ -358,3 +358,13 @@ def _plan_expand_timed(self, device: int = 0):
 
 
 RoutingPlan.expand_timed = _plan_expand_timed
+
+
+def _plan_validate(self, drop: int = -1) -> List[str]:
+    """validate_plan: violation lines, empty on success."""
+    p, n, k = C.c_void_p(), C.c_size_t(), C.c_int64()
+    A.check(A.lib().rs_plan_validate(self.h, drop, C.byref(p), C.byref(n), C.byref(k)))
+    return [x for x in A.take_string(p, n).splitlines() if x]
+
+
+RoutingPlan.validate = _plan_validate

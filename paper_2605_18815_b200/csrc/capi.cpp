@@ -16,6 +16,7 @@
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
 #include "reshard/schedule.hpp"
+#include "reshard/validate.hpp"
 
 namespace reshard {
 namespace gpuplan {
@@ -304,6 +305,17 @@ int rs_plan_summary(const rs_plan_t* p, rs_plan_summary_t* out) {
 int rs_plan_dump(const rs_plan_t* p, int device, char** out, size_t* len) {
     return guarded([&] {
         *out = dup_string(core::dump(p->core, expand(p, device)), len);
+        return RS_OK;
+    });
+}
+
+int rs_plan_validate(const rs_plan_t* p, int64_t drop, char** report, size_t* len, int64_t* n_violations) {
+    return guarded([&] {
+        const std::vector<std::string> v = core::validate_plan(p->core, core::expand_flat_host(p->core), drop);
+        std::string s;
+        for (const std::string& x : v) s += x + "\n";
+        *n_violations = static_cast<int64_t>(v.size());
+        *report = dup_string(s, len);
         return RS_OK;
     });
 }
