@@ -127,4 +127,5 @@ class ElasticDeviceManager:
             self._thread.join()
         if self._error is not None:
             raise self._error
-        return self._result
+        res, self._result = self._result, None  # the caller owns the prepared state now
+        return res

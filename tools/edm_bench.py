@@ -31,11 +31,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--gemm", type=int, default=8192)
+    ap.add_argument("--balance", action="store_true",
+                    help="grow with balance_fanout (reference PlanOptions): joiners spread over the replicas")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     shrink, grow = S.config3(args.layers)
+    grow.balance = args.balance
     edm = ElasticDeviceManager()
     train_stream = torch.cuda.Stream()
     a = torch.randn(args.gemm, args.gemm, device="cuda", dtype=torch.bfloat16)
@@ -152,10 +155,13 @@ def main():
                         if t.data_ptr() == p:
                             state[("cur", r, bb)] = t
         results[name] = out
-        del tr
+        # the old layout is gone after the switch: drop every reference to its buffers
+        del tr, keep, last
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
-                          "n_gpus": world, "results": results}), flush=True)
+                          "n_gpus": world, "grow_balance_fanout": args.balance, "results": results}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
