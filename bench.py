@@ -192,7 +192,15 @@ def run_ours(args):
     bwd = Transition(ba, n, rank, dev, alloc=False)
     keep = []
     arena = None
-    if n == 1 and not args.no_arena:
+    multi_arena = n > 1 and args.arena_multi
+    if multi_arena:
+        # N>1 memory-aware arena: VMM buffers shared by POSIX descriptors, eager-free
+        # aliasing under the per-GPU cap, one global barrier per memory-aware stage
+        from paper_2605_18815_b200.runtime import run_stages, shared_arena
+        arena, cuts = shared_arena(ab, ba, rank, world, dev, cap_bytes=args.hbm_cap,
+                                   tag=os.environ.get("MASTER_PORT", "0"))
+        arena.bind(fwd.ex, bwd.ex, cuts)
+    elif n == 1 and not args.no_arena:
         # 8 virtual ranks on one GPU: old + new state (240.9 GB at L=32) exceed HBM, so
         # the memory-aware arena maps new-layout chunks onto dead old-layout chunks
         from paper_2605_18815_b200.api import Arena
@@ -216,6 +224,12 @@ def run_ours(args):
         bwd_staged = StagedTransition(ba, bwd.ex, n, rank)
         fwd.run, bwd.run = fwd_staged.run, bwd_staged.run
         reprepare = (fwd.ex.prepare_staged, bwd.ex.prepare_staged)
+    elif multi_arena:
+        fwd.ex.prepare()
+        bwd.ex.prepare()
+        fwd.run = lambda st: run_stages(fwd.ex, st, world)
+        bwd.run = lambda st: run_stages(bwd.ex, st, world)
+        reprepare = (fwd.ex.prepare, bwd.ex.prepare)
     else:
         fwd.connect()
         bwd.connect()
@@ -372,7 +386,8 @@ def run_ours(args):
             a = arena.stats()
             out["memory"] = {"physical_gb": round(a.physical_bytes / 1e9, 2), "old_layout_gb": round(a.a_bytes / 1e9, 2),
                              "new_layout_gb": round(a.b_bytes / 1e9, 2), "aliased_gb": round(a.aliased_bytes / 1e9, 2),
-                             "stages_fwd": arena.stage_order(0), "stages_bwd": arena.stage_order(1)}
+                             "stages_fwd": arena.stage_order(0), "stages_bwd": arena.stage_order(1),
+                             "stage_groups": [fwd.ex.num_stages(), bwd.ex.num_stages()]}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
@@ -389,6 +404,8 @@ def main():
     ap.add_argument("--cpu-layers", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-arena", action="store_true", help="N=1: plain allocations (needs old+new to fit)")
+    ap.add_argument("--arena-multi", action="store_true",
+                    help="N>1: memory-aware arena across GPUs (stage barriers) instead of plain allocations")
     ap.add_argument("--hbm-cap", type=int, default=0, help="arena physical budget in bytes (0: free HBM - 1 GiB)")
     ap.add_argument("--transport", default="fused", choices=["fused", "nccl"],
                     help="fused: one-sided NVLink stores (product); nccl: pack -> NCCL send/recv -> unpack (comparison)")

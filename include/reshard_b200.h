@@ -224,6 +224,7 @@ typedef struct {
 typedef struct rs_arena rs_arena_t;
 typedef struct {
     int64_t physical_bytes, a_bytes, b_bytes, aliased_bytes, chunks;
+    int64_t stage_groups[2]; /* concurrent stage groups (barriers) per direction */
 } rs_arena_stats_t;
 int rs_arena_create(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int device, int64_t cap_bytes,
                     int64_t chunk_bytes, int with_grads, rs_arena_t** out);
@@ -232,13 +233,43 @@ void rs_arena_destroy(rs_arena_t* a);
 int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** dptr, int64_t* bytes);
 /* destination-rank stage order of direction 0 (A->B) or 1 (B->A) */
 int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n);
+/* per position of that order: 1 = a barrier must precede it (positions between two cuts
+ * share one stage and run concurrently); position 0 is always 1 */
+int rs_arena_stage_cuts(const rs_arena_t* a, int dir, int* out, int cap, int* n);
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out);
 /* host-only memory plan (no GPU): stats and the execution-simulation check
  * (violations == 0 means every read sees its own data) */
+/* fewest concurrency groups of the stage order whose memory plan for `gpu` fits
+ * cap_bytes (*groups = -1: none); every GPU must use the same groups (take the max) */
+int rs_memory_min_groups(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
+                         int n_gpus, int gpu, int64_t cap_bytes, int* groups, int64_t* physical_bytes);
+/* the same for the buffers GPU `gpu` of n_gpus hosts, with the stage order coarsened
+ * into `groups` concurrency groups (0 = one per stage) */
+int rs_memory_plan_ex(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                      int gpu, int groups, rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba,
+                      int cap);
 int rs_memory_plan(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                    rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap);
+/* multi-GPU arena: this process maps the buffers of the virtual ranks placed on GPU
+ * `gpu` of `n_gpus` (shareable VMM); peers' buffers are imported from their export */
+int rs_arena_create_multi(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int n_gpus, int gpu, int device,
+                          int64_t cap_bytes, int64_t chunk_bytes, int with_grads, int groups, rs_arena_t** out);
+/* POSIX-FD export of this GPU's physical allocations + mapping table (malloc'd; rs_free) */
+int rs_arena_export(const rs_arena_t* a, int** fds, int* n_fds, void** table, size_t* table_len);
+/* map a peer's buffers (consumes the descriptors) */
+int rs_arena_import(rs_arena_t* a, const int* fds, int n_fds, const void* table, size_t table_len);
+/* descriptor exchange between local processes (Unix socket, SCM_RIGHTS, abstract name) */
+int rs_fdx_listen(const char* name, int* sock);
+int rs_fdx_send(const char* peer_name, const int* fds, int n_fds, const void* payload, size_t len);
+int rs_fdx_recv(int sock, int** fds, int* n_fds, void** payload, size_t* len);
+int rs_fdx_close(int fd);
+/* memory-aware stages across GPUs: one stage per call, barrier in between (caller) */
+int rs_exec_num_stages(const rs_exec_t* e, int* n);
+int rs_exec_run_stage(rs_exec_t* e, int stage, void* stream, int* launches);
 /* run the plan as memory-aware stages: dst ranks in the given order */
 int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n);
+/* the same order, grouped: cuts[i] == 1 starts a new stage at position i (cuts may be NULL) */
+int rs_exec_set_stage_groups(rs_exec_t* e, const int* dst_order, const int* cuts, int n);
 
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
 void rs_exec_destroy(rs_exec_t* e);

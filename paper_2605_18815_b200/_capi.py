@@ -86,7 +86,7 @@ class ScheduleSummary_t(C.Structure):
 
 class ArenaStats_t(C.Structure):
     _fields_ = [("physical_bytes", C.c_int64), ("a_bytes", C.c_int64), ("b_bytes", C.c_int64),
-                ("aliased_bytes", C.c_int64), ("chunks", C.c_int64)]
+                ("aliased_bytes", C.c_int64), ("chunks", C.c_int64), ("stage_groups", C.c_int64 * 2)]
 
 
 _lib = None
@@ -192,6 +192,26 @@ def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
 
 
 def _late_bindings(L):
+    vp, i64, P = C.c_void_p, C.c_int64, C.POINTER
+    for name, args in (
+        ("rs_arena_create_multi", [vp, vp, C.c_int, C.c_int, C.c_int, i64, i64, C.c_int, C.c_int, P(vp)]),
+        ("rs_memory_plan_ex", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int),
+                               P(C.c_int), C.c_int]),
+        ("rs_memory_min_groups", [vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, P(C.c_int), P(i64)]),
+        ("rs_arena_export", [vp, P(P(C.c_int)), P(C.c_int), P(vp), P(C.c_size_t)]),
+        ("rs_arena_import", [vp, P(C.c_int), C.c_int, vp, C.c_size_t]),
+        ("rs_fdx_listen", [C.c_char_p, P(C.c_int)]),
+        ("rs_fdx_send", [C.c_char_p, P(C.c_int), C.c_int, vp, C.c_size_t]),
+        ("rs_fdx_recv", [C.c_int, P(P(C.c_int)), P(C.c_int), P(vp), P(C.c_size_t)]),
+        ("rs_fdx_close", [C.c_int]),
+        ("rs_exec_num_stages", [vp, P(C.c_int)]),
+        ("rs_exec_run_stage", [vp, C.c_int, vp, P(C.c_int)]),
+        ("rs_exec_set_stage_groups", [vp, P(C.c_int), P(C.c_int), C.c_int]),
+        ("rs_arena_stage_cuts", [vp, C.c_int, P(C.c_int), C.c_int, P(C.c_int)]),
+    ):
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
     L.rs_plan_validate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                    C.POINTER(C.c_int64)]
     L.rs_plan_validate.restype = C.c_int

@@ -226,9 +226,18 @@ class Arena:
         A.check(A.lib().rs_arena_stats(self.h, C.byref(s)))
         return s
 
-    def bind(self, fwd: "Executor", bwd: Optional["Executor"] = None) -> None:
+    def stage_cuts(self, direction: int) -> List[int]:
+        """1 where a barrier must precede that stage position; the positions in between
+        share one stage (run concurrently)."""
+        out = (C.c_int * 1024)()
+        n = C.c_int()
+        A.check(A.lib().rs_arena_stage_cuts(self.h, direction, out, 1024, C.byref(n)))
+        return list(out[: n.value])
+
+    def bind(self, fwd: "Executor", bwd: Optional["Executor"] = None, cuts=None) -> None:
         """Bind A/B buffers into the forward (A->B) and backward (B->A) executors and
-        set their stage orders."""
+        set their stage orders, grouped by `cuts` (default: this arena's own; with
+        several GPUs pass the union over all GPUs, runtime.exchange_arena)."""
         for layout, nr in ((0, self.ab.summary.src_world), (1, self.ab.summary.dst_world)):
             for r in range(nr):
                 for b in range(6):
@@ -237,9 +246,14 @@ class Arena:
                         fwd.bind(layout, r, b, p, n)
                         if bwd is not None:
                             bwd.bind(1 - layout, r, b, p, n)
-        fwd.set_stages(self.stage_order(0))
-        if bwd is not None:
-            bwd.set_stages(self.stage_order(1))
+        cuts = cuts or [self.stage_cuts(0), self.stage_cuts(1)]
+        for d, ex in ((0, fwd), (1, bwd)):
+            if ex is None:
+                continue
+            order = self.stage_order(d)
+            cu = list(cuts[d]) if cuts[d] else [1] * len(order)
+            arr_o, arr_c = (C.c_int * len(order))(*order), (C.c_int * len(order))(*cu)
+            A.check(A.lib().rs_exec_set_stage_groups(ex.h, arr_o, arr_c, len(order)))
 
 
 def xor_peer(i: int, s: int, n: int) -> int:
@@ -341,12 +355,14 @@ def _exec_staged_methods():
 _exec_staged_methods()
 
 
-def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False):
-    """Host-only arena plan: (stats, simulated violations, stage orders)."""
+def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False,
+                n_gpus: int = 1, gpu: int = 0, groups: int = 0):
+    """Host-only arena plan of the buffers `gpu` hosts: (stats, simulated violations,
+    stage orders); `groups` coarsens the stage order (0 = one group per stage)."""
     st, viol = A.ArenaStats_t(), C.c_int64()
     oa, ob = (C.c_int * 1024)(), (C.c_int * 1024)()
-    A.check(A.lib().rs_memory_plan(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), C.byref(st), C.byref(viol),
-                                   oa, ob, 1024))
+    A.check(A.lib().rs_memory_plan_ex(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, groups,
+                                      C.byref(st), C.byref(viol), oa, ob, 1024))
     return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
 
 
@@ -368,3 +384,85 @@ def _plan_validate(self, drop: int = -1) -> List[str]:
 
 
 RoutingPlan.validate = _plan_validate
+
+
+# ---- multi-GPU arena, descriptor exchange, staged runs -------------------------
+
+def fdx_listen(name: str) -> int:
+    s = C.c_int()
+    A.check(A.lib().rs_fdx_listen(name.encode(), C.byref(s)))
+    return s.value
+
+
+def fdx_send(peer: str, fds: Sequence[int], payload: bytes) -> None:
+    arr = (C.c_int * max(1, len(fds)))(*fds)
+    A.check(A.lib().rs_fdx_send(peer.encode(), arr, len(fds), payload, len(payload)))
+
+
+def fdx_recv(sock: int):
+    p_fds, n, p_pl, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
+    A.check(A.lib().rs_fdx_recv(sock, C.byref(p_fds), C.byref(n), C.byref(p_pl), C.byref(ln)))
+    fds = [p_fds[i] for i in range(n.value)]
+    payload = C.string_at(p_pl.value, ln.value) if ln.value else b""
+    A.lib().rs_free(C.cast(p_fds, C.c_void_p))
+    A.lib().rs_free(p_pl)
+    return fds, payload
+
+
+def fdx_close(fd: int) -> None:
+    A.lib().rs_fdx_close(fd)
+
+
+def memory_min_groups(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
+                      chunk_bytes: int = 0, with_grads: bool = False):
+    """(fewest stage groups whose plan fits cap_bytes on `gpu` or -1, physical bytes)."""
+    g, phys = C.c_int(), C.c_int64()
+    A.check(A.lib().rs_memory_min_groups(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
+                                         cap_bytes, C.byref(g), C.byref(phys)))
+    return g.value, phys.value
+
+
+def _arena_multi(cls, ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, device: int,
+                 cap_bytes: int = 0, chunk_bytes: int = 0, with_grads: bool = False, groups: int = 0) -> "Arena":
+    self = cls.__new__(cls)
+    h = C.c_void_p()
+    A.check(A.lib().rs_arena_create_multi(ab.h, ba.h if ba else None, n_gpus, gpu, device, cap_bytes, chunk_bytes,
+                                          int(with_grads), groups, C.byref(h)))
+    self.h, self.ab, self.ba = h.value, ab, ba
+    return self
+
+
+def _arena_export(self):
+    p_fds, n, p_t, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
+    A.check(A.lib().rs_arena_export(self.h, C.byref(p_fds), C.byref(n), C.byref(p_t), C.byref(ln)))
+    fds = [p_fds[i] for i in range(n.value)]
+    table = C.string_at(p_t.value, ln.value)
+    A.lib().rs_free(C.cast(p_fds, C.c_void_p))
+    A.lib().rs_free(p_t)
+    return fds, table
+
+
+def _arena_import(self, fds: Sequence[int], table: bytes) -> None:
+    arr = (C.c_int * max(1, len(fds)))(*fds)
+    A.check(A.lib().rs_arena_import(self.h, arr, len(fds), table, len(table)))
+
+
+Arena.multi = classmethod(_arena_multi)
+Arena.export = _arena_export
+Arena.import_peer = _arena_import
+
+
+def _exec_num_stages(self) -> int:
+    n = C.c_int()
+    A.check(A.lib().rs_exec_num_stages(self.h, C.byref(n)))
+    return n.value
+
+
+def _exec_run_stage(self, stage: int, stream: int = 0) -> int:
+    n = C.c_int()
+    A.check(A.lib().rs_exec_run_stage(self.h, stage, C.c_void_p(stream), C.byref(n)))
+    return n.value
+
+
+Executor.num_stages = _exec_num_stages
+Executor.run_stage = _exec_run_stage

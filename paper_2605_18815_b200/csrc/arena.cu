@@ -1,8 +1,11 @@
-// Arena: VMM-backed old/new layouts with plan-time eager-free aliasing (arena.hpp).
+// Arena: VMM-backed old/new layouts with plan-time eager-free aliasing (arena.hpp),
+// on one GPU or across GPUs (POSIX-FD export of the physical allocations).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cstring>
 #include <limits>
 #include <map>
 
@@ -23,6 +26,8 @@ struct Drv {
     CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
     CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
     CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+    CUresult (*export_fd)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
+    CUresult (*import_fd)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
 
     static const Drv& get() {
         static Drv d = [] {
@@ -42,6 +47,8 @@ struct Drv {
             load("cuMemUnmap", x.unmap);
             load("cuMemSetAccess", x.set_access);
             load("cuMemGetAllocationGranularity", x.granularity);
+            load("cuMemExportToShareableHandle", x.export_fd);
+            load("cuMemImportFromShareableHandle", x.import_fd);
             return x;
         }();
         return d;
@@ -52,18 +59,50 @@ void drv_check(CUresult r, const char* what) {
     if (r != CUDA_SUCCESS) throw exec::CudaError(strfmt("%s failed (CUresult %d)", what, static_cast<int>(r)));
 }
 
+CUmemAllocationProp device_prop(int device, bool shareable) {
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    if (shareable) prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    return prop;
+}
+
+// export table entry: layout, rank, buf, number of handles, bytes, reserved, piece size
+struct Entry {
+    std::int32_t layout, rank, buf, nh;
+    std::int64_t bytes, reserved, piece;
+};
+
 }  // namespace
 
-Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConfig& cfg, bool with_grads) : cfg_(cfg) {
+Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConfig& cfg, bool with_grads, int n_gpus,
+             int gpu)
+    : cfg_(cfg), n_gpus_(n_gpus) {
     const Drv& D = Drv::get();
     if (cudaSetDevice(cfg.device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
     const std::int64_t C = cfg.chunk_bytes;
-    const MemoryPlan mp = plan_memory(ab, ba, C, with_grads);
+    std::int64_t cap = cfg.cap_bytes;
+    if (cap <= 0) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        cap = static_cast<std::int64_t>(fr) - (1ll << 30);
+    }
+    int groups = cfg.groups;
+    if (groups <= 0) {
+        std::int64_t need = 0;
+        groups = min_stage_groups(ab, ba, C, with_grads, n_gpus, gpu, cap, &need);
+        if (groups < 0)
+            throw exec::BudgetError(strfmt("infeasible budget: memory plan needs %.2f GB of HBM on GPU %d, cap %.2f GB",
+                                           need / 1e9, gpu, cap / 1e9));
+    }
+    const MemoryPlan mp = plan_memory(ab, ba, C, with_grads, n_gpus, gpu, groups);
+    const bool shareable = n_gpus > 1;
     order_[0] = mp.order[0];
     order_[1] = mp.order[1];
+    cut_[0] = mp.cut[0];
+    cut_[1] = mp.cut[1];
     stats_ = mp.stats;
-    const int nphys = mp.nphys;
-    const bool small_direct = true;
     for (int l = 0; l < 2; ++l) {
         nranks_[l] = l == 0 ? ab.src_cfg.world_size() : ab.dst_cfg.world_size();
         bufs_[l].resize(mp.bufs[l].size());
@@ -71,27 +110,19 @@ Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConf
             bufs_[l][i].bytes = mp.bufs[l][i].bytes;
             bufs_[l][i].reserved = mp.bufs[l][i].reserved;
             bufs_[l][i].phys = mp.bufs[l][i].phys;
+            bufs_[l][i].remote = mp.bufs[l][i].remote;
         }
     }
-    std::int64_t cap = cfg.cap_bytes;
-    if (cap <= 0) {
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
-        cap = static_cast<std::int64_t>(fr) - (1ll << 30);
-    }
     if (stats_.physical_bytes > cap)
-        throw exec::BudgetError(strfmt("infeasible budget: memory plan needs %.2f GB of HBM, cap %.2f GB",
-                                 stats_.physical_bytes / 1e9, cap / 1e9));
+        throw exec::BudgetError(strfmt("infeasible budget: memory plan needs %.2f GB of HBM on GPU %d, cap %.2f GB",
+                                       stats_.physical_bytes / 1e9, gpu, cap / 1e9));
     // ---- create and map
-    CUmemAllocationProp prop = {};
-    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    prop.location.id = cfg.device;
+    const CUmemAllocationProp prop = device_prop(cfg.device, shareable);
     size_t gran = 0;
     drv_check(D.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
     if (C % static_cast<std::int64_t>(gran)) throw ConfigError("arena chunk is not a multiple of the VMM granularity");
-    handles_.resize(static_cast<size_t>(nphys));
-    for (int i = 0; i < nphys; ++i) {
+    handles_.resize(static_cast<size_t>(mp.nphys));
+    for (int i = 0; i < mp.nphys; ++i) {
         CUmemGenericAllocationHandle h;
         drv_check(D.create(&h, static_cast<size_t>(C), &prop, 0), "cuMemCreate");
         handles_[static_cast<size_t>(i)] = h;
@@ -101,39 +132,137 @@ Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConf
     acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     for (int l = 0; l < 2; ++l)
         for (BufMap& m : bufs_[l]) {
-            if (m.bytes == 0) continue;
-            if (small_direct && m.bytes < C / 4) {
-                void* p = nullptr;
-                if (cudaMalloc(&p, static_cast<size_t>(m.bytes)) != cudaSuccess) throw exec::CudaError("cudaMalloc failed");
-                m.va = reinterpret_cast<std::uint64_t>(p);
-                m.reserved = 0;
+            if (m.bytes == 0 || m.remote) continue;
+            if (m.reserved == 0) {  // small buffer: its own allocation
+                if (!shareable) {
+                    void* p = nullptr;
+                    if (cudaMalloc(&p, static_cast<size_t>(m.bytes)) != cudaSuccess) throw exec::CudaError("cudaMalloc failed");
+                    m.va = reinterpret_cast<std::uint64_t>(p);
+                    continue;
+                }
+                const std::int64_t g = static_cast<std::int64_t>(gran);
+                const std::int64_t sz = (m.bytes + g - 1) / g * g;
+                CUmemGenericAllocationHandle h;
+                drv_check(D.create(&h, static_cast<size_t>(sz), &prop, 0), "cuMemCreate");
+                CUdeviceptr va = 0;
+                drv_check(D.reserve(&va, static_cast<size_t>(sz), gran, 0, 0), "cuMemAddressReserve");
+                drv_check(D.map(va, static_cast<size_t>(sz), 0, h, 0), "cuMemMap");
+                drv_check(D.set_access(va, static_cast<size_t>(sz), &acc, 1), "cuMemSetAccess");
+                m.va = va;
+                m.reserved = sz;
+                m.own_handle = true;
+                m.mapped_vmm = true;
+                m.handle = h;
                 continue;
             }
             CUdeviceptr va = 0;
             drv_check(D.reserve(&va, static_cast<size_t>(m.reserved), static_cast<size_t>(C), 0, 0), "cuMemAddressReserve");
             m.va = va;
+            m.mapped_vmm = true;
             for (size_t c = 0; c < m.phys.size(); ++c)
                 drv_check(D.map(va + c * static_cast<std::uint64_t>(C), static_cast<size_t>(C), 0,
                                 handles_[static_cast<size_t>(m.phys[c])], 0), "cuMemMap");
             drv_check(D.set_access(va, static_cast<size_t>(m.reserved), &acc, 1), "cuMemSetAccess");
         }
-    stats_.b_bytes = 0;
-    for (const BufMap& m : bufs_[1]) stats_.b_bytes += m.bytes;
+}
+
+void Arena::export_local(std::vector<int>* fds, std::vector<std::uint8_t>* table) const {
+    const Drv& D = Drv::get();
+    if (n_gpus_ < 2) throw ConfigError("arena export needs a multi-GPU arena");
+    fds->clear();
+    table->clear();
+    // physical chunks first (indices = chunk ids), then the small buffers' own handles
+    for (std::uint64_t h : handles_) {
+        int fd = -1;
+        drv_check(D.export_fd(&fd, h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
+        fds->push_back(fd);
+    }
+    auto put = [table](const void* p, size_t n) {
+        const auto* c = static_cast<const std::uint8_t*>(p);
+        table->insert(table->end(), c, c + n);
+    };
+    const std::int64_t nchunk_handles = static_cast<std::int64_t>(handles_.size());
+    put(&nchunk_handles, sizeof nchunk_handles);
+    for (int l = 0; l < 2; ++l)
+        for (size_t i = 0; i < bufs_[l].size(); ++i) {
+            const BufMap& m = bufs_[l][i];
+            if (m.remote || m.bytes == 0) continue;
+            Entry e{l, static_cast<std::int32_t>(i / exec::kNumBufs), static_cast<std::int32_t>(i % exec::kNumBufs), 0,
+                    m.bytes, m.reserved, 0};
+            std::vector<std::int32_t> idx;
+            if (m.own_handle) {
+                int fd = -1;
+                drv_check(D.export_fd(&fd, m.handle, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+                          "cuMemExportToShareableHandle");
+                idx.push_back(static_cast<std::int32_t>(fds->size()));
+                fds->push_back(fd);
+                e.piece = m.reserved;
+            } else {
+                for (int p : m.phys) idx.push_back(p);
+                e.piece = cfg_.chunk_bytes;
+            }
+            e.nh = static_cast<std::int32_t>(idx.size());
+            put(&e, sizeof e);
+            put(idx.data(), idx.size() * sizeof(std::int32_t));
+        }
+}
+
+void Arena::import_peer(const std::vector<int>& fds, const std::vector<std::uint8_t>& table) {
+    const Drv& D = Drv::get();
+    if (cudaSetDevice(cfg_.device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    std::vector<CUmemGenericAllocationHandle> hs(fds.size());
+    for (size_t i = 0; i < fds.size(); ++i) {
+        drv_check(D.import_fd(&hs[i], reinterpret_cast<void*>(static_cast<std::intptr_t>(fds[i])),
+                              CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR),
+                  "cuMemImportFromShareableHandle");
+        ::close(fds[i]);  // the imported handle keeps the allocation alive
+        imported_.push_back(hs[i]);
+    }
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = cfg_.device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    size_t at = sizeof(std::int64_t);
+    while (at + sizeof(Entry) <= table.size()) {
+        Entry e;
+        std::memcpy(&e, table.data() + at, sizeof e);
+        at += sizeof e;
+        std::vector<std::int32_t> idx(static_cast<size_t>(e.nh));
+        std::memcpy(idx.data(), table.data() + at, idx.size() * sizeof(std::int32_t));
+        at += idx.size() * sizeof(std::int32_t);
+        BufMap& m = bufs_[e.layout].at(static_cast<size_t>(e.rank) * exec::kNumBufs + e.buf);
+        CUdeviceptr va = 0;
+        drv_check(D.reserve(&va, static_cast<size_t>(e.reserved), static_cast<size_t>(e.piece), 0, 0), "cuMemAddressReserve");
+        for (size_t c = 0; c < idx.size(); ++c)
+            drv_check(D.map(va + c * static_cast<std::uint64_t>(e.piece), static_cast<size_t>(e.piece), 0,
+                            hs.at(static_cast<size_t>(idx[c])), 0),
+                      "cuMemMap");
+        drv_check(D.set_access(va, static_cast<size_t>(e.reserved), &acc, 1), "cuMemSetAccess");
+        m.va = va;
+        m.bytes = e.bytes;
+        peer_maps_.push_back({va, e.reserved});
+    }
 }
 
 Arena::~Arena() {
     const Drv& D = Drv::get();
     cudaSetDevice(cfg_.device);
     cudaDeviceSynchronize();
+    for (const auto& pm : peer_maps_) {
+        D.unmap(pm.first, static_cast<size_t>(pm.second));
+        D.addr_free(pm.first, static_cast<size_t>(pm.second));
+    }
+    for (std::uint64_t h : imported_) D.release(h);
     for (int l = 0; l < 2; ++l)
         for (BufMap& m : bufs_[l]) {
-            if (!m.va) continue;
-            if (m.reserved == 0) {
+            if (!m.va || m.remote) continue;
+            if (!m.mapped_vmm) {
                 cudaFree(reinterpret_cast<void*>(m.va));
                 continue;
             }
             D.unmap(m.va, static_cast<size_t>(m.reserved));
             D.addr_free(m.va, static_cast<size_t>(m.reserved));
+            if (m.own_handle) D.release(m.handle);
         }
     for (std::uint64_t h : handles_) D.release(h);
 }

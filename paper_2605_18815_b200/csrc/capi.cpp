@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "reshard/arena.hpp"
+#include "reshard/fdx.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
 #include "reshard/schedule.hpp"
@@ -709,6 +710,24 @@ int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n) {
     });
 }
 
+int rs_exec_set_stage_groups(rs_exec_t* e, const int* dst_order, const int* cuts, int n) {
+    return guarded([&] {
+        e->ex->set_stage_order(std::vector<int>(dst_order, dst_order + n),
+                               cuts ? std::vector<int>(cuts, cuts + n) : std::vector<int>());
+        return RS_OK;
+    });
+}
+
+int rs_arena_stage_cuts(const rs_arena_t* a, int dir, int* out, int cap, int* n) {
+    return guarded([&] {
+        if (dir < 0 || dir > 1) throw ConfigError("bad direction");
+        const std::vector<int>& c = a->a->stage_cuts(dir);
+        *n = static_cast<int>(c.size());
+        for (int i = 0; i < *n && i < cap; ++i) out[i] = c[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
 int rs_arena_create(const rs_plan_t* ab, const rs_plan_t* ba, int device, int64_t cap_bytes, int64_t chunk_bytes,
                     int with_grads, rs_arena_t** out) {
     return guarded([&] {
@@ -727,6 +746,99 @@ int rs_arena_create(const rs_plan_t* ab, const rs_plan_t* ba, int device, int64_
 }
 
 void rs_arena_destroy(rs_arena_t* a) { delete a; }
+
+int rs_arena_create_multi(const rs_plan_t* ab, const rs_plan_t* ba, int n_gpus, int gpu, int device, int64_t cap_bytes,
+                          int64_t chunk_bytes, int with_grads, int groups, rs_arena_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw exec::CudaError("no CUDA device");
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad arena placement");
+        mem::ArenaConfig cfg;
+        cfg.device = device;
+        cfg.cap_bytes = cap_bytes;
+        if (chunk_bytes > 0) cfg.chunk_bytes = chunk_bytes;
+        cfg.groups = groups;
+        auto a = std::make_unique<rs_arena>();
+        a->a = std::make_unique<mem::Arena>(ab->core, ba ? &ba->core : nullptr, cfg, with_grads != 0, n_gpus, gpu);
+        *out = a.release();
+        return RS_OK;
+    });
+}
+
+int rs_arena_export(const rs_arena_t* a, int** fds, int* n_fds, void** table, size_t* table_len) {
+    return guarded([&] {
+        std::vector<int> f;
+        std::vector<std::uint8_t> t;
+        a->a->export_local(&f, &t);
+        *fds = static_cast<int*>(std::malloc(sizeof(int) * (f.empty() ? 1 : f.size())));
+        *table = std::malloc(t.empty() ? 1 : t.size());
+        if (!*fds || !*table) throw std::bad_alloc();
+        std::memcpy(*fds, f.data(), sizeof(int) * f.size());
+        std::memcpy(*table, t.data(), t.size());
+        *n_fds = static_cast<int>(f.size());
+        *table_len = t.size();
+        return RS_OK;
+    });
+}
+
+int rs_arena_import(rs_arena_t* a, const int* fds, int n_fds, const void* table, size_t table_len) {
+    return guarded([&] {
+        const auto* t = static_cast<const std::uint8_t*>(table);
+        a->a->import_peer(std::vector<int>(fds, fds + n_fds), std::vector<std::uint8_t>(t, t + table_len));
+        return RS_OK;
+    });
+}
+
+int rs_fdx_listen(const char* name, int* sock) {
+    return guarded([&] {
+        *sock = fdx::listen_on(name);
+        return RS_OK;
+    });
+}
+
+int rs_fdx_send(const char* peer_name, const int* fds, int n_fds, const void* payload, size_t len) {
+    return guarded([&] {
+        const auto* p = static_cast<const std::uint8_t*>(payload);
+        fdx::send_fds(peer_name, std::vector<int>(fds, fds + n_fds), std::vector<std::uint8_t>(p, p + len));
+        return RS_OK;
+    });
+}
+
+int rs_fdx_recv(int sock, int** fds, int* n_fds, void** payload, size_t* len) {
+    return guarded([&] {
+        std::vector<std::uint8_t> pl;
+        const std::vector<int> f = fdx::recv_fds(sock, &pl);
+        *fds = static_cast<int*>(std::malloc(sizeof(int) * (f.empty() ? 1 : f.size())));
+        *payload = std::malloc(pl.empty() ? 1 : pl.size());
+        if (!*fds || !*payload) throw std::bad_alloc();
+        std::memcpy(*fds, f.data(), sizeof(int) * f.size());
+        std::memcpy(*payload, pl.data(), pl.size());
+        *n_fds = static_cast<int>(f.size());
+        *len = pl.size();
+        return RS_OK;
+    });
+}
+
+int rs_fdx_close(int fd) {
+    fdx::close_fd(fd);
+    return RS_OK;
+}
+
+int rs_exec_num_stages(const rs_exec_t* e, int* n) {
+    return guarded([&] {
+        *n = e->ex->num_stages();
+        return RS_OK;
+    });
+}
+
+int rs_exec_run_stage(rs_exec_t* e, int stage, void* stream, int* launches) {
+    return guarded([&] {
+        const int k = e->ex->run_stage(stage, static_cast<cudaStream_t>(stream));
+        if (launches) *launches = k;
+        return RS_OK;
+    });
+}
 
 int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** dptr, int64_t* bytes) {
     return guarded([&] {
@@ -747,17 +859,31 @@ int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n
     });
 }
 
-int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, rs_arena_stats_t* stats,
-                   int64_t* violations, int* order_ab, int* order_ba, int cap) {
+int rs_memory_min_groups(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                         int gpu, int64_t cap_bytes, int* groups, int64_t* physical_bytes) {
+    return guarded([&] {
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad arena placement");
+        *groups = mem::min_stage_groups(ab->core, ba ? &ba->core : nullptr, chunk_bytes > 0 ? chunk_bytes : (32ll << 20),
+                                        with_grads != 0, n_gpus, gpu, cap_bytes, physical_bytes);
+        return RS_OK;
+    });
+}
+
+int rs_memory_plan_ex(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus, int gpu,
+                      int groups, rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap) {
     return guarded([&] {
         const mem::MemoryPlan mp = mem::plan_memory(ab->core, ba ? &ba->core : nullptr,
-                                                    chunk_bytes > 0 ? chunk_bytes : (32ll << 20), with_grads != 0);
+                                                    chunk_bytes > 0 ? chunk_bytes : (32ll << 20), with_grads != 0,
+                                                    n_gpus, gpu, groups);
         stats->physical_bytes = mp.stats.physical_bytes;
         stats->a_bytes = mp.stats.a_bytes;
         stats->b_bytes = mp.stats.b_bytes;
         stats->aliased_bytes = mp.stats.aliased_bytes;
         stats->chunks = mp.stats.chunks;
         *violations = mem::simulate_memory_plan(mp, ab->core, ba ? &ba->core : nullptr);
+        stats->stage_groups[0] = stats->stage_groups[1] = 0;
+        for (int d = 0; d < 2; ++d)
+            for (int c : mp.cut[d]) stats->stage_groups[d] += c;
         for (int d = 0; d < 2; ++d) {
             int* o = d == 0 ? order_ab : order_ba;
             if (!o) continue;
@@ -765,6 +891,11 @@ int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes
         }
         return RS_OK;
     });
+}
+
+int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, rs_arena_stats_t* stats,
+                   int64_t* violations, int* order_ab, int* order_ba, int cap) {
+    return rs_memory_plan_ex(ab, ba, chunk_bytes, with_grads, 1, 0, 0, stats, violations, order_ab, order_ba, cap);
 }
 
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
@@ -775,6 +906,10 @@ int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
         out->b_bytes = s.b_bytes;
         out->aliased_bytes = s.aliased_bytes;
         out->chunks = s.chunks;
+        for (int d = 0; d < 2; ++d) {
+            out->stage_groups[d] = 0;
+            for (int c : a->a->stage_cuts(d)) out->stage_groups[d] += c;
+        }
         return RS_OK;
     });
 }

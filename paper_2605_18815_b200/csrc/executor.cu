@@ -352,18 +352,23 @@ Executor::~Executor() {
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
 
-void Executor::set_stage_order(const std::vector<int>& dst_order) {
+void Executor::set_stage_order(const std::vector<int>& dst_order, const std::vector<int>& cuts) {
     const int nd = P_.dst_cfg.world_size();
     if (dst_order.empty()) {
         stage_of_dst_.clear();
         return;
     }
     if (static_cast<int>(dst_order.size()) != nd) throw ConfigError("stage order must list every destination rank once");
+    if (!cuts.empty() && cuts.size() != dst_order.size()) throw ConfigError("stage cuts must match the stage order");
     std::vector<int> pos(static_cast<size_t>(nd), -1);
+    int group = -1;
     for (size_t s = 0; s < dst_order.size(); ++s) {
         const int j = dst_order[s];
         if (j < 0 || j >= nd || pos[static_cast<size_t>(j)] >= 0) throw ConfigError("bad stage order");
-        pos[static_cast<size_t>(j)] = static_cast<int>(s);
+        // without cuts every position is its own stage; with cuts, positions between two
+        // cuts share one stage (they may run concurrently)
+        if (cuts.empty() || s == 0 || cuts[s]) ++group;
+        pos[static_cast<size_t>(j)] = group;
     }
     stage_of_dst_ = pos;
     prepared_ = false;
@@ -565,6 +570,7 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
     const Tile* base = static_cast<const Tile*>(dev);
     for (const Group& g : groups) {
         if (key_mod > 0 && g.key % key_mod != key_rem) continue;
+        if (key_mod < 0 && g.key != key_rem) continue;  // exact key (one memory-aware stage)
         const int n = g.count;
         const int grid = std::min(n, grid_cap);
         const Tile* t = base + g.begin;
@@ -730,6 +736,17 @@ int Executor::run(cudaStream_t stream) {
     RS_CUDA(cudaEventRecord(ev_join_, aux_));
     RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
     return n;
+}
+
+int Executor::num_stages() const {
+    return stage_of_dst_.empty() ? 1 : *std::max_element(stage_of_dst_.begin(), stage_of_dst_.end()) + 1;
+}
+
+int Executor::run_stage(int stage, cudaStream_t stream) {
+    if (!prepared_) throw ConfigError("run before prepare");
+    if (split_remote_ || !ce_ops_.empty()) throw ConfigError("run_stage needs the single mixed launch (no CE offload)");
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, has_remote_ ? remote_bulk_ : use_bulk_, -1, stage);
 }
 
 std::int64_t Executor::channel_bytes(int src_phys, int dst_phys) const {

@@ -29,6 +29,7 @@ struct ArenaConfig {
     int device = 0;
     std::int64_t cap_bytes = 0;             // physical budget; 0 -> free memory minus 1 GiB
     std::int64_t chunk_bytes = 32ll << 20;  // physical chunk (multiple of the VMM granularity)
+    int groups = 0;  // concurrency groups of the stage order; 0 -> fewest that fit the cap
 };
 
 struct ArenaStats {
@@ -44,17 +45,31 @@ std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<e
 /// Host-side memory plan (no driver calls; CPU-testable).
 struct BufPlan {
     std::int64_t bytes = 0, reserved = 0;
-    bool direct = false;     // small buffer: plain allocation, never aliased
+    bool direct = false;     // small buffer: own allocation, never aliased (or hosted elsewhere)
+    bool remote = false;     // hosted by another GPU (multi-GPU plans)
     std::vector<int> phys;   // physical chunk per VA chunk
 };
 struct MemoryPlan {
     std::int64_t chunk = 0;
     std::vector<BufPlan> bufs[2];  // [layout][rank * kNumBufs + buf]
     std::vector<int> order[2];     // stage orders (dst ranks) A->B, B->A
+    std::vector<int> cut[2];       // per stage position: 1 = a barrier precedes it
     int nphys = 0;
     ArenaStats stats;
 };
-MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads);
+/// Plan the buffers hosted by `gpu` (contiguous-block placement over n_gpus). Stage
+/// orders are global, so with n_gpus > 1 every stage boundary is a cross-GPU barrier.
+/// `groups` (0 = one per stage) coarsens the stage order into that many concurrency
+/// groups: fewer barriers, less aliasing.
+MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads,
+                       int n_gpus = 1, int gpu = 0, int groups = 0);
+/// fewest groups whose plan fits `cap` bytes on `gpu` (-1: none does); the physical
+/// bytes of the last plan tried in *physical
+int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads, int n_gpus,
+                     int gpu, std::int64_t cap, std::int64_t* physical);
+/// Group consecutive stages that may run concurrently (fills mp.cut): a barrier only
+/// where a stage overwrites a chunk an earlier stage of the running group still reads.
+void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba);
 /// Replays the staged execution chunk by chunk (A->B, then B->A) tracking which
 /// logical chunk each physical chunk holds; counts reads of clobbered data and
 /// same-stage read/write races. 0 == the aliasing is safe.
@@ -62,31 +77,44 @@ std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab
 
 class Arena {
 public:
-    /// ab: A->B; ba: B->A on the same buffers (or nullptr for one-way). All virtual
-    /// ranks must be placed on this GPU (n_gpus == 1).
-    Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConfig& cfg, bool with_grads);
+    /// ab: A->B; ba: B->A on the same buffers (or nullptr for one-way). With n_gpus > 1
+    /// this GPU maps the buffers it hosts; peers' buffers arrive through import_peer().
+    Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConfig& cfg, bool with_grads, int n_gpus = 1,
+          int gpu = 0);
     ~Arena();
     Arena(const Arena&) = delete;
     Arena& operator=(const Arena&) = delete;
 
-    /// layout 0 = A (src of ab), 1 = B (dst of ab)
+    /// layout 0 = A (src of ab), 1 = B (dst of ab); remote buffers once imported
     void* ptr(int layout, int rank, int buf) const;
     std::int64_t bytes(int layout, int rank, int buf) const;
     const std::vector<int>& stage_order(int dir) const { return order_[dir]; }
+    const std::vector<int>& stage_cuts(int dir) const { return cut_[dir]; }
     const ArenaStats& stats() const { return stats_; }
+
+    /// POSIX-FD export of every physical allocation backing this GPU's buffers, with a
+    /// table of how the buffers map them (the caller passes both to the peers, fdx).
+    void export_local(std::vector<int>* fds, std::vector<std::uint8_t>* table) const;
+    /// map a peer's buffers into this process's address space (consumes the fds)
+    void import_peer(const std::vector<int>& fds, const std::vector<std::uint8_t>& table);
 
 private:
     struct BufMap {
         std::uint64_t va = 0;
         std::int64_t bytes = 0, reserved = 0;
-        std::vector<int> phys;  // physical chunk per VA chunk
+        std::vector<int> phys;  // physical chunk per VA chunk (local buffers)
+        bool remote = false, mapped_vmm = false, own_handle = false;
+        std::uint64_t handle = 0;  // own allocation (small buffers, multi-GPU mode)
     };
     std::vector<BufMap> bufs_[2];  // [layout][rank * kNumBufs + buf]
-    std::vector<std::uint64_t> handles_;
-    std::vector<int> order_[2];
+    std::vector<std::uint64_t> handles_;           // local physical chunks
+    std::vector<std::uint64_t> imported_;          // peers' physical allocations
+    std::vector<std::pair<std::uint64_t, std::int64_t>> peer_maps_;  // (va, reserved) to unmap
+    std::vector<int> order_[2], cut_[2];
     ArenaConfig cfg_;
     ArenaStats stats_;
     int nranks_[2] = {0, 0};
+    int n_gpus_ = 1;
 };
 
 }  // namespace mem

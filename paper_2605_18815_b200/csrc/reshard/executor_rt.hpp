@@ -93,7 +93,7 @@ public:
     int gpu_of_phys(int phys) const;
     /// memory-aware stages: destination ranks in execution order, one launch group
     /// per stage (a stage starts after all reads of earlier stages completed)
-    void set_stage_order(const std::vector<int>& dst_order);
+    void set_stage_order(const std::vector<int>& dst_order, const std::vector<int>& cuts = {});
     /// cudaMalloc every unbound buffer of the virtual ranks placed on this GPU
     void alloc();
     /// use a caller-owned device buffer (side 0 src / 1 dst)
@@ -111,6 +111,10 @@ public:
     void prepare(bool staged = false);
     /// launch the transition (fused part); returns the number of kernel launches
     int run(cudaStream_t stream);
+    /// memory-aware stages across GPUs: launch one stage; the caller puts a cross-GPU
+    /// barrier between stages (a stage's writes may land in chunks freed by the last one)
+    int run_stage(int stage, cudaStream_t stream);
+    int num_stages() const;
     /// staged mode: bytes of the (src phys -> dst phys) channel, pack into / unpack from
     /// a contiguous buffer (same layout on both sides, derived from the plan)
     std::int64_t channel_bytes(int src_phys, int dst_phys) const;

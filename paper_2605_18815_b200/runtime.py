@@ -149,6 +149,98 @@ class StagedTransition:
                 self._exchange(chans, stream, per_op=True)
 
 
+def global_stage_cuts(arena, world: int):
+    """A barrier is needed before a stage if ANY GPU's aliasing needs it (each GPU plans
+    only the chunks it hosts): element-wise max of the cuts over all ranks."""
+    cuts = [arena.stage_cuts(0), arena.stage_cuts(1)]
+    if world < 2:
+        return cuts
+    import torch
+    import torch.distributed as dist
+    n0 = len(cuts[0])
+    t = torch.tensor(cuts[0] + cuts[1], dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    v = t.tolist()
+    return [v[:n0], v[n0:]]
+
+
+def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
+    """Share every GPU's arena buffers with every other GPU: POSIX descriptors of the
+    VMM allocations over Unix sockets (fdx), mapped by the receiver (import_peer).
+    Bind executors afterwards with arena.bind(fwd, bwd, global_stage_cuts(arena, world))."""
+    import threading
+
+    import torch.distributed as dist
+
+    from .api import fdx_close, fdx_listen, fdx_recv, fdx_send
+    if world < 2:
+        return
+    sock = fdx_listen(f"reshard-{tag}-{rank}")
+    dist.barrier()
+    errors = []
+
+    def receive():
+        try:
+            for _ in range(world - 1):
+                fds, table = fdx_recv(sock)
+                arena.import_peer(fds, table)
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    t = threading.Thread(target=receive, name="arena-import")
+    t.start()
+    for peer in range(world):
+        if peer == rank:
+            continue
+        fds, table = arena.export()
+        try:
+            fdx_send(f"reshard-{tag}-{peer}", fds, table)
+        finally:
+            for fd in fds:
+                os.close(fd)
+    t.join()
+    fdx_close(sock)
+    if errors:
+        raise errors[0]
+    dist.barrier()
+
+
+def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: int, device: int, cap_bytes: int = 0,
+                 tag: str = "0", chunk_bytes: int = 0):
+    """Memory-aware arena over `world` GPUs: every GPU plans the buffers it hosts with the
+    same stage grouping (the fewest groups that fit every GPU's cap: max over ranks),
+    then the buffers are shared (exchange_arena). Returns (arena, global stage cuts)."""
+    import torch
+    import torch.distributed as dist
+
+    from .api import Arena, memory_min_groups
+    if cap_bytes <= 0:
+        cap_bytes = torch.cuda.mem_get_info(device)[0] - (1 << 30)
+    k, need = memory_min_groups(ab, ba, world, rank, cap_bytes, chunk_bytes)
+    if world > 1:
+        t = torch.tensor([k if k > 0 else 1 << 20], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        k = int(t.item())
+    if k <= 0 or k >= 1 << 20:
+        raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs {need / 1e9:.2f} GB, "
+                                              f"cap {cap_bytes / 1e9:.2f} GB)")
+    arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k)
+    exchange_arena(arena, rank, world, tag)
+    return arena, global_stage_cuts(arena, world)
+
+
+def run_stages(ex: Executor, stream: int, world: int) -> None:
+    """Memory-aware stages across GPUs: a stage may write chunks that the previous stage
+    read on another GPU, so every stage boundary is a global barrier."""
+    import torch
+    import torch.distributed as dist
+    for s in range(ex.num_stages()):
+        ex.run_stage(s, stream)
+        if world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+
+
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:
     n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
     return [r for r in range(n) if ex.buffer(side, r, A.BUF_PARAM)[2] == ex.gpu]

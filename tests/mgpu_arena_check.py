@@ -1,0 +1,70 @@
+"""Multi-GPU memory-aware arena (run under torchrun): old and new layouts of every GPU's
+virtual ranks in VMM with eager-free aliasing, shared with the peers through POSIX
+descriptors, memory-aware stages with a global barrier between them. Round trips must
+stay bit-exact and each GPU must use less physical HBM than old + new.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_arena_check.py [layers]
+"""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env, exchange_arena, global_stage_cuts, run_stages  # noqa: E402
+
+
+def main():
+    layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seed = 0xA7E4
+    fails = 0
+    # groups 0: one group per stage (most aliasing); 2: the stage order in two halves
+    for sc, groups in ((S.config2(layers), 0), (S.config2(layers), 2), (S.config3(2)[0], 0)):
+        ab = RoutingPlan.from_scenario(sc)
+        ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+        arena = Arena.multi(ab, ba, world, rank, local, chunk_bytes=64 << 20, groups=groups or 64)
+        exchange_arena(arena, rank, world, tag=f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{groups}")
+        fwd = Transition(ab, world, rank, local, alloc=False)
+        bwd = Transition(ba, world, rank, local, alloc=False)
+        arena.bind(fwd.ex, bwd.ex, global_stage_cuts(arena, world))
+        fwd.ex.prepare()
+        bwd.ex.prepare()
+        fwd.ex.fill(A.SIDE_SRC, seed)
+        torch.cuda.synchronize()
+        dist.barrier()
+        bad = []
+        for _ in range(2):
+            run_stages(fwd.ex, 0, world)
+            torch.cuda.synchronize()
+            dist.barrier()
+            bad.append(fwd.ex.verify(A.SIDE_DST, seed)[0])
+            run_stages(bwd.ex, 0, world)
+            torch.cuda.synchronize()
+            dist.barrier()
+            bad.append(bwd.ex.verify(A.SIDE_DST, seed)[0])
+        st = arena.stats()
+        print(f"[rank {rank}] {sc.name} groups={groups}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, physical {st.physical_bytes/1e9:.2f} GB "
+              f"(old {st.a_bytes/1e9:.2f} + new {st.b_bytes/1e9:.2f}, aliased {st.aliased_bytes/1e9:.2f})", flush=True)
+        fails += sum(1 for b in bad if b)
+        del fwd, bwd, arena
+        torch.cuda.synchronize()
+        dist.barrier()
+    t = torch.tensor([fails], device="cuda")
+    dist.all_reduce(t)
+    dist.destroy_process_group()
+    if rank == 0:
+        print("ARENA_OK" if t.item() == 0 else f"ARENA_FAIL {t.item()}", flush=True)
+    sys.exit(0 if t.item() == 0 else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,3 +66,52 @@ def test_placement_single_gpu_is_all_local():
     st = plan.placement(1, 0)
     assert st.out_bytes == 0 and st.in_bytes == 0
     assert st.local_bytes == plan.bytes_moved() - 7 * 64 + plan.bytes_retained() + 8 * 64
+
+
+def _fdx_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_18815_b200.api import fdx_close, fdx_listen, fdx_recv, fdx_send
+    sock = fdx_listen(f"reshard-test-{port}-{rank}")
+    dist.barrier()
+    if rank == 0:
+        r, w = os.pipe()
+        os.write(w, b"descriptor crossed the process boundary")
+        os.close(w)
+        fdx_send(f"reshard-test-{port}-1", [r] * 300, b"payload")  # > one SCM_RIGHTS batch
+        os.close(r)
+    else:
+        fds, payload = fdx_recv(sock)
+        q.put((len(fds), payload, os.read(fds[0], 100)))
+        for fd in fds:
+            os.close(fd)
+    fdx_close(sock)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_fdx_passes_descriptors_between_processes():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fdx_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    n, payload, data = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert n == 300 and payload == b"payload" and data == b"descriptor crossed the process boundary"
+
+
+def test_memory_plan_per_gpu_is_safe():
+    from paper_2605_18815_b200 import scenarios as S
+    from paper_2605_18815_b200.api import RoutingPlan
+    import ctypes as C
+    from paper_2605_18815_b200 import _capi as A
+    sc = S.config2(2)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    st, viol = A.ArenaStats_t(), C.c_int64()
+    A.check(A.lib().rs_memory_plan(ab.h, ba.h, 0, 0, C.byref(st), C.byref(viol), None, None, 0))
+    assert viol.value == 0
