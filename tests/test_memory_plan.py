@@ -36,3 +36,32 @@ def test_replay_safe_on_campaign(golden):
         assert viol == 0, e["name"]
         n += 1
     assert n >= 40
+
+
+@pytest.mark.parametrize("n_gpus", [1, 2, 4])
+@pytest.mark.parametrize("groups", [0, 1, 2, 3])
+def test_grouped_plans_per_gpu_are_safe(n_gpus, groups):
+    """Every GPU's share of the arena, with the stage order coarsened into concurrency
+    groups, replays without reading clobbered data; fewer groups never alias more."""
+    sc = S.config2(2)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    for g in range(n_gpus):
+        st, viol, _, _ = memory_plan(ab, ba, chunk_bytes=8 << 20, n_gpus=n_gpus, gpu=g, groups=groups)
+        assert viol == 0
+        if groups == 1:
+            assert st.aliased_bytes == 0 and list(st.stage_groups) == [1, 1]
+        assert 1 <= st.stage_groups[0] <= 8
+
+
+def test_min_groups_fits_cap():
+    from paper_2605_18815_b200.api import memory_min_groups
+    sc = S.config2(2)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    full, _, _, _ = memory_plan(ab, ba, groups=1)
+    most, _, _, _ = memory_plan(ab, ba, groups=0)
+    assert memory_min_groups(ab, ba, 1, 0, full.physical_bytes)[0] == 1
+    k, need = memory_min_groups(ab, ba, 1, 0, most.physical_bytes)
+    assert k > 1 and need <= most.physical_bytes
+    assert memory_min_groups(ab, ba, 1, 0, most.physical_bytes - 1)[0] == -1
