@@ -308,10 +308,15 @@ def run_ours(args):
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
+        ta = time.perf_counter()
         reprepare[0]()
         reprepare[1]()
+        tb = time.perf_counter()
         step()
         torch.cuda.synchronize()
+        if os.environ.get("RS_TIMING"):
+            print(f"[bench rank {rank}] e2e step: prepare {1e3 * (tb - ta):.1f} ms, run {1e3 * (time.perf_counter() - tb):.1f} ms",
+                  file=sys.stderr, flush=True)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <queue>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -467,19 +468,24 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
 }
 
 void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
-                  std::int64_t dp, std::int64_t kTile) {
+                  std::int64_t dp, std::int64_t kTile, int lane) {
     if (rows <= 0 || rb <= 0) return;
     if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
         rb *= rows;
         rows = 1;
     }
-    if (static_cast<int>(buckets.size()) < (key + 1) * 5) buckets.resize(static_cast<size_t>(key + 1) * 5);
+    if (static_cast<int>(buckets.size()) < (key + 1) * 5) {
+        buckets.resize(static_cast<size_t>(key + 1) * 5);
+        lanes.resize(buckets.size());
+    }
     auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
         Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
                static_cast<std::uint32_t>(nb)};
         std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
         if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-        buckets[static_cast<size_t>(key) * 5 + class_index(align_class(a))].push_back(t);
+        const size_t b = static_cast<size_t>(key) * 5 + class_index(align_class(a));
+        buckets[b].push_back(t);
+        lanes[b].push_back(static_cast<std::uint8_t>(lane));
     };
     if (rows == 1 || rb >= kTile) {
         for (std::int64_t r = 0; r < rows; ++r) {
@@ -525,22 +531,71 @@ PinnedBuf::~PinnedBuf() {
     if (ptr) cudaFreeHost(ptr);
 }
 
+namespace {
+
+// Reorder one launch group's tiles so every destination lane (peer GPU, or this GPU's
+// HBM) progresses in proportion to its bytes: CTAs walk the tile list front to back, so
+// in op order (sorted by destination rank) all senders would converge on the same
+// receivers at the same time and leave other links idle.
+void interleave_lanes(std::vector<Tile>* v, const std::vector<std::uint8_t>& lane) {
+    int nl = 0;
+    for (std::uint8_t l : lane) nl = std::max(nl, l + 1);
+    if (nl < 2) return;
+    std::vector<std::vector<std::uint32_t>> q(static_cast<size_t>(nl));
+    std::vector<double> total(static_cast<size_t>(nl), 0.0), done(static_cast<size_t>(nl), 0.0);
+    auto bytes = [&](const Tile& t) { return static_cast<double>(t.rows) * t.row_bytes; };
+    for (size_t i = 0; i < v->size(); ++i) {
+        q[lane[i]].push_back(static_cast<std::uint32_t>(i));
+        total[lane[i]] += bytes((*v)[i]);
+    }
+    std::vector<size_t> head(static_cast<size_t>(nl), 0);
+    std::vector<Tile> out;
+    out.reserve(v->size());
+    using Item = std::pair<double, int>;  // (progress fraction after the lane's next tile, lane)
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
+    auto push = [&](int l) {
+        if (head[static_cast<size_t>(l)] < q[static_cast<size_t>(l)].size()) {
+            const Tile& t = (*v)[q[static_cast<size_t>(l)][head[static_cast<size_t>(l)]]];
+            pq.push({(done[static_cast<size_t>(l)] + 0.5 * bytes(t)) / total[static_cast<size_t>(l)], l});
+        }
+    };
+    for (int l = 0; l < nl; ++l) push(l);
+    while (!pq.empty()) {
+        const int l = pq.top().second;
+        pq.pop();
+        const Tile& t = (*v)[q[static_cast<size_t>(l)][head[static_cast<size_t>(l)]++]];
+        done[static_cast<size_t>(l)] += bytes(t);
+        out.push_back(t);
+        push(l);
+    }
+    v->swap(out);
+}
+
+}  // namespace
+
 void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging) {
     host.clear();
     groups.clear();
     for (size_t b = 0; b < buckets.size(); ++b) {
-        const auto& v = buckets[b];
+        auto& v = buckets[b];
         if (v.empty()) continue;
+        if (interleave) interleave_lanes(&v, lanes[b]);
         const int c = static_cast<int>(b % 5);
         groups.push_back({c, static_cast<int>(host.size()), static_cast<int>(v.size()), static_cast<int>(b / 5)});
         host.insert(host.end(), v.begin(), v.end());
         if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(v.size());
     }
     buckets.clear();
-    if (dev) cudaFree(dev);
-    dev = nullptr;
+    lanes.clear();
     if (!host.empty()) {
-        RS_CUDA(cudaMalloc(&dev, host.size() * sizeof(Tile)));
+        // keep the descriptor buffer across re-prepares: with peer access enabled every
+        // cudaMalloc/cudaFree also edits the peers' mappings (measured: 0.6 s stalls)
+        if (host.size() * sizeof(Tile) > dev_bytes) {
+            if (dev) cudaFree(dev);
+            dev = nullptr;
+            dev_bytes = host.size() * sizeof(Tile) * 5 / 4;
+            RS_CUDA(cudaMalloc(&dev, dev_bytes));
+        }
         // private non-blocking stream: descriptor uploads never serialize with the
         // caller's (training) streams, so the EDM can prepare in the background
         const size_t bytes = host.size() * sizeof(Tile);
@@ -609,7 +664,13 @@ void Executor::prepare(bool staged) {
     // copy engines and the SM stores contend for the same links (profiles/r01_nvlink.md)
     ce_min_bytes_ = ce ? std::atoll(ce) : 0;
     channels_.clear();
-    fused_ = std::make_unique<TileSet>();
+    if (!fused_) fused_ = std::make_unique<TileSet>();  // reused: keeps its device buffer
+    fused_->buckets.clear();
+    fused_->lanes.clear();
+    {
+        const char* to = std::getenv("RS_TILE_ORDER");
+        fused_->interleave = !(to && std::string(to) == "op");
+    }
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
     std::map<std::pair<int, int>, std::int64_t> chan_off;
     for (const CopyOp& op : ops) {
@@ -665,7 +726,7 @@ void Executor::prepare(bool staged) {
         // the caller's stream, local HBM tiles on an aux stream); otherwise one mixed launch
         fused_->add(split_remote_ ? stage * 2 + (dst_here ? 0 : 1) : stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
-                    op.row_bytes, op.src_pitch, op.dst_pitch, kTile);
+                    op.row_bytes, op.src_pitch, op.dst_pitch, kTile, D.gpu);
     }
     const auto t_tiles = std::chrono::steady_clock::now();
     if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));

@@ -68,15 +68,18 @@ struct TileSet {
         int cls, begin, count, key;
     };
     std::vector<std::vector<Tile>> buckets;  // [key * 5 + class] while building
+    std::vector<std::vector<std::uint8_t>> lanes;  // per bucket tile: destination lane (GPU)
+    bool interleave = false;  // finalize: interleave lanes in proportion to their bytes
     std::vector<Tile> host;
     std::vector<Group> groups;
     void* dev = nullptr;
+    size_t dev_bytes = 0;
     TileSet() = default;
     TileSet(const TileSet&) = delete;
     TileSet& operator=(const TileSet&) = delete;
     ~TileSet();
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
-             std::int64_t dp, std::int64_t kTile);
+             std::int64_t dp, std::int64_t kTile, int lane = 0);
     void finalize(ExecStats* stats, cudaStream_t upload, struct PinnedBuf* staging);
     /// launch groups in key order; key_mod > 0 restricts to keys with key % key_mod == key_rem
     int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk,
