@@ -215,6 +215,7 @@ typedef struct {
     int64_t tiles;
     int64_t tiles_by_class[5];
     int64_t launches;      /* kernel launches per rs_exec_run */
+    int64_t mc_bytes;      /* bytes delivered to peers by NVLS multicast stores */
 } rs_exec_stats_t;
 
 /* ---- memory-aware arena (Algorithm 1 FreeObsoleteBuffers / eager free,
@@ -270,6 +271,33 @@ int rs_exec_run_stage(rs_exec_t* e, int stage, void* stream, int* launches);
 int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n);
 /* the same order, grouped: cuts[i] == 1 starts a new stage at position i (cuts may be NULL) */
 int rs_exec_set_stage_groups(rs_exec_t* e, const int* dst_order, const int* cuts, int n);
+
+/* ---- broadcast promotion over NVLS multicast (optimize_primitives, SPEC.md:282-290,
+ * PAPER.md:719-740). A group = one source region copied to >= 2 destination ranks on
+ * distinct GPUs at the source's own offsets (DP replicas); slot s = each GPU's s-th
+ * destination rank. The root GPU stores it once through a multicast address whose object
+ * binds the root's source buffer and every member's destination buffer. */
+#define RS_MAX_MEMBERS 64
+typedef struct {
+    int id, root_rank, root_gpu, buf, slot, n_members;
+    int member_gpu[RS_MAX_MEMBERS], member_rank[RS_MAX_MEMBERS];
+    int64_t buffer_bytes;  /* size of buffer `buf` (equal on root and members) */
+    int64_t payload_bytes; /* bytes the root stores once */
+} rs_bcast_group_t;
+int rs_exec_bcast_groups(rs_exec_t* e, rs_bcast_group_t* out, int cap, int* n);
+/* root only; mc_va NULL reverts to per-destination pushes; takes effect at the next prepare */
+int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va);
+
+typedef struct rs_mc rs_mc_t;
+int rs_mc_create(int64_t bytes, int n_devices, rs_mc_t** out);
+int rs_mc_import(int fd, int64_t bytes, rs_mc_t** out); /* consumes fd */
+int rs_mc_export(const rs_mc_t* m, int* fd);
+int rs_mc_add_device(rs_mc_t* m, int device);
+/* every member must have added its device first (the bind blocks until then) */
+int rs_mc_bind_arena(rs_mc_t* m, const rs_arena_t* a, int layout, int rank, int buf);
+int rs_mc_map(rs_mc_t* m, int device, void** mc_va);
+void rs_mc_destroy(rs_mc_t* m);
+int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64_t* bytes);
 
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
 void rs_exec_destroy(rs_exec_t* e);

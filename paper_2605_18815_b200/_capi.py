@@ -71,7 +71,16 @@ class ExecOpts_t(C.Structure):
 
 class ExecStats_t(C.Structure):
     _fields_ = [("local_bytes", C.c_int64), ("remote_bytes", C.c_int64), ("tiles", C.c_int64),
-                ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64)]
+                ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64), ("mc_bytes", C.c_int64)]
+
+
+RS_MAX_MEMBERS = 64
+
+
+class BcastGroup_t(C.Structure):
+    _fields_ = [("id", C.c_int), ("root_rank", C.c_int), ("root_gpu", C.c_int), ("buf", C.c_int), ("slot", C.c_int),
+                ("n_members", C.c_int), ("member_gpu", C.c_int * RS_MAX_MEMBERS),
+                ("member_rank", C.c_int * RS_MAX_MEMBERS), ("buffer_bytes", C.c_int64), ("payload_bytes", C.c_int64)]
 
 
 class PlacementStats_t(C.Structure):
@@ -208,10 +217,21 @@ def _late_bindings(L):
         ("rs_exec_run_stage", [vp, C.c_int, vp, P(C.c_int)]),
         ("rs_exec_set_stage_groups", [vp, P(C.c_int), P(C.c_int), C.c_int]),
         ("rs_arena_stage_cuts", [vp, C.c_int, P(C.c_int), C.c_int, P(C.c_int)]),
+        ("rs_exec_bcast_groups", [vp, P(BcastGroup_t), C.c_int, P(C.c_int)]),
+        ("rs_exec_set_multicast", [vp, C.c_int, vp]),
+        ("rs_mc_create", [i64, C.c_int, P(vp)]),
+        ("rs_mc_import", [C.c_int, i64, P(vp)]),
+        ("rs_mc_export", [vp, P(C.c_int)]),
+        ("rs_mc_add_device", [vp, C.c_int]),
+        ("rs_mc_bind_arena", [vp, vp, C.c_int, C.c_int, C.c_int]),
+        ("rs_mc_map", [vp, C.c_int, P(vp)]),
+        ("rs_arena_bind_size", [vp, C.c_int, C.c_int, C.c_int, P(i64)]),
     ):
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    L.rs_mc_destroy.argtypes = [vp]
+    L.rs_mc_destroy.restype = None
     L.rs_plan_validate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                    C.POINTER(C.c_int64)]
     L.rs_plan_validate.restype = C.c_int

@@ -466,3 +466,72 @@ def _exec_run_stage(self, stage: int, stream: int = 0) -> int:
 
 Executor.num_stages = _exec_num_stages
 Executor.run_stage = _exec_run_stage
+
+
+def _exec_bcast_groups(self) -> List[A.BcastGroup_t]:
+    """Broadcast groups of this plan and placement (identical on every rank)."""
+    n = C.c_int()
+    A.check(A.lib().rs_exec_bcast_groups(self.h, None, 0, C.byref(n)))
+    arr = (A.BcastGroup_t * max(1, n.value))()
+    A.check(A.lib().rs_exec_bcast_groups(self.h, arr, n.value, C.byref(n)))
+    return list(arr[: n.value])
+
+
+def _exec_set_multicast(self, group_id: int, mc_va: int) -> None:
+    A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
+
+
+Executor.bcast_groups = _exec_bcast_groups
+Executor.set_multicast = _exec_set_multicast
+
+
+def _arena_bind_size(self, layout: int, rank: int, buf: int) -> int:
+    n = C.c_int64()
+    A.check(A.lib().rs_arena_bind_size(self.h, layout, rank, buf, C.byref(n)))
+    return n.value
+
+
+Arena.bind_size = _arena_bind_size
+
+
+class Multicast:
+    """NVLS multicast object (rs_mc_*): created by the root, imported by the members."""
+
+    def __init__(self, handle: int, nbytes: int):
+        self.h, self.nbytes = handle, nbytes
+
+    @classmethod
+    def create(cls, nbytes: int, n_devices: int) -> "Multicast":
+        h = C.c_void_p()
+        A.check(A.lib().rs_mc_create(nbytes, n_devices, C.byref(h)))
+        return cls(h.value, nbytes)
+
+    @classmethod
+    def import_fd(cls, fd: int, nbytes: int) -> "Multicast":
+        h = C.c_void_p()
+        A.check(A.lib().rs_mc_import(fd, nbytes, C.byref(h)))
+        return cls(h.value, nbytes)
+
+    def export_fd(self) -> int:
+        fd = C.c_int()
+        A.check(A.lib().rs_mc_export(self.h, C.byref(fd)))
+        return fd.value
+
+    def add_device(self, device: int) -> None:
+        A.check(A.lib().rs_mc_add_device(self.h, device))
+
+    def bind_arena(self, arena: "Arena", layout: int, rank: int, buf: int) -> None:
+        A.check(A.lib().rs_mc_bind_arena(self.h, arena.h, layout, rank, buf))
+
+    def map(self, device: int) -> int:
+        va = C.c_void_p()
+        A.check(A.lib().rs_mc_map(self.h, device, C.byref(va)))
+        return va.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
+            A.lib().rs_mc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

@@ -28,6 +28,13 @@ struct Drv {
     CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
     CUresult (*export_fd)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) = nullptr;
     CUresult (*import_fd)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
+    CUresult (*mc_create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+    CUresult (*mc_add)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+    CUresult (*mc_bind)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+    CUresult (*mc_unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+    CUresult (*mc_granularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+    CUresult (*device_get)(CUdevice*, int) = nullptr;
 
     static const Drv& get() {
         static Drv d = [] {
@@ -49,6 +56,12 @@ struct Drv {
             load("cuMemGetAllocationGranularity", x.granularity);
             load("cuMemExportToShareableHandle", x.export_fd);
             load("cuMemImportFromShareableHandle", x.import_fd);
+            load("cuMulticastCreate", x.mc_create);
+            load("cuMulticastAddDevice", x.mc_add);
+            load("cuMulticastBindMem", x.mc_bind);
+            load("cuMulticastUnbind", x.mc_unbind);
+            load("cuMulticastGetGranularity", x.mc_granularity);
+            load("cuDeviceGet", x.device_get);
             return x;
         }();
         return d;
@@ -272,6 +285,113 @@ void* Arena::ptr(int layout, int rank, int buf) const {
 }
 std::int64_t Arena::bytes(int layout, int rank, int buf) const {
     return bufs_[layout].at(static_cast<size_t>(rank) * exec::kNumBufs + buf).bytes;
+}
+
+std::int64_t Arena::bind_size(int layout, int rank, int buf) const {
+    // from the size alone (plan_memory's rule), so every rank agrees, hosted here or not
+    const BufMap& m = bufs_[layout][static_cast<size_t>(rank) * exec::kNumBufs + buf];
+    const std::int64_t C = cfg_.chunk_bytes, gran = 2ll << 20;
+    return m.bytes < C / 4 ? (m.bytes + gran - 1) / gran * gran : (m.bytes + C - 1) / C * C;
+}
+
+void Arena::bind_multicast(Multicast& mc, int layout, int rank, int buf) const {
+    const BufMap& m = bufs_[layout][static_cast<size_t>(rank) * exec::kNumBufs + buf];
+    if (m.remote || m.bytes == 0) throw ConfigError("bind_multicast: buffer is not hosted by this GPU");
+    if (m.own_handle) {
+        const std::int64_t gran = 2ll << 20;
+        mc.bind(cfg_.device, m.handle, 0, (m.bytes + gran - 1) / gran * gran);
+        return;
+    }
+    if (!m.mapped_vmm) throw ConfigError("bind_multicast: buffer is not VMM-backed");
+    const std::int64_t C = cfg_.chunk_bytes;
+    for (size_t c = 0; c < m.phys.size(); ++c)
+        mc.bind(cfg_.device, handles_[static_cast<size_t>(m.phys[c])], static_cast<std::int64_t>(c) * C, C);
+}
+
+namespace {
+CUmulticastObjectProp mc_prop(std::int64_t bytes, int n) {
+    CUmulticastObjectProp p = {};
+    p.numDevices = static_cast<unsigned>(n);
+    p.size = static_cast<size_t>(bytes);
+    p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    return p;
+}
+}  // namespace
+
+Multicast::Multicast(std::int64_t bytes, int n_devices) : bytes_(bytes) {
+    const Drv& D = Drv::get();
+    const CUmulticastObjectProp p = mc_prop(bytes, n_devices);
+    size_t gran = 0;
+    drv_check(D.mc_granularity(&gran, &p, CU_MULTICAST_GRANULARITY_MINIMUM), "cuMulticastGetGranularity");
+    if (bytes % static_cast<std::int64_t>(gran)) throw ConfigError("multicast size is not a multiple of its granularity");
+    CUmemGenericAllocationHandle h;
+    drv_check(D.mc_create(&h, &p), "cuMulticastCreate");
+    handle_ = h;
+}
+
+Multicast::Multicast(int fd, std::int64_t bytes) : bytes_(bytes) {
+    const Drv& D = Drv::get();
+    CUmemGenericAllocationHandle h;
+    const CUresult r = D.import_fd(&h, reinterpret_cast<void*>(static_cast<std::intptr_t>(fd)),
+                                   CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    ::close(fd);
+    drv_check(r, "cuMemImportFromShareableHandle (multicast)");
+    handle_ = h;
+}
+
+Multicast::~Multicast() {
+    const Drv& D = Drv::get();
+    if (va_) {
+        D.unmap(va_, static_cast<size_t>(bytes_));
+        D.addr_free(va_, static_cast<size_t>(bytes_));
+    }
+    for (const Binding& b : bindings_) {
+        CUdevice dev;
+        if (D.device_get(&dev, b.device) == CUDA_SUCCESS)
+            D.mc_unbind(handle_, dev, static_cast<size_t>(b.offset), static_cast<size_t>(b.bytes));
+    }
+    if (handle_) D.release(handle_);
+}
+
+int Multicast::export_fd() const {
+    int fd = -1;
+    drv_check(Drv::get().export_fd(&fd, handle_, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+              "cuMemExportToShareableHandle (multicast)");
+    return fd;
+}
+
+void Multicast::add_device(int device) {
+    const Drv& D = Drv::get();
+    CUdevice dev;
+    drv_check(D.device_get(&dev, device), "cuDeviceGet");
+    drv_check(D.mc_add(handle_, dev), "cuMulticastAddDevice");
+}
+
+void Multicast::bind(int device, std::uint64_t mem_handle, std::int64_t mc_offset, std::int64_t bytes) {
+    if (mc_offset + bytes > bytes_) throw ConfigError("multicast bind beyond the object");
+    if (cudaSetDevice(device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    drv_check(Drv::get().mc_bind(handle_, static_cast<size_t>(mc_offset), mem_handle, 0, static_cast<size_t>(bytes), 0),
+              "cuMulticastBindMem");
+    bindings_.push_back({device, mc_offset, bytes});
+}
+
+void* Multicast::map(int device) {
+    if (va_) return reinterpret_cast<void*>(va_);
+    const Drv& D = Drv::get();
+    if (cudaSetDevice(device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    const CUmulticastObjectProp p = mc_prop(bytes_, 1);
+    size_t gran = 0;
+    drv_check(D.mc_granularity(&gran, &p, CU_MULTICAST_GRANULARITY_RECOMMENDED), "cuMulticastGetGranularity");
+    CUdeviceptr va = 0;
+    drv_check(D.reserve(&va, static_cast<size_t>(bytes_), gran, 0, 0), "cuMemAddressReserve (multicast)");
+    drv_check(D.map(va, static_cast<size_t>(bytes_), 0, handle_, 0), "cuMemMap (multicast)");
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    drv_check(D.set_access(va, static_cast<size_t>(bytes_), &acc, 1), "cuMemSetAccess (multicast)");
+    va_ = va;
+    return reinterpret_cast<void*>(va_);
 }
 
 }  // namespace mem

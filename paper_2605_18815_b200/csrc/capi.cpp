@@ -699,6 +699,7 @@ int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
         out->tiles = s.tiles;
         for (int i = 0; i < 5; ++i) out->tiles_by_class[i] = s.tiles_by_class[i];
         out->launches = s.launches;
+        out->mc_bytes = s.mc_bytes;
         return RS_OK;
     });
 }
@@ -910,6 +911,102 @@ int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
             out->stage_groups[d] = 0;
             for (int c : a->a->stage_cuts(d)) out->stage_groups[d] += c;
         }
+        return RS_OK;
+    });
+}
+
+
+struct rs_mc {
+    std::unique_ptr<mem::Multicast> m;
+};
+
+int rs_exec_bcast_groups(rs_exec_t* e, rs_bcast_group_t* out, int cap, int* n) {
+    return guarded([&] {
+        const std::vector<exec::BcastGroup>& G = e->ex->bcast_groups();
+        *n = static_cast<int>(G.size());
+        for (int i = 0; i < *n && i < cap; ++i) {
+            const exec::BcastGroup& g = G[static_cast<size_t>(i)];
+            rs_bcast_group_t& o = out[i];
+            o.id = g.id;
+            o.root_rank = g.root_rank;
+            o.root_gpu = g.root_gpu;
+            o.buf = g.buf;
+            o.slot = g.slot;
+            if (g.member_ranks.size() > RS_MAX_MEMBERS) throw ConfigError("broadcast group exceeds RS_MAX_MEMBERS");
+            o.n_members = static_cast<int>(g.member_ranks.size());
+            for (int k = 0; k < o.n_members; ++k) {
+                o.member_gpu[k] = g.member_gpus[static_cast<size_t>(k)];
+                o.member_rank[k] = g.member_ranks[static_cast<size_t>(k)];
+            }
+            o.buffer_bytes = g.buffer_bytes;
+            o.payload_bytes = g.payload_bytes;
+        }
+        return RS_OK;
+    });
+}
+
+int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va) {
+    return guarded([&] {
+        e->ex->set_multicast(id, mc_va);
+        return RS_OK;
+    });
+}
+
+int rs_mc_create(int64_t bytes, int n_devices, rs_mc_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto m = std::make_unique<rs_mc>();
+        m->m = std::make_unique<mem::Multicast>(bytes, n_devices);
+        *out = m.release();
+        return RS_OK;
+    });
+}
+
+int rs_mc_import(int fd, int64_t bytes, rs_mc_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto m = std::make_unique<rs_mc>();
+        m->m = std::make_unique<mem::Multicast>(fd, bytes);
+        *out = m.release();
+        return RS_OK;
+    });
+}
+
+int rs_mc_export(const rs_mc_t* m, int* fd) {
+    return guarded([&] {
+        *fd = m->m->export_fd();
+        return RS_OK;
+    });
+}
+
+int rs_mc_add_device(rs_mc_t* m, int device) {
+    return guarded([&] {
+        m->m->add_device(device);
+        return RS_OK;
+    });
+}
+
+int rs_mc_bind_arena(rs_mc_t* m, const rs_arena_t* a, int layout, int rank, int buf) {
+    return guarded([&] {
+        if (layout < 0 || layout > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
+        a->a->bind_multicast(*m->m, layout, rank, buf);
+        return RS_OK;
+    });
+}
+
+int rs_mc_map(rs_mc_t* m, int device, void** mc_va) {
+    return guarded([&] {
+        *mc_va = m->m->map(device);
+        return RS_OK;
+    });
+}
+
+void rs_mc_destroy(rs_mc_t* m) { delete m; }
+
+int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64_t* bytes) {
+    return guarded([&] {
+        if (layout < 0 || layout > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
+        *bytes = a->a->bind_size(layout, rank, buf);
         return RS_OK;
     });
 }

@@ -60,10 +60,24 @@ __device__ __forceinline__ uint4 ld_stream<uint4>(const uint4* p) {
     return r;
 }
 
+template <bool MC, typename T>
+__device__ __forceinline__ void st_vec(T* p, const T& v) {
+    *p = v;
+}
+// NVLS multicast store: one 16-B store through the multicast address lands in every
+// member GPU's bound memory. .f32 only names the register format: a plain store moves
+// the bits unchanged (NaN payloads included; the verify kernel checks every byte).
+template <>
+__device__ __forceinline__ void st_vec<true, uint4>(uint4* p, const uint4& v) {
+    asm volatile("multimem.st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 /// Copy tiles of alignment class V (all addresses, pitches and row sizes are
 /// multiples of V). Persistent grid: CTA b takes tiles b, b+grid, ... Each thread
-/// keeps kUnroll independent loads in flight before storing.
-template <int V>
+/// keeps kUnroll independent loads in flight before storing. MC: the destination is a
+/// multicast address (16-B class only).
+template <int V, bool MC = false>
 __global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles, std::uint64_t sbase,
                                                               std::uint64_t dbase) {
     using T = typename VecT<V>::T;
@@ -81,9 +95,9 @@ __global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __rest
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(s + i + u * kThreads);
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) d[i + u * kThreads] = r[u];
+                for (int u = 0; u < kUnroll; ++u) st_vec<MC>(d + i + u * kThreads, r[u]);
             }
-            for (; i < vpr; i += kThreads) d[i] = ld_stream(s + i);
+            for (; i < vpr; i += kThreads) st_vec<MC>(d + i, ld_stream(s + i));
         } else {
             const unsigned n = tl.rows * vpr;
             for (unsigned i = threadIdx.x; i < n; i += kUnroll * kThreads) {
@@ -100,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __rest
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
                     const unsigned e = i + u * kThreads;
-                    if (e < n) reinterpret_cast<T*>(tl.dst + row[u] * tl.dst_pitch)[col[u]] = r[u];
+                    if (e < n) st_vec<MC>(reinterpret_cast<T*>(tl.dst + row[u] * tl.dst_pitch) + col[u], r[u]);
                 }
             }
         }
@@ -349,6 +363,9 @@ Executor::~Executor() {
     if (aux_) cudaStreamDestroy(aux_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (mc_stream_) cudaStreamDestroy(mc_stream_);
+    for (cudaEvent_t e : mc_ev_)
+        if (e) cudaEventDestroy(e);
 }
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
@@ -649,6 +666,82 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
     return launches;
 }
 
+const std::vector<BcastGroup>& Executor::bcast_groups() {
+    if (bcast_ready_) return bcast_;
+    bcast_.clear();
+    const std::vector<CopyOp> ops = build_ops(P_);
+    // candidate ops: cross-GPU, destination at the source's own offset in an equally
+    // sized buffer (replica layout), 16-B aligned (multimem.st.v4)
+    using Key = std::tuple<int, int, std::int64_t, std::int64_t, std::int64_t, std::int64_t>;
+    std::map<Key, std::vector<size_t>> by_src;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const CopyOp& op = ops[i];
+        if (op.rows <= 0 || op.row_bytes <= 0) continue;
+        const RankBufs& S = bufs_[0][static_cast<size_t>(op.src_side_rank)];
+        const RankBufs& D = bufs_[1][static_cast<size_t>(op.dst_rank)];
+        if (S.gpu == D.gpu || op.dst_buf != op.src_buf || op.dst_off != op.src_off) continue;
+        if (op.rows > 1 && op.dst_pitch != op.src_pitch) continue;
+        if ((op.src_off | op.row_bytes | (op.rows > 1 ? op.src_pitch : 0)) % 16 != 0) continue;
+        if (S.bytes[op.src_buf] != D.bytes[op.dst_buf]) continue;
+        by_src[Key{op.src_side_rank, op.src_buf, op.src_off, op.rows, op.row_bytes, op.rows > 1 ? op.src_pitch : 0}].push_back(i);
+    }
+    std::map<std::tuple<int, int, int, std::vector<int>>, size_t> index;
+    for (const auto& kv : by_src) {
+        std::map<int, std::vector<size_t>> per_gpu;  // destination GPU -> ops by dst rank
+        for (size_t i : kv.second) per_gpu[bufs_[1][static_cast<size_t>(ops[i].dst_rank)].gpu].push_back(i);
+        if (per_gpu.size() < 2) continue;
+        size_t slots = 0;
+        for (auto& g : per_gpu) {
+            std::sort(g.second.begin(), g.second.end(), [&](size_t a, size_t b) { return ops[a].dst_rank < ops[b].dst_rank; });
+            slots = std::max(slots, g.second.size());
+        }
+        const int root = std::get<0>(kv.first), buf = std::get<1>(kv.first);
+        for (size_t sl = 0; sl < slots; ++sl) {
+            std::vector<int> ranks, gpus;
+            std::vector<size_t> sel;
+            for (const auto& g : per_gpu)
+                if (sl < g.second.size()) {
+                    ranks.push_back(ops[g.second[sl]].dst_rank);
+                    gpus.push_back(g.first);
+                    sel.push_back(g.second[sl]);
+                }
+            if (ranks.size() < 2) continue;  // a single destination left: plain push
+            const auto key = std::make_tuple(root, buf, static_cast<int>(sl), ranks);
+            auto it = index.find(key);
+            if (it == index.end()) {
+                BcastGroup g;
+                g.id = static_cast<int>(bcast_.size());
+                g.root_rank = root;
+                g.root_gpu = bufs_[0][static_cast<size_t>(root)].gpu;
+                g.buf = buf;
+                g.slot = static_cast<int>(sl);
+                g.member_gpus = gpus;
+                g.member_ranks = ranks;
+                g.buffer_bytes = bufs_[0][static_cast<size_t>(root)].bytes[buf];
+                it = index.emplace(key, bcast_.size()).first;
+                bcast_.push_back(std::move(g));
+            }
+            BcastGroup& g = bcast_[it->second];
+            const CopyOp& lead = ops[sel[0]];
+            g.payload_bytes += lead.rows * lead.row_bytes;
+            g.ops.insert(g.ops.end(), sel.begin(), sel.end());
+        }
+    }
+    bcast_ready_ = true;
+    return bcast_;
+}
+
+void Executor::set_multicast(int id, void* mc_va) {
+    bcast_groups();
+    if (id < 0 || id >= static_cast<int>(bcast_.size())) throw ConfigError("set_multicast: no such broadcast group");
+    if (bcast_[static_cast<size_t>(id)].root_gpu != cfg_.gpu) throw ConfigError("set_multicast: this GPU is not the group's root");
+    for (int s : stage_of_dst_)
+        if (s != 0) throw ConfigError("set_multicast: needs a single-stage transition (multicast stores span stages)");
+    if (mc_va) mc_va_[id] = mc_va;
+    else mc_va_.erase(id);
+    prepared_ = false;
+}
+
 void Executor::prepare(bool staged) {
     const auto t_begin = std::chrono::steady_clock::now();
     RS_CUDA(cudaSetDevice(cfg_.device));
@@ -672,8 +765,30 @@ void Executor::prepare(bool staged) {
         fused_->interleave = !(to && std::string(to) == "op");
     }
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
+    if (!mc_) mc_ = std::make_unique<TileSet>();
+    mc_src_bytes_ = 0;
+    mc_->buckets.clear();
+    mc_->lanes.clear();
+    // ops delivered by a multicast store stream: -1 no, else the multicast address; the
+    // first op of each source region (lead) emits the tiles, the other members' copies ride along
+    std::vector<std::uint64_t> op_mc(ops.size(), 0);
+    std::vector<char> op_lead(ops.size(), 0);
+    std::vector<int> op_mc_group(ops.size(), 0);  // one launch per multicast object
+    if (!staged && !mc_va_.empty()) {
+        bcast_groups();
+        for (const auto& kv : mc_va_) {
+            const BcastGroup& g = bcast_[static_cast<size_t>(kv.first)];
+            const size_t members = g.member_ranks.size();
+            for (size_t k = 0; k < g.ops.size(); ++k) {
+                op_mc[g.ops[k]] = reinterpret_cast<std::uint64_t>(kv.second);
+                op_mc_group[g.ops[k]] = kv.first;
+                op_lead[g.ops[k]] = (k % members) == 0;
+            }
+        }
+    }
     std::map<std::pair<int, int>, std::int64_t> chan_off;
-    for (const CopyOp& op : ops) {
+    for (size_t oi = 0; oi < ops.size(); ++oi) {
+        const CopyOp& op = ops[oi];
         const RankBufs& S = bufs_[0][static_cast<size_t>(op.src_side_rank)];
         const RankBufs& D = bufs_[1][static_cast<size_t>(op.dst_rank)];
         if (op.rows <= 0 || op.row_bytes <= 0) continue;
@@ -706,6 +821,18 @@ void Executor::prepare(bool staged) {
             continue;
         }
         if (!src_here) continue;  // pushed by the source's GPU
+        if (op_mc[oi]) {
+            if (!S.ptr[op.src_buf]) throw ConfigError("prepare: multicast source buffer not bound");
+            if (op_lead[oi]) mc_src_bytes_ += total;
+            if (op_lead[oi])
+                mc_->add(op_mc_group[oi], reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+                         op_mc[oi] + static_cast<std::uint64_t>(op.dst_off), op.rows, op.row_bytes, op.src_pitch, op.dst_pitch,
+                         kTile);
+            stats_.remote_bytes += total;
+            stats_.mc_bytes += total;
+            has_remote_ = true;
+            continue;
+        }
         if (!S.ptr[op.src_buf] || !D.ptr[op.dst_buf])
             throw ConfigError(strfmt("prepare: buffer not bound (src rank %d buf %d -> dst rank %d buf %d)",
                                      op.src_side_rank, op.src_buf, op.dst_rank, op.dst_buf));
@@ -731,6 +858,9 @@ void Executor::prepare(bool staged) {
     const auto t_tiles = std::chrono::steady_clock::now();
     if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
     fused_->finalize(&stats_, upload_, &staging_);
+    mc_->finalize(&stats_, upload_, &staging_);
+    for (const TileSet::Group& g : mc_->groups)
+        if (g.cls != 0) throw ConfigError("prepare: multicast tiles must be 16-byte aligned");
     for (auto& kv : channels_) {
         kv.second.pack->finalize(nullptr, upload_, &staging_);
         kv.second.unpack->finalize(nullptr, upload_, &staging_);
@@ -758,9 +888,70 @@ void Executor::prepare(bool staged) {
     prepared_ = true;
 }
 
+int Executor::launch_multicast(cudaStream_t stream) const {
+    if (!mc_ || mc_->groups.empty()) return 0;
+    const Tile* base = static_cast<const Tile*>(mc_->dev);
+    int n = 0;
+    for (const TileSet::Group& g : mc_->groups) {
+        const char* mcc = std::getenv("RS_MC_CTAS_PER_SM");
+        const int grid = std::min(g.count, sms_ * (mcc ? std::max(1, std::atoi(mcc)) : 1));
+        copy_tiles_kernel<16, true><<<grid, kThreads, 0, stream>>>(base + g.begin, g.count, 0, 0);
+        ++n;
+    }
+    RS_CUDA(cudaGetLastError());
+    return n;
+}
+
 int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     RS_CUDA(cudaSetDevice(cfg_.device));
+    if (!mc_ || mc_->groups.empty()) return run_fused(stream);
+    // the multicast stream runs concurrently with the fused pushes (the root's NVLink
+    // carries both): one CTA per SM for it, two per SM for the fused kernel
+    if (!mc_stream_) {
+        RS_CUDA(cudaStreamCreateWithFlags(&mc_stream_, cudaStreamNonBlocking));
+        for (auto& e : mc_ev_) RS_CUDA(cudaEventCreate(&e));
+    }
+    const bool timing = std::getenv("RS_TIMING") != nullptr;
+    if (const char* ser = std::getenv("RS_MC_SERIAL"); ser && std::string(ser) == "1") {  // diagnostics
+        RS_CUDA(cudaEventRecord(mc_ev_[0], stream));
+        const int n0 = launch_multicast(stream);
+        RS_CUDA(cudaEventRecord(mc_ev_[1], stream));
+        const int n1 = run_fused(stream);
+        RS_CUDA(cudaEventRecord(mc_ev_[2], stream));
+        if (timing) {
+            RS_CUDA(cudaEventSynchronize(mc_ev_[2]));
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, mc_ev_[0], mc_ev_[1]);
+            cudaEventElapsedTime(&b, mc_ev_[1], mc_ev_[2]);
+            std::fprintf(stderr, "[reshard] gpu %d run: multicast %.3f ms (%.1f GB/s source), then fused %.3f ms\n", cfg_.gpu,
+                         a, a > 0 ? mc_src_bytes_ / (a * 1e6) : 0.0, b);
+        }
+        return n0 + n1;
+    }
+    RS_CUDA(cudaEventRecord(mc_ev_[0], stream));
+    RS_CUDA(cudaStreamWaitEvent(mc_stream_, mc_ev_[0], 0));
+    const int n0 = launch_multicast(mc_stream_);
+    RS_CUDA(cudaEventRecord(mc_ev_[1], mc_stream_));
+    const int saved = cfg_.ctas_per_sm;
+    cfg_.ctas_per_sm = 2;
+    const int n1 = run_fused(stream);
+    cfg_.ctas_per_sm = saved;
+    RS_CUDA(cudaEventRecord(mc_ev_[2], stream));
+    RS_CUDA(cudaStreamWaitEvent(stream, mc_ev_[1], 0));
+    if (timing) {  // diagnostics: both parts timed from the fork
+        RS_CUDA(cudaEventSynchronize(mc_ev_[1]));
+        RS_CUDA(cudaEventSynchronize(mc_ev_[2]));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, mc_ev_[0], mc_ev_[1]);
+        cudaEventElapsedTime(&b, mc_ev_[0], mc_ev_[2]);
+        std::fprintf(stderr, "[reshard] gpu %d run: multicast %.3f ms (%.1f GB/s source), fused %.3f ms (concurrent)\n",
+                     cfg_.gpu, a, a > 0 ? mc_src_bytes_ / (a * 1e6) : 0.0, b);
+    }
+    return n0 + n1;
+}
+
+int Executor::run_fused(cudaStream_t stream) {
     if (!has_remote_) return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
     if (!aux_) {
         RS_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
@@ -807,7 +998,8 @@ int Executor::run_stage(int stage, cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     if (split_remote_ || !ce_ops_.empty()) throw ConfigError("run_stage needs the single mixed launch (no CE offload)");
     RS_CUDA(cudaSetDevice(cfg_.device));
-    return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, has_remote_ ? remote_bulk_ : use_bulk_, -1, stage);
+    const int nmc = stage == 0 ? launch_multicast(stream) : 0;
+    return nmc + fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, has_remote_ ? remote_bulk_ : use_bulk_, -1, stage);
 }
 
 std::int64_t Executor::channel_bytes(int src_phys, int dst_phys) const {

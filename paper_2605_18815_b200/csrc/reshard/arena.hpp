@@ -97,6 +97,11 @@ public:
     void export_local(std::vector<int>* fds, std::vector<std::uint8_t>* table) const;
     /// map a peer's buffers into this process's address space (consumes the fds)
     void import_peer(const std::vector<int>& fds, const std::vector<std::uint8_t>& table);
+    /// bind this GPU's buffer (layout, rank, buf) to a multicast object at offset 0,
+    /// chunk by chunk (the object then writes through to these physical chunks)
+    void bind_multicast(class Multicast& mc, int layout, int rank, int buf) const;
+    /// bytes a multicast object must span to bind that buffer whole
+    std::int64_t bind_size(int layout, int rank, int buf) const;
 
 private:
     struct BufMap {
@@ -115,6 +120,35 @@ private:
     ArenaStats stats_;
     int nranks_[2] = {0, 0};
     int n_gpus_ = 1;
+};
+
+/// NVLS multicast object shared by the processes of its member GPUs (created by the
+/// root, passed as a POSIX descriptor). Protocol: create/import -> add_device on every
+/// member -> (barrier) -> bind memory -> map (root) -> multimem stores.
+class Multicast {
+public:
+    Multicast(std::int64_t bytes, int n_devices);  // create
+    Multicast(int fd, std::int64_t bytes);         // import (consumes fd)
+    ~Multicast();
+    Multicast(const Multicast&) = delete;
+    Multicast& operator=(const Multicast&) = delete;
+
+    int export_fd() const;
+    void add_device(int device);
+    void bind(int device, std::uint64_t mem_handle, std::int64_t mc_offset, std::int64_t bytes);
+    void* map(int device);
+    std::int64_t bytes() const { return bytes_; }
+    std::uint64_t handle() const { return handle_; }
+
+private:
+    std::uint64_t handle_ = 0;
+    std::int64_t bytes_ = 0;
+    std::uint64_t va_ = 0;
+    struct Binding {
+        int device;
+        std::int64_t offset, bytes;
+    };
+    std::vector<Binding> bindings_;
 };
 
 }  // namespace mem

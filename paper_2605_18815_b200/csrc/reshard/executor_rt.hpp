@@ -41,6 +41,7 @@ struct ExecStats {
     std::int64_t tiles_by_class[5] = {0, 0, 0, 0, 0};  // 16/8/4/2/1-byte vectors
     std::int64_t launches = 0;                         // kernel launches per run()
     std::int64_t ce_bytes = 0;                         // peer-bound bytes moved by copy engines
+    std::int64_t mc_bytes = 0;                         // bytes delivered by multicast stores
 };
 
 struct RankBufs {
@@ -86,6 +87,19 @@ struct TileSet {
                int key_mod = 0, int key_rem = 0) const;
 };
 
+/// Broadcast promotion (optimize_primitives): one
+/// source region pushed to several destination ranks on distinct GPUs, all with the same
+/// layout as the source (DP replicas). Executed as one NVLS multicast store stream from
+/// the root GPU instead of one push per destination. Slot s of a GPU = its s-th
+/// destination rank of the broadcast (one multicast object per slot).
+struct BcastGroup {
+    int id = 0, root_rank = 0, root_gpu = 0, buf = 0, slot = 0;
+    std::vector<int> member_gpus, member_ranks;  // destination GPUs / ranks (root excluded)
+    std::int64_t buffer_bytes = 0;              // bytes of buffer `buf` (same on every member)
+    std::int64_t payload_bytes = 0;             // bytes the root sends once (per member they arrive)
+    std::vector<size_t> ops;                    // build_ops indices covered (every member's copy)
+};
+
 class Executor {
 public:
     Executor(const core::PlanCore& P, const ExecConfig& cfg);
@@ -124,6 +138,13 @@ public:
     int pack(int src_phys, int dst_phys, void* buf, cudaStream_t stream);
     int unpack(int src_phys, int dst_phys, const void* buf, cudaStream_t stream);
 
+    /// broadcast groups of this plan and placement (identical on every rank)
+    const std::vector<BcastGroup>& bcast_groups();
+    /// root GPU: execute group `id` through the multicast address `mc_va` (its object binds
+    /// the root's source buffer and every member's destination buffer at equal offsets);
+    /// nullptr reverts to per-destination pushes. Takes effect at the next prepare().
+    void set_multicast(int id, void* mc_va);
+
     void fill(int side, std::uint64_t seed, cudaStream_t stream);
     std::int64_t verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad);
 
@@ -132,6 +153,8 @@ public:
 
 private:
     std::vector<FillTask> fill_tasks(int side) const;
+    int launch_multicast(cudaStream_t stream) const;
+    int run_fused(cudaStream_t stream);
     void upload_tasks(const std::vector<FillTask>& tasks);
 
     const core::PlanCore& P_;
@@ -158,6 +181,13 @@ public:
 
 private:
     std::unique_ptr<TileSet> fused_;
+    std::unique_ptr<TileSet> mc_;  // multicast tiles (dst = multicast address)
+    std::vector<BcastGroup> bcast_;
+    bool bcast_ready_ = false;
+    std::map<int, void*> mc_va_;
+    std::int64_t mc_src_bytes_ = 0;
+    cudaStream_t mc_stream_ = nullptr;
+    cudaEvent_t mc_ev_[3] = {nullptr, nullptr, nullptr};
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;
     cudaStream_t upload_ = nullptr;

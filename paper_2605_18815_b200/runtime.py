@@ -229,6 +229,72 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
     return arena, global_stage_cuts(arena, world)
 
 
+def setup_multicast(arena, ex: Executor, rank: int, world: int, device: int, tag: str = "0", min_payload: int = 0):
+    """Broadcast promotion over NVLS multicast for the executor's broadcast groups
+    (Executor.bcast_groups): per group the root GPU creates a multicast object and passes
+    it to the members (fdx); every member adds its device; after a barrier each binds its
+    buffer (root: the source, members: the destination ranks' buffers, equal layouts);
+    the root maps it and its executor stores the group once through the multicast address.
+    Collective over all ranks. Returns the objects to keep alive (close() before the
+    arena goes away); call ex.prepare() afterwards."""
+    import threading
+
+    import torch.distributed as dist
+
+    from .api import Multicast, fdx_close, fdx_listen, fdx_recv, fdx_send
+    groups = [g for g in ex.bcast_groups() if g.payload_bytes >= min_payload]
+    mcs = {}
+    size = {g.id: arena.bind_size(0, g.root_rank, g.buf) for g in groups}
+    expect = sum(1 for g in groups if rank in list(g.member_gpu[: g.n_members]) and g.root_gpu != rank)
+    sock = fdx_listen(f"reshard-mc-{tag}-{rank}")
+    dist.barrier()
+    errors = []
+
+    def receive():
+        try:
+            for _ in range(expect):
+                fds, payload = fdx_recv(sock)
+                gid = int(payload.decode())
+                mcs[gid] = Multicast.import_fd(fds[0], size[gid])
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    t = threading.Thread(target=receive, name="mc-import")
+    t.start()
+    for g in groups:
+        if g.root_gpu != rank:
+            continue
+        members = sorted(set(g.member_gpu[: g.n_members]))
+        mc = Multicast.create(size[g.id], len(members) + 1)
+        mcs[g.id] = mc
+        for peer in members:
+            fd = mc.export_fd()
+            try:
+                fdx_send(f"reshard-mc-{tag}-{peer}", [fd], str(g.id).encode())
+            finally:
+                os.close(fd)
+    t.join()
+    fdx_close(sock)
+    if errors:
+        raise errors[0]
+    for gid in sorted(mcs):
+        mcs[gid].add_device(device)
+    dist.barrier()
+    by_id = {g.id: g for g in groups}
+    for gid in sorted(mcs):
+        g = by_id[gid]
+        if g.root_gpu == rank:
+            mcs[gid].bind_arena(arena, 0, g.root_rank, g.buf)
+        for k in range(g.n_members):
+            if g.member_gpu[k] == rank:
+                mcs[gid].bind_arena(arena, 1, g.member_rank[k], g.buf)
+    dist.barrier()
+    for gid in sorted(mcs):
+        if by_id[gid].root_gpu == rank:
+            ex.set_multicast(gid, mcs[gid].map(device))
+    return [mcs[k] for k in sorted(mcs)]
+
+
 def run_stages(ex: Executor, stream: int, world: int) -> None:
     """Memory-aware stages across GPUs: a stage may write chunks that the previous stage
     read on another GPU, so every stage boundary is a global barrier."""

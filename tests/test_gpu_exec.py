@@ -164,12 +164,19 @@ def test_arena_round_trip_aliased():
     sc = S.config2(2)
     ab = RoutingPlan.from_scenario(sc)
     ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
-    arena = Arena(ab, ba, chunk_bytes=2 << 20)
+    # cap = the most-aliased plan's footprint: the arena must pick one group per stage
+    # (with room to spare it would run everything as one stage and alias nothing)
+    from paper_2605_18815_b200.api import memory_plan
+    most, viol, _, _ = memory_plan(ab, ba, chunk_bytes=2 << 20, groups=0)
+    assert viol == 0
+    arena = Arena(ab, ba, chunk_bytes=2 << 20, cap_bytes=most.physical_bytes)
     st = arena.stats()
-    assert st.aliased_bytes > 0
+    assert st.aliased_bytes > 0 and st.physical_bytes == most.physical_bytes
+    assert list(st.stage_groups) == list(most.stage_groups)
     assert st.physical_bytes < st.a_bytes + st.b_bytes
     e1, e2 = Executor(ab), Executor(ba)
     arena.bind(e1, e2)
+    assert e1.num_stages() == st.stage_groups[0] and e2.num_stages() == st.stage_groups[1]
     e1.fill(0, SEED)
     e1.prepare()
     e2.prepare()
@@ -211,3 +218,42 @@ def test_multi_gpu_arena_stages():
                         os.path.join(root, "tests", "mgpu_arena_check.py"), "2"],
                        capture_output=True, text=True, timeout=900)
     assert "ARENA_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_multicast_broadcast_grow():
+    """Broadcast promotion over NVLS multicast (config 3 grow DP4 -> DP8): the joiners'
+    parameters leave the root once through a multicast object; bit-exact against canon.
+    Needs >= 3 GPUs (a broadcast group spans >= 2 GPUs besides the root)."""
+    import json
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 4:
+        pytest.skip("needs 4 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+                        "--master-addr", "127.0.0.1", "--master-port", "29535",
+                        os.path.join(root, "tools", "bcast_bench.py"), "--layers", "2", "--reps", "2"],
+                       capture_output=True, text=True, timeout=900)
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert line, r.stdout[-3000:] + r.stderr[-3000:]
+    d = json.loads(line[-1])
+    assert d["push"]["mismatches"] == 0
+    assert d["bcast_groups"] and d["multicast"]["mismatches"] == 0
+    assert d["multicast"]["mc_gb_rank0"] > 0
+
+
+def test_broadcast_groups_need_two_remote_gpus():
+    """Broadcast detection (one GPU is enough to list the groups): config 3
+    grow at 4 GPUs yields the two per-slot parameter groups rooted at rank 0; at 2 GPUs
+    every joiner sits on one GPU and nothing is promoted."""
+    from paper_2605_18815_b200 import scenarios as S
+    from paper_2605_18815_b200.api import Executor, RoutingPlan
+    _, grow = S.config3(2)
+    plan = RoutingPlan.from_scenario(grow)
+    ex4 = Executor(plan, n_gpus=4, gpu=0, device=0)
+    g4 = [g for g in ex4.bcast_groups() if g.payload_bytes > 1 << 20]
+    assert [(g.root_rank, g.slot, list(g.member_rank[: g.n_members])) for g in g4] == [(0, 0, [4, 6]), (0, 1, [5, 7])]
+    assert all(g.payload_bytes == g4[0].payload_bytes for g in g4)
+    ex2 = Executor(plan, n_gpus=2, gpu=0, device=0)
+    assert not [g for g in ex2.bcast_groups() if g.payload_bytes > 1 << 20]

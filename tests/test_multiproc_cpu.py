@@ -115,3 +115,4 @@ def test_memory_plan_per_gpu_is_safe():
     st, viol = A.ArenaStats_t(), C.c_int64()
     A.check(A.lib().rs_memory_plan(ab.h, ba.h, 0, 0, C.byref(st), C.byref(viol), None, None, 0))
     assert viol.value == 0
+

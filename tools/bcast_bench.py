@@ -1,0 +1,124 @@
+"""Broadcast promotion over NVLS multicast on BASELINE config 3's grow (Llama-3-8B
+DP4 -> DP8, ZeRO-1): the joiners' parameters (every DP replica needs the whole model)
+go from the root GPU as ONE multicast store stream instead of one push per joiner.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bcast_bench.py [--layers L]
+
+Both variants run on the same multi-GPU arena (VMM buffers, shared by descriptors) and
+are verified bit-exact against canon. Prints one JSON line (rank 0) with the forward
+transition time (max over ranks) of: per-destination pushes, and multicast.
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
+from paper_2605_18815_b200.runtime import (Transition, dist_env, exchange_arena, global_stage_cuts,  # noqa: E402
+                                           setup_multicast)
+
+
+def timed(ex, stream, reps, world):
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ex.run(stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    mine = torch.tensor([min(ts)], dtype=torch.float64, device="cuda")
+    per = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(per, mine)
+    t = torch.tensor([min(ts), sum(ts) / len(ts)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist() + [[round(x.item(), 3) for x in per]]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--chunk-mb", type=int, default=512,
+                    help="arena chunk (multicast binds chunk by chunk; 512 MiB = the recommended granularity)")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _, grow = S.config3(args.layers)
+    plan = RoutingPlan.from_scenario(grow)
+    arena = Arena.multi(plan, None, world, rank, local, chunk_bytes=args.chunk_mb << 20, groups=1)
+    exchange_arena(arena, rank, world, tag=f"{os.environ.get('MASTER_PORT', '0')}-bcast")
+    tr = Transition(plan, world, rank, local, alloc=False)
+    arena.bind(tr.ex, None, global_stage_cuts(arena, world))
+    ex = tr.ex
+    stream = torch.cuda.current_stream()
+    seed = 0xB0CA57
+    out = {"workload": f"llama3-8b (L={args.layers}) dp4->dp8 zero1 grow (config 3)", "n_gpus": world,
+           "chunk_mb": args.chunk_mb,
+           "plan_bytes": plan.bytes_moved()}
+
+    ex.prepare()
+    ex.fill(A.SIDE_SRC, seed)
+    ex.run(stream.cuda_stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    bad_push = ex.verify(A.SIDE_DST, seed)[0]
+    push_min, push_avg, push_per = timed(ex, stream, args.reps, world)
+    st = ex.stats()
+    out["push"] = {"ms_min": round(push_min, 3), "ms_avg": round(push_avg, 3), "mismatches": int(bad_push), "ms_per_rank": push_per,
+                   "remote_gb_rank0": round(st.remote_bytes / 1e9, 2)}
+
+    groups = ex.bcast_groups()
+    out["bcast_groups"] = [{"id": g.id, "root_rank": g.root_rank, "root_gpu": g.root_gpu, "slot": g.slot,
+                            "member_gpus": list(g.member_gpu[: g.n_members]),
+                            "member_ranks": list(g.member_rank[: g.n_members]),
+                            "payload_gb": round(g.payload_bytes / 1e9, 3)} for g in groups]
+    mcs = []
+    if groups:
+        mcs = setup_multicast(arena, ex, rank, world, local, tag=f"{os.environ.get('MASTER_PORT', '0')}-bcast",
+                              min_payload=1 << 20)
+        ex.prepare()
+        # clear the destinations so the check proves the multicast delivered them
+        ex.fill(A.SIDE_DST, seed ^ 0x5A5A)
+        ex.fill(A.SIDE_SRC, seed)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ex.run(stream.cuda_stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        bad_mc = ex.verify(A.SIDE_DST, seed)[0]
+        bad_src = ex.verify(A.SIDE_SRC, seed)[0]  # the root's bound source is rewritten in place
+        mc_min, mc_avg, mc_per = timed(ex, stream, args.reps, world)
+        st = ex.stats()
+        t = torch.tensor([bad_mc + bad_src], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        out["multicast"] = {"ms_min": round(mc_min, 3), "ms_avg": round(mc_avg, 3), "mismatches": int(t.item()),
+                            "ms_per_rank": mc_per, "mc_gb_rank0": round(st.mc_bytes / 1e9, 2),
+                            "remote_gb_rank0": round(st.remote_bytes / 1e9, 2)}
+        out["speedup"] = round(push_min / mc_min, 3)
+    t = torch.tensor([bad_push], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    out["push"]["mismatches"] = int(t.item())
+    for m in mcs:
+        m.close()
+    del ex, tr, arena
+    torch.cuda.synchronize()
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

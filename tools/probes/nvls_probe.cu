@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <string>
 #include <vector>
 
 #define CK(x) do { CUresult r = (x); if (r != CUDA_SUCCESS) { const char* s; cuGetErrorString(r, &s); printf("ERR %s line %d: %s\n", #x, __LINE__, s); return 1; } } while (0)
@@ -17,7 +18,11 @@ __global__ void mc_store(const uint4* __restrict__ src, uint4* mc, size_t n) {
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
+    // argv[1] == "unbound-root": GPU 0 joins the multicast object but binds no memory
+    const bool unbound_root = argc > 1 && std::string(argv[1]) == "unbound-root";
+    // "self-src": the root reads the very memory it has bound (the executor's layout identity)
+    const bool self_src = argc > 1 && std::string(argv[1]) == "self-src";
     CK(cuInit(0));
     int n = 0;
     CR(cudaGetDeviceCount(&n));
@@ -45,6 +50,7 @@ int main() {
     std::vector<CUdeviceptr> uc(n);
     for (int d = 0; d < n; ++d) {
         CR(cudaSetDevice(d));
+        if (d == 0 && unbound_root) continue;
         CUmemAllocationProp p = {};
         p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
         p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -70,7 +76,11 @@ int main() {
     a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
     CK(cuMemSetAccess(mcva, bytes, &a, 1));
     void* src;
-    CR(cudaMalloc(&src, bytes));
+    if (self_src) {
+        src = (void*)uc[0];
+    } else {
+        CR(cudaMalloc(&src, bytes));
+    }
     CR(cudaMemset(src, 0x5A, bytes));
     CR(cudaDeviceSynchronize());
     cudaEvent_t e0, e1;
@@ -92,7 +102,7 @@ int main() {
                best, bytes / best / 1e6, (double)n * bytes / best / 1e6);
     }
     int ok = 1;
-    for (int d = 0; d < n; ++d) {
+    for (int d = unbound_root ? 1 : 0; d < n; ++d) {
         CR(cudaSetDevice(d));
         unsigned char h[16];
         CR(cudaMemcpy(h, (void*)(uc[d] + bytes - 16), 16, cudaMemcpyDeviceToHost));
