@@ -141,6 +141,31 @@ int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len);
 typedef struct {
     int64_t local_bytes, out_bytes, in_bytes, ops;
 } rs_placement_stats_t;
+/* ---- state layout of one virtual rank (the buffer contract): what a
+ * training job needs to register its tensors as views into the transition buffers
+ * (PAPER.md:938-939). side: RS_SIDE_SRC / RS_SIDE_DST. */
+typedef struct {
+    int tensor;                  /* index in the model's declaration order */
+    int expert;                  /* 1: lives in the expert span */
+    int64_t box_lo[4], box_hi[4];/* the rank's box of the tensor (tensor coordinates) */
+    int64_t local_lo, local_hi;  /* element range in its span (dense or expert) */
+    int64_t param_byte_off;      /* byte offset in the param buffer */
+    int64_t elem_off;            /* element offset in the param-geometry buffers (grads) */
+} rs_segment_t;
+typedef struct {
+    int phys, n_segments;
+    int64_t dense_len, expert_len;          /* elements */
+    int64_t dshard_lo, dshard_hi;           /* ZeRO shard of the dense span (whole span without ZeRO) */
+    int64_t eshard_lo, eshard_hi;           /* ... of the expert span */
+    int64_t param_bytes, nelem, optim_len;  /* optimizer buffers: [dense shard | expert shard], fp32 each */
+    int64_t scalar_bytes;                   /* scalar blob (scalar_words x 8 B) */
+} rs_rank_geom_t;
+int rs_plan_rank_geom(const rs_plan_t* p, int side, int rank, rs_rank_geom_t* out);
+int rs_plan_segments(const rs_plan_t* p, int side, int rank, rs_segment_t* out, int cap, int* n);
+/* tensor `index` of the model: id (NUL-terminated into id_buf), shape, dtype bytes */
+int rs_plan_tensor(const rs_plan_t* p, int index, char* id_buf, int cap, int64_t shape[4], int* ndim, int* dtype_bytes);
+int rs_plan_num_tensors(const rs_plan_t* p, int* n);
+
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
 /* validate_plan: invariants + destination coverage; violations are
  * returned (one per line), not raised. drop >= 0 removes one fragment first (fault

@@ -396,6 +396,76 @@ int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64
     });
 }
 
+namespace {
+const core::RankGeom& rank_geom(const rs_plan_t* p, int side, int rank) {
+    if (side != RS_SIDE_SRC && side != RS_SIDE_DST) throw ConfigError("bad side");
+    const core::Side& S = side == RS_SIDE_SRC ? p->core.src : p->core.dst;
+    if (rank < 0 || rank >= static_cast<int>(S.ranks.size())) throw ConfigError("rank out of range");
+    return S.ranks[static_cast<size_t>(rank)];
+}
+}  // namespace
+
+int rs_plan_rank_geom(const rs_plan_t* p, int side, int rank, rs_rank_geom_t* out) {
+    return guarded([&] {
+        const core::RankGeom& g = rank_geom(p, side, rank);
+        out->phys = g.phys;
+        out->n_segments = static_cast<int>(g.segs.size());
+        out->dense_len = g.dense_len;
+        out->expert_len = g.expert_len;
+        out->dshard_lo = g.dshard.lo;
+        out->dshard_hi = g.dshard.hi;
+        out->eshard_lo = g.eshard.lo;
+        out->eshard_hi = g.eshard.hi;
+        out->param_bytes = g.param_bytes;
+        out->nelem = g.nelem;
+        out->optim_len = g.optim_len;
+        out->scalar_bytes = p->core.opts.scalar_words * kScalarWordBytes;
+        return RS_OK;
+    });
+}
+
+int rs_plan_segments(const rs_plan_t* p, int side, int rank, rs_segment_t* out, int cap, int* n) {
+    return guarded([&] {
+        const core::RankGeom& g = rank_geom(p, side, rank);
+        *n = static_cast<int>(g.segs.size());
+        for (int i = 0; i < *n && i < cap; ++i) {
+            const core::Seg& sg = g.segs[static_cast<size_t>(i)];
+            rs_segment_t& o = out[i];
+            o.tensor = sg.tensor;
+            o.expert = sg.expert ? 1 : 0;
+            for (int d = 0; d < 4; ++d) o.box_lo[d] = sg.blo[d], o.box_hi[d] = sg.bhi[d];
+            o.local_lo = sg.local_lo;
+            o.local_hi = sg.local_hi;
+            o.param_byte_off = sg.param_byte_off;
+            o.elem_off = sg.elem_off;
+        }
+        return RS_OK;
+    });
+}
+
+int rs_plan_num_tensors(const rs_plan_t* p, int* n) {
+    return guarded([&] {
+        *n = p->core.ntensors();
+        return RS_OK;
+    });
+}
+
+int rs_plan_tensor(const rs_plan_t* p, int index, char* id_buf, int cap, int64_t shape[4], int* ndim, int* dtype_bytes) {
+    return guarded([&] {
+        if (index < 0 || index >= p->core.ntensors()) throw ConfigError("tensor index out of range");
+        const TensorSpec& t = p->core.space->entries()[static_cast<size_t>(index)].spec;
+        if (cap > 0) {
+            const size_t k = std::min(static_cast<size_t>(cap - 1), t.tensor_id.size());
+            std::memcpy(id_buf, t.tensor_id.data(), k);
+            id_buf[k] = 0;
+        }
+        *ndim = static_cast<int>(t.shape.size());
+        for (int d = 0; d < 4; ++d) shape[d] = d < *ndim ? t.shape[static_cast<size_t>(d)] : 1;
+        *dtype_bytes = t.dtype_bytes;
+        return RS_OK;
+    });
+}
+
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out) {
     return guarded([&] {
         if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad placement");
