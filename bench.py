@@ -337,6 +337,15 @@ def run_ours(args):
                     "frac": round(achieved_hbm / pk["hbm_gbs"], 4), "traffic": None, "peak_source": pk["source"],
                     "kernel": "bulk_tiles_kernel<4,32K> (TMA bulk, forward transition)",
                     "algorithmic_bytes_per_launch": local_rw}
+            # DRAM read + write of the same forward transition from the committed ncu capture
+            # (one launch per concurrency group, summed like `achieved`)
+            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic_n1_L32.json")
+            if args.layers == 32 and os.path.exists(tp):
+                with open(tp) as f:
+                    cap = json.load(f)
+                if cap.get("algorithmic_bytes_forward") == local_rw:
+                    roof["traffic"] = cap["forward"]["traffic"]
+                    roof["traffic_source"] = "profiles/r01_traffic_n1_L32.json (ncu dram__bytes_read.sum + write.sum)"
         else:
             # T_roof = max_g max(out_g / NVLink, in_g / NVLink, HBM_g / B_HBM); the
             # binding GPU's NVLink bytes over the measured (max over ranks) transition time
