@@ -347,6 +347,9 @@ int rs_exec_fill(rs_exec_t* e, int side, uint64_t seed, void* stream);
 int rs_exec_run(rs_exec_t* e, void* stream, int* launches);
 /* verify_state on this GPU's ranks of one side */
 int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t* mismatches, int64_t* first_bad);
+/* copy `bytes` at `offset` of a buffer this GPU can address into host memory (a result
+ * readback; synchronous on `stream`) */
+int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream);
 int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out);
 
 #ifdef __cplusplus

@@ -481,6 +481,14 @@ def _exec_set_multicast(self, group_id: int, mc_va: int) -> None:
     A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
 
 
+def _exec_read(self, side: int, rank: int, buf: int, offset: int, nbytes: int, stream: int = 0) -> bytes:
+    """Read `nbytes` of a buffer back to the host (synchronous on `stream`)."""
+    out = C.create_string_buffer(nbytes)
+    A.check(A.lib().rs_exec_read(self.h, side, rank, buf, offset, out, nbytes, C.c_void_p(stream)))
+    return out.raw
+
+
+Executor.read = _exec_read
 Executor.bcast_groups = _exec_bcast_groups
 Executor.set_multicast = _exec_set_multicast
 

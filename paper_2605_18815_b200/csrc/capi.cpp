@@ -761,6 +761,21 @@ int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t*
     });
 }
 
+int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream) {
+    return guarded([&] {
+        if (side < 0 || side > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
+        std::int64_t n = 0;
+        void* p = e->ex->buffer(side, rank, buf, &n);
+        if (!p || offset < 0 || bytes < 0 || offset + bytes > n) throw ConfigError("read outside the buffer");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (cudaMemcpyAsync(host, static_cast<const char*>(p) + offset, static_cast<size_t>(bytes), cudaMemcpyDeviceToHost,
+                            st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            throw exec::CudaError("rs_exec_read: copy failed");
+        return RS_OK;
+    });
+}
+
 int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
     return guarded([&] {
         const exec::ExecStats& s = e->ex->stats();

@@ -748,6 +748,7 @@ void Executor::prepare(bool staged) {
     const char* sr = std::getenv("RS_SPLIT_REMOTE");
     split_remote_ = sr && std::string(sr) == "1";
     const std::vector<CopyOp> ops = build_ops(P_);
+    const auto t_ops = std::chrono::steady_clock::now();
     stats_ = ExecStats{};
     staged_ = staged;
     has_remote_ = false;
@@ -867,8 +868,9 @@ void Executor::prepare(bool staged) {
     }
     if (std::getenv("RS_TIMING")) {
         const auto t_end = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[reshard] prepare: ops+tiles %.1f ms, upload %.1f ms, %lld tiles\n",
-                     std::chrono::duration<double, std::milli>(t_tiles - t_begin).count(),
+        std::fprintf(stderr, "[reshard] prepare: ops %.1f ms (%zu), tiles %.1f ms, finalize+upload %.1f ms, %lld tiles\n",
+                     std::chrono::duration<double, std::milli>(t_ops - t_begin).count(), ops.size(),
+                     std::chrono::duration<double, std::milli>(t_tiles - t_ops).count(),
                      std::chrono::duration<double, std::milli>(t_end - t_tiles).count(),
                      static_cast<long long>(stats_.tiles));
     }

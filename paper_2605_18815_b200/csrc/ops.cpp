@@ -136,20 +136,28 @@ std::vector<CopyOp> build_ops(const PlanCore& P) {
     for (const stair::Triple& T : P.triples)
         if (!overridden(T.dst, T.tensor)) E.triple(T);
     for (const stair::Triple& T : P.retain_triples) E.triple(T);
-    for (const core::FlatXfer& f : P.d2_runs) {
-        // only the overridden tensors of a D2 route come from runs
-        core::FlatXfer g = f;
-        const auto& ents = P.space->entries();
-        std::int64_t x = g.lo;
-        while (x < g.hi) {
-            auto it = std::upper_bound(ents.begin(), ents.end(), x,
-                                       [](std::int64_t v, const ModelSpace::Entry& e) { return v < e.offset; });
-            const int t = static_cast<int>(it - ents.begin()) - 1;
-            const std::int64_t tend = ents[static_cast<size_t>(t)].offset + ents[static_cast<size_t>(t)].spec.numel();
-            const std::int64_t end = std::min(g.hi, tend);
-            if (overridden(g.dst, t)) E.flat_run(core::FlatXfer{x, end, g.src, g.dst});
-            x = end;
+    // only the overridden tensors of a D2 route come from runs. Runs are sorted by
+    // (src, dst, lo) and disjoint within a (src, dst) group, so each overridden tensor's
+    // runs are found by binary search (the D2 list holds every run of the route: ~1.8 M
+    // for the north star's way back, of which a few hundred belong to flagged tensors)
+    const std::vector<core::FlatXfer>& R = P.d2_runs;
+    const auto& ents = P.space->entries();
+    for (size_t i = 0; i < R.size();) {
+        const int src = R[i].src, dst = R[i].dst;
+        const size_t e = static_cast<size_t>(
+            std::partition_point(R.begin() + static_cast<std::ptrdiff_t>(i), R.end(),
+                                 [&](const core::FlatXfer& f) { return f.src == src && f.dst == dst; }) -
+            R.begin());
+        for (int t = 0; t < nt; ++t) {
+            if (!overridden(dst, t)) continue;
+            const std::int64_t tlo = ents[static_cast<size_t>(t)].offset;
+            const std::int64_t thi = tlo + ents[static_cast<size_t>(t)].spec.numel();
+            auto it = std::partition_point(R.begin() + static_cast<std::ptrdiff_t>(i), R.begin() + static_cast<std::ptrdiff_t>(e),
+                                           [&](const core::FlatXfer& f) { return f.hi <= tlo; });
+            for (; it != R.begin() + static_cast<std::ptrdiff_t>(e) && it->lo < thi; ++it)
+                E.flat_run(core::FlatXfer{std::max(it->lo, tlo), std::min(it->hi, thi), src, dst});
         }
+        i = e;
     }
     if (P.has_scalars)
         for (int j = 0; j < P.dst_cfg.world_size(); ++j)

@@ -116,3 +116,14 @@ def test_memory_plan_per_gpu_is_safe():
     A.check(A.lib().rs_memory_plan(ab.h, ba.h, 0, 0, C.byref(st), C.byref(viol), None, None, 0))
     assert viol.value == 0
 
+
+
+def test_placement_covers_d2_plan_exactly():
+    """The way back (DP2xTP4 -> TP8, D2 extension): the ops cover every plan byte and
+    every retained byte once (flagged tensors' runs come from the D2 list)."""
+    from paper_2605_18815_b200 import scenarios as S
+    from paper_2605_18815_b200.api import RoutingPlan
+    for L in (1, 2):
+        plan = RoutingPlan.from_scenario(S.config2(L).reversed(), allow_oversourced=True)
+        st = plan.placement(1, 0)
+        assert st.local_bytes == plan.bytes_moved() - 7 * 64 + plan.bytes_retained() + 8 * 64
