@@ -116,10 +116,12 @@ std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device,
         void* dTmp = nullptr;
         size_t tmp_bytes = 0;
         cudaStream_t s = nullptr;
-        cudaEvent_t e0, e1;
+        cudaEvent_t e0, e1, ea, eb;  // kernel time = [e0, ea] (count + scan) + [eb, e1] (write)
         RS_CUDA_P(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         RS_CUDA_P(cudaEventCreate(&e0));
         RS_CUDA_P(cudaEventCreate(&e1));
+        RS_CUDA_P(cudaEventCreate(&ea));
+        RS_CUDA_P(cudaEventCreate(&eb));
         try {
             RS_CUDA_P(cudaMalloc(&dT, trip.size() * sizeof(stair::Triple)));
             RS_CUDA_P(cudaMalloc(&dOff, off.size() * sizeof(long long)));
@@ -136,11 +138,13 @@ std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device,
             RS_CUDA_P(cudaEventRecord(e0, s));
             count_kernel<<<blocks, threads, 0, s>>>(dT, dOff, static_cast<int>(trip.size()), nrows, dStarts);
             cub::DeviceScan::ExclusiveSum(dTmp, tmp_bytes, dStarts, dIdx, nrows + 1, s);
+            RS_CUDA_P(cudaEventRecord(ea, s));
             int total = 0;
             RS_CUDA_P(cudaMemcpyAsync(&total, dIdx + nrows, sizeof(int), cudaMemcpyDeviceToHost, s));
             RS_CUDA_P(cudaStreamSynchronize(s));
             RS_CUDA_P(cudaMalloc(&dOut, static_cast<size_t>(total > 0 ? total : 1) * sizeof(core::FlatXfer)));
             RS_CUDA_P(cudaMemsetAsync(dOut, 0, static_cast<size_t>(total > 0 ? total : 1) * sizeof(core::FlatXfer), s));
+            RS_CUDA_P(cudaEventRecord(eb, s));
             write_kernel<<<blocks, threads, 0, s>>>(dT, dOff, static_cast<int>(trip.size()), nrows, dIdx, dOut);
             RS_CUDA_P(cudaEventRecord(e1, s));
             RS_CUDA_P(cudaGetLastError());
@@ -148,16 +152,17 @@ std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device,
             RS_CUDA_P(cudaMemcpyAsync(out.data(), dOut, static_cast<size_t>(total) * sizeof(core::FlatXfer),
                                       cudaMemcpyDeviceToHost, s));
             RS_CUDA_P(cudaStreamSynchronize(s));
-            float ms = 0;
-            cudaEventElapsedTime(&ms, e0, e1);
-            if (kernel_ms) *kernel_ms = ms;
+            float m1 = 0, m2 = 0;
+            cudaEventElapsedTime(&m1, e0, ea);
+            cudaEventElapsedTime(&m2, eb, e1);
+            if (kernel_ms) *kernel_ms = m1 + m2;
         } catch (...) {
             cudaFree(dT), cudaFree(dOff), cudaFree(dStarts), cudaFree(dIdx), cudaFree(dOut), cudaFree(dTmp);
             cudaStreamDestroy(s);
             throw;
         }
         cudaFree(dT), cudaFree(dOff), cudaFree(dStarts), cudaFree(dIdx), cudaFree(dOut), cudaFree(dTmp);
-        cudaEventDestroy(e0), cudaEventDestroy(e1);
+        cudaEventDestroy(e0), cudaEventDestroy(e1), cudaEventDestroy(ea), cudaEventDestroy(eb);
         cudaStreamDestroy(s);
     }
     if (P.d2_runs.empty()) return out;
