@@ -1,0 +1,119 @@
+"""BASELINE's other configurations through the same fused executor (SURVEY §8d
+"Other configs"), one direction each, bit-exact verified, timed max over ranks, with
+the §8d roofline T_roof = max_g max(out_g / NVLink, in_g / NVLink, HBM_g / B_HBM).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/configs_bench.py [--config 4 --layers 48]
+
+Prints one JSON line per configuration (rank 0). Config 5 (Llama-3-70B) needs 247 GB of
+old + new state per GPU at N=8; on fewer GPUs pass --layers to scale its depth.
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+
+NVLINK_GBS = 900.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f).get("hbm_gbs", 6558.0))
+    except (OSError, ValueError):
+        return 6558.0
+
+
+def scenario(cfg: int, layers: int):
+    if cfg == 1:
+        return S.config1()
+    if cfg == 2:
+        return S.config2(layers or 32)
+    if cfg == 3:
+        return S.config3(layers or 32)[1]
+    if cfg == 4:
+        return S.config4(layers or 48)
+    if cfg == 5:
+        return S.config5(layers or 80)
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def run_one(sc, rank, world, local, reps):
+    plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+    tr = Transition(plan, world, rank, local)
+    tr.connect()
+    ex = tr.ex
+    seed = 0x5EED5
+    ex.fill(A.SIDE_SRC, seed)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ex.run(stream.cuda_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    bad = ex.verify(A.SIDE_DST, seed)[0]
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ex.run(stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = torch.tensor([min(ts), float(bad)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, bad = t.tolist()
+    pl = [plan.placement(world, g) for g in range(world)]
+    link = max(max(p.out_bytes, p.in_bytes) for p in pl)
+    hbm = max(2 * p.local_bytes + p.out_bytes + p.in_bytes for p in pl)
+    hbm_gbs = peaks()
+    t_roof = max(link / (NVLINK_GBS * 1e9), hbm / (hbm_gbs * 1e9))
+    out = {"config": sc.name, "n_gpus": world, "plan_bytes": plan.bytes_moved(), "retained_bytes": plan.bytes_retained(),
+           "transfers": plan.num_transfers(), "ms": round(ms, 3), "mismatches": int(bad),
+           "gbs_per_gpu": round(plan.bytes_moved() / (ms / 1e3) / 1e9 / world, 1),
+           "roofline": {"bound": "nvlink" if link / NVLINK_GBS > hbm / hbm_gbs else "hbm",
+                        "t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms, 4),
+                        "max_link_gb": round(link / 1e9, 2), "max_hbm_gb": round(hbm / 1e9, 2),
+                        "peaks": {"nvlink_gbs": NVLINK_GBS, "hbm_gbs": hbm_gbs}}}
+    del tr, ex
+    torch.cuda.synchronize()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, action="append")
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    for cfg in args.config or [1, 4]:
+        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps)
+        if rank == 0:
+            print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
