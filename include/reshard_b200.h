@@ -324,6 +324,17 @@ int rs_mc_map(rs_mc_t* m, int device, void** mc_va);
 void rs_mc_destroy(rs_mc_t* m);
 int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64_t* bytes);
 
+/* one shareable VMM device buffer (POSIX-FD handle): state buffers that peers map
+ * without cudaIpc and a multicast object can bind. Import maps a peer's buffer for
+ * `device` (consumes fd). The size is rounded up to the VMM granularity (2 MiB). */
+typedef struct rs_vmm rs_vmm_t;
+int rs_vmm_alloc(int device, int64_t bytes, rs_vmm_t** out);
+int rs_vmm_import(int fd, int64_t bytes, int device, rs_vmm_t** out);
+int rs_vmm_export(const rs_vmm_t* v, int* fd);
+int rs_vmm_ptr(const rs_vmm_t* v, void** ptr, int64_t* mapped_bytes);
+void rs_vmm_free(rs_vmm_t* v);
+int rs_mc_bind_vmm(rs_mc_t* m, const rs_vmm_t* v, int64_t mc_offset);
+
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
 void rs_exec_destroy(rs_exec_t* e);
 int rs_exec_alloc(rs_exec_t* e);

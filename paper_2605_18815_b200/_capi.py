@@ -227,12 +227,19 @@ def _late_bindings(L):
         ("rs_mc_bind_arena", [vp, vp, C.c_int, C.c_int, C.c_int]),
         ("rs_mc_map", [vp, C.c_int, P(vp)]),
         ("rs_arena_bind_size", [vp, C.c_int, C.c_int, C.c_int, P(i64)]),
+        ("rs_vmm_alloc", [C.c_int, i64, P(vp)]),
+        ("rs_vmm_import", [C.c_int, i64, C.c_int, P(vp)]),
+        ("rs_vmm_export", [vp, P(C.c_int)]),
+        ("rs_vmm_ptr", [vp, P(vp), P(i64)]),
+        ("rs_mc_bind_vmm", [vp, vp, i64]),
     ):
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = C.c_int
     L.rs_mc_destroy.argtypes = [vp]
     L.rs_mc_destroy.restype = None
+    L.rs_vmm_free.argtypes = [vp]
+    L.rs_vmm_free.restype = None
     L.rs_plan_validate.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
                                    C.POINTER(C.c_int64)]
     L.rs_plan_validate.restype = C.c_int

@@ -531,6 +531,9 @@ class Multicast:
     def bind_arena(self, arena: "Arena", layout: int, rank: int, buf: int) -> None:
         A.check(A.lib().rs_mc_bind_arena(self.h, arena.h, layout, rank, buf))
 
+    def bind_vmm(self, buf: "VmmBuffer", mc_offset: int = 0) -> None:
+        A.check(A.lib().rs_mc_bind_vmm(self.h, buf.h, mc_offset))
+
     def map(self, device: int) -> int:
         va = C.c_void_p()
         A.check(A.lib().rs_mc_map(self.h, device, C.byref(va)))
@@ -539,6 +542,42 @@ class Multicast:
     def close(self) -> None:
         if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_mc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+class VmmBuffer:
+    """One shareable VMM device buffer (rs_vmm_*): allocated here, or a peer's imported
+    from its POSIX descriptor and mapped for this GPU."""
+
+    def __init__(self, handle: int, nbytes: int):
+        self.h, self.nbytes = handle, nbytes
+        p, n = C.c_void_p(), C.c_int64()
+        A.check(A.lib().rs_vmm_ptr(self.h, C.byref(p), C.byref(n)))
+        self.ptr, self.mapped_bytes = p.value, n.value
+
+    @classmethod
+    def alloc(cls, device: int, nbytes: int) -> "VmmBuffer":
+        h = C.c_void_p()
+        A.check(A.lib().rs_vmm_alloc(device, nbytes, C.byref(h)))
+        return cls(h.value, nbytes)
+
+    @classmethod
+    def import_fd(cls, fd: int, nbytes: int, device: int) -> "VmmBuffer":
+        h = C.c_void_p()
+        A.check(A.lib().rs_vmm_import(fd, nbytes, device, C.byref(h)))
+        return cls(h.value, nbytes)
+
+    def export_fd(self) -> int:
+        fd = C.c_int()
+        A.check(A.lib().rs_vmm_export(self.h, C.byref(fd)))
+        return fd.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None) and A is not None and A._lib is not None:
+            A.lib().rs_vmm_free(self.h)
             self.h = None
 
     def __del__(self):

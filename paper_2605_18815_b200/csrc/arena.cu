@@ -294,6 +294,67 @@ std::int64_t Arena::bind_size(int layout, int rank, int buf) const {
     return m.bytes < C / 4 ? (m.bytes + gran - 1) / gran * gran : (m.bytes + C - 1) / C * C;
 }
 
+namespace {
+std::int64_t vmm_round(int device, std::int64_t bytes) {
+    const CUmemAllocationProp p = device_prop(device, true);
+    size_t gran = 0;
+    drv_check(Drv::get().granularity(&gran, &p, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
+    const std::int64_t g = static_cast<std::int64_t>(gran);
+    return (std::max<std::int64_t>(bytes, 1) + g - 1) / g * g;
+}
+
+std::uint64_t vmm_map(std::uint64_t handle, std::int64_t size, int device) {
+    const Drv& D = Drv::get();
+    CUdeviceptr va = 0;
+    drv_check(D.reserve(&va, static_cast<size_t>(size), 0, 0, 0), "cuMemAddressReserve");
+    drv_check(D.map(va, static_cast<size_t>(size), 0, handle, 0), "cuMemMap");
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    drv_check(D.set_access(va, static_cast<size_t>(size), &acc, 1), "cuMemSetAccess");
+    return va;
+}
+}  // namespace
+
+VmmBuffer::VmmBuffer(int device, std::int64_t bytes) : bytes_(bytes), device_(device) {
+    if (cudaSetDevice(device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    size_ = vmm_round(device, bytes);
+    const CUmemAllocationProp p = device_prop(device, true);
+    CUmemGenericAllocationHandle h;
+    drv_check(Drv::get().create(&h, static_cast<size_t>(size_), &p, 0), "cuMemCreate");
+    handle_ = h;
+    va_ = vmm_map(handle_, size_, device);
+}
+
+VmmBuffer::VmmBuffer(int fd, std::int64_t bytes, int device) : bytes_(bytes), device_(device) {
+    if (cudaSetDevice(device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    const Drv& D = Drv::get();
+    CUmemGenericAllocationHandle h;
+    const CUresult r = D.import_fd(&h, reinterpret_cast<void*>(static_cast<std::intptr_t>(fd)),
+                                   CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    ::close(fd);
+    drv_check(r, "cuMemImportFromShareableHandle");
+    handle_ = h;
+    size_ = vmm_round(device, bytes);
+    va_ = vmm_map(handle_, size_, device);
+}
+
+VmmBuffer::~VmmBuffer() {
+    const Drv& D = Drv::get();
+    if (va_) {
+        D.unmap(va_, static_cast<size_t>(size_));
+        D.addr_free(va_, static_cast<size_t>(size_));
+    }
+    if (handle_) D.release(handle_);
+}
+
+int VmmBuffer::export_fd() const {
+    int fd = -1;
+    drv_check(Drv::get().export_fd(&fd, handle_, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0), "cuMemExportToShareableHandle");
+    return fd;
+}
+
 void Arena::bind_multicast(Multicast& mc, int layout, int rank, int buf) const {
     const BufMap& m = bufs_[layout][static_cast<size_t>(rank) * exec::kNumBufs + buf];
     if (m.remote || m.bytes == 0) throw ConfigError("bind_multicast: buffer is not hosted by this GPU");

@@ -1088,6 +1088,54 @@ int rs_mc_map(rs_mc_t* m, int device, void** mc_va) {
 
 void rs_mc_destroy(rs_mc_t* m) { delete m; }
 
+struct rs_vmm {
+    std::unique_ptr<mem::VmmBuffer> v;
+};
+
+int rs_vmm_alloc(int device, int64_t bytes, rs_vmm_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto v = std::make_unique<rs_vmm>();
+        v->v = std::make_unique<mem::VmmBuffer>(device, bytes);
+        *out = v.release();
+        return RS_OK;
+    });
+}
+
+int rs_vmm_import(int fd, int64_t bytes, int device, rs_vmm_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto v = std::make_unique<rs_vmm>();
+        v->v = std::make_unique<mem::VmmBuffer>(fd, bytes, device);
+        *out = v.release();
+        return RS_OK;
+    });
+}
+
+int rs_vmm_export(const rs_vmm_t* v, int* fd) {
+    return guarded([&] {
+        *fd = v->v->export_fd();
+        return RS_OK;
+    });
+}
+
+int rs_vmm_ptr(const rs_vmm_t* v, void** ptr, int64_t* mapped_bytes) {
+    return guarded([&] {
+        *ptr = v->v->ptr();
+        *mapped_bytes = v->v->mapped_bytes();
+        return RS_OK;
+    });
+}
+
+void rs_vmm_free(rs_vmm_t* v) { delete v; }
+
+int rs_mc_bind_vmm(rs_mc_t* m, const rs_vmm_t* v, int64_t mc_offset) {
+    return guarded([&] {
+        m->m->bind(*v->v, mc_offset);
+        return RS_OK;
+    });
+}
+
 int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64_t* bytes) {
     return guarded([&] {
         if (layout < 0 || layout > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");

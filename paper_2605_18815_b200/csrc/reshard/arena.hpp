@@ -122,6 +122,30 @@ private:
     int n_gpus_ = 1;
 };
 
+/// One shareable VMM device buffer (POSIX-FD handle): allocated on this process's GPU,
+/// or imported from a peer process and mapped for this GPU (P2P over NVLink). State
+/// buffers a multicast object can bind and peers can map without cudaIpc.
+class VmmBuffer {
+public:
+    VmmBuffer(int device, std::int64_t bytes);             // allocate + map locally
+    VmmBuffer(int fd, std::int64_t bytes, int device);     // import a peer's (consumes fd), map for `device`
+    ~VmmBuffer();
+    VmmBuffer(const VmmBuffer&) = delete;
+    VmmBuffer& operator=(const VmmBuffer&) = delete;
+
+    void* ptr() const { return reinterpret_cast<void*>(va_); }
+    std::int64_t bytes() const { return bytes_; }        // requested size
+    std::int64_t mapped_bytes() const { return size_; }  // rounded to the VMM granularity
+    std::uint64_t handle() const { return handle_; }
+    int device() const { return device_; }
+    int export_fd() const;
+
+private:
+    std::uint64_t handle_ = 0, va_ = 0;
+    std::int64_t bytes_ = 0, size_ = 0;
+    int device_ = 0;
+};
+
 /// NVLS multicast object shared by the processes of its member GPUs (created by the
 /// root, passed as a POSIX descriptor). Protocol: create/import -> add_device on every
 /// member -> (barrier) -> bind memory -> map (root) -> multimem stores.
@@ -136,6 +160,7 @@ public:
     int export_fd() const;
     void add_device(int device);
     void bind(int device, std::uint64_t mem_handle, std::int64_t mc_offset, std::int64_t bytes);
+    void bind(const VmmBuffer& b, std::int64_t mc_offset) { bind(b.device(), b.handle(), mc_offset, b.mapped_bytes()); }
     void* map(int device);
     std::int64_t bytes() const { return bytes_; }
     std::uint64_t handle() const { return handle_; }

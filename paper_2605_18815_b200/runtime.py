@@ -229,25 +229,111 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
     return arena, global_stage_cuts(arena, world)
 
 
-def setup_multicast(arena, ex: Executor, rank: int, world: int, device: int, tag: str = "0", min_payload: int = 0):
+def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str = "0", group=None,
+                  adopt: Optional[dict] = None) -> dict:
+    """Shareable VMM buffers for every buffer of the virtual ranks this GPU hosts (both
+    sides); `adopt` maps (side, rank, buf) to VmmBuffers to reuse (the current state as
+    the source). Destination buffers are passed to every peer by POSIX descriptor (fdx)
+    and mapped there, so the fused push writes into them; everything is bound into
+    tr.ex. Collective over `group` (gloo in the EDM side thread). Returns
+    {(side, rank, buf): VmmBuffer} for local buffers plus ("peer", side, rank, buf) keys
+    for the mapped peers' buffers (keep it alive while the executor runs)."""
+    import pickle
+    import threading
+
+    import torch.distributed as dist
+
+    from .api import VmmBuffer, fdx_close, fdx_listen, fdx_recv, fdx_send
+    adopt = adopt or {}
+    out = {}
+    ex = tr.ex
+    table = []
+    for side in (A.SIDE_SRC, A.SIDE_DST):
+        nr = tr.plan.summary.src_world if side == A.SIDE_SRC else tr.plan.summary.dst_world
+        for r in range(nr):
+            for b in range(6):
+                _, n, g = ex.buffer(side, r, b)
+                if not n or g != ex.gpu:
+                    continue
+                buf = adopt.get((side, r, b))
+                if buf is None or buf.nbytes < n:
+                    buf = VmmBuffer.alloc(device, n)
+                out[(side, r, b)] = buf
+                ex.bind(side, r, b, buf.ptr, n)
+                if side == A.SIDE_DST:
+                    table.append((r, b, n))
+    if world < 2:
+        return out
+    sock = fdx_listen(f"reshard-vmm-{tag}-{rank}")
+    dist.barrier(group=group)
+    errors = []
+    received = []
+
+    def receive():
+        try:
+            for _ in range(world - 1):
+                fds, payload = fdx_recv(sock)
+                rows = pickle.loads(payload)
+                for fd, (r, b, n) in zip(fds, rows):
+                    received.append((r, b, n, VmmBuffer.import_fd(fd, n, device)))
+        except BaseException as e:  # surfaced below
+            errors.append(e)
+
+    t = threading.Thread(target=receive, name="vmm-import")
+    t.start()
+    for peer in range(world):
+        if peer == rank:
+            continue
+        fds = [out[(A.SIDE_DST, r, b)].export_fd() for r, b, _ in table]
+        try:
+            fdx_send(f"reshard-vmm-{tag}-{peer}", fds, pickle.dumps(table))
+        finally:
+            for fd in fds:
+                os.close(fd)
+    t.join()
+    fdx_close(sock)
+    if errors:
+        raise errors[0]
+    for r, b, n, buf in received:
+        out[("peer", A.SIDE_DST, r, b)] = buf
+        ex.bind(A.SIDE_DST, r, b, buf.ptr, n)
+    dist.barrier(group=group)
+    return out
+
+
+def setup_multicast(source, ex: Executor, rank: int, world: int, device: int, tag: str = "0", min_payload: int = 0,
+                    group=None):
     """Broadcast promotion over NVLS multicast for the executor's broadcast groups
     (Executor.bcast_groups): per group the root GPU creates a multicast object and passes
     it to the members (fdx); every member adds its device; after a barrier each binds its
     buffer (root: the source, members: the destination ranks' buffers, equal layouts);
     the root maps it and its executor stores the group once through the multicast address.
-    Collective over all ranks. Returns the objects to keep alive (close() before the
-    arena goes away); call ex.prepare() afterwards."""
+    `source` holds the buffers: an Arena (Arena.multi) or the dict of share_buffers().
+    Collective over `group`. Returns the objects to keep alive (close() them before the
+    buffers go away); call ex.prepare() afterwards."""
     import threading
 
     import torch.distributed as dist
 
-    from .api import Multicast, fdx_close, fdx_listen, fdx_recv, fdx_send
+    from .api import Arena, Multicast, fdx_close, fdx_listen, fdx_recv, fdx_send
+    arena = source if isinstance(source, Arena) else None
+    gran = 2 << 20
     groups = [g for g in ex.bcast_groups() if g.payload_bytes >= min_payload]
     mcs = {}
-    size = {g.id: arena.bind_size(0, g.root_rank, g.buf) for g in groups}
+    if arena is not None:
+        size = {g.id: arena.bind_size(0, g.root_rank, g.buf) for g in groups}
+    else:
+        size = {g.id: (g.buffer_bytes + gran - 1) // gran * gran for g in groups}
+
+    def bind(mc, side, r, b):
+        if arena is not None:
+            mc.bind_arena(arena, side, r, b)
+        else:
+            mc.bind_vmm(source[(side, r, b)])
+
     expect = sum(1 for g in groups if rank in list(g.member_gpu[: g.n_members]) and g.root_gpu != rank)
     sock = fdx_listen(f"reshard-mc-{tag}-{rank}")
-    dist.barrier()
+    dist.barrier(group=group)
     errors = []
 
     def receive():
@@ -279,16 +365,16 @@ def setup_multicast(arena, ex: Executor, rank: int, world: int, device: int, tag
         raise errors[0]
     for gid in sorted(mcs):
         mcs[gid].add_device(device)
-    dist.barrier()
+    dist.barrier(group=group)
     by_id = {g.id: g for g in groups}
     for gid in sorted(mcs):
         g = by_id[gid]
         if g.root_gpu == rank:
-            mcs[gid].bind_arena(arena, 0, g.root_rank, g.buf)
+            bind(mcs[gid], A.SIDE_SRC, g.root_rank, g.buf)
         for k in range(g.n_members):
             if g.member_gpu[k] == rank:
-                mcs[gid].bind_arena(arena, 1, g.member_rank[k], g.buf)
-    dist.barrier()
+                bind(mcs[gid], A.SIDE_DST, g.member_rank[k], g.buf)
+    dist.barrier(group=group)
     for gid in sorted(mcs):
         if by_id[gid].root_gpu == rank:
             ex.set_multicast(gid, mcs[gid].map(device))

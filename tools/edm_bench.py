@@ -24,7 +24,7 @@ from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.edm import ElasticDeviceManager, overlap_accounting  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env, setup_multicast, share_buffers  # noqa: E402
 
 
 def main():
@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--gemm", type=int, default=8192)
     ap.add_argument("--balance", action="store_true",
                     help="grow with balance_fanout (reference PlanOptions): joiners spread over the replicas")
+    ap.add_argument("--multicast", action="store_true",
+                    help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -59,6 +61,7 @@ def main():
     step_s = (time.perf_counter() - t0) / 5
 
     state = {}
+    nbuild = [0]
 
     def build_for(sc):
         def build(ctrl):
@@ -67,6 +70,21 @@ def main():
             edm.get_or_create_groups(sc.dst)
             plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
             t["plan_s"] = time.perf_counter() - t0
+            tr = Transition(plan, world, rank, local, alloc=False)
+            keep = []
+            if args.multicast:
+                # VMM state buffers shared by descriptor; the current state is the source
+                adopt = {(A.SIDE_SRC, k[1], k[2]): v for k, v in state.items()}
+                nbuild[0] += 1  # same sequence on every rank: a rank-independent socket tag
+                tag = f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{nbuild[0]}"
+                shared = share_buffers(tr, rank, world, local, tag=tag, group=ctrl, adopt=adopt)
+                t["alloc_s"] = time.perf_counter() - t0 - t["plan_s"]
+                mcs = setup_multicast(shared, tr.ex, rank, world, local, tag=tag, min_payload=1 << 20, group=ctrl)
+                t["multicast_groups"] = len(mcs)
+                keep = [shared, mcs]
+                tr.ex.prepare()
+                t["total_s"] = time.perf_counter() - t0
+                return tr, keep, t
             tr = Transition(plan, world, rank, local, alloc=False)
             keep = []
             for side in (A.SIDE_SRC, A.SIDE_DST):
@@ -97,6 +115,17 @@ def main():
 
     results = {}
     seed = 0xED
+
+    def release(keep, buffers=True):
+        """Multicast objects unbind before the buffers they bind go away."""
+        if not args.multicast or not keep:
+            return
+        for m in keep[1]:
+            m.close()
+        if buffers:
+            for k, v in keep[0].items():
+                if not (k[0] == A.SIDE_SRC and ("cur", k[1], k[2]) in state):
+                    v.close()
     # the DP8 state lives in its own buffers first
     first = RoutingPlan.from_scenario(shrink)
     ex0 = Transition(first, world, rank, local, alloc=False).ex
@@ -104,8 +133,13 @@ def main():
         for bb in range(6):
             _, n, g = ex0.buffer(A.SIDE_SRC, r, bb)
             if n and g == rank:
-                state[("cur", r, bb)] = torch.empty(n, dtype=torch.uint8, device="cuda")
-                ex0.bind(A.SIDE_SRC, r, bb, state[("cur", r, bb)].data_ptr(), n)
+                if args.multicast:
+                    from paper_2605_18815_b200.api import VmmBuffer
+                    state[("cur", r, bb)] = VmmBuffer.alloc(local, n)
+                    ex0.bind(A.SIDE_SRC, r, bb, state[("cur", r, bb)].ptr, n)
+                else:
+                    state[("cur", r, bb)] = torch.empty(n, dtype=torch.uint8, device="cuda")
+                    ex0.bind(A.SIDE_SRC, r, bb, state[("cur", r, bb)].data_ptr(), n)
     ex0.fill(A.SIDE_SRC, seed)
     del ex0
     for name, sc in (("shrink_dp8_to_dp4", shrink), ("grow_dp4_to_dp8", grow)):
@@ -140,6 +174,7 @@ def main():
                        bytes_moved=tr.plan.bytes_moved(), prepare_breakdown_rank0=tprep)
             out[mode] = acc
             if mode == "blocking":  # free the blocking run's new layout before the overlapped one
+                release(keep)
                 del tr, keep
                 torch.cuda.synchronize()
             else:
@@ -147,13 +182,23 @@ def main():
         # the new layout becomes the current state for the next event
         tr, keep = last
         state.clear()
-        for r in range(tr.plan.summary.dst_world):
-            for bb in range(6):
-                p, n, g = tr.ex.buffer(A.SIDE_DST, r, bb)
-                if n and g == rank:
-                    for t in keep:
-                        if t.data_ptr() == p:
-                            state[("cur", r, bb)] = t
+        if args.multicast:
+            for k, v in keep[0].items():
+                if k[0] == A.SIDE_DST:
+                    state[("cur", k[1], k[2])] = v
+            release(keep, buffers=False)
+            # the old layout (the adopted sources) is dead after the switch
+            for k, v in keep[0].items():
+                if k[0] != A.SIDE_DST:
+                    v.close()
+        else:
+            for r in range(tr.plan.summary.dst_world):
+                for bb in range(6):
+                    p, n, g = tr.ex.buffer(A.SIDE_DST, r, bb)
+                    if n and g == rank:
+                        for t in keep:
+                            if t.data_ptr() == p:
+                                state[("cur", r, bb)] = t
         results[name] = out
         # the old layout is gone after the switch: drop every reference to its buffers
         del tr, keep, last
@@ -161,7 +206,8 @@ def main():
         torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
-                          "n_gpus": world, "grow_balance_fanout": args.balance, "results": results}), flush=True)
+                          "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast,
+                          "results": results}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
