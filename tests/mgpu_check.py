@@ -21,6 +21,7 @@ from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
 def main():
     layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     staged = "--staged" in sys.argv
+    vmm = "--vmm" in sys.argv  # shareable VMM buffers mapped by descriptor instead of cudaIpc
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -33,7 +34,14 @@ def main():
         fwd = Transition(ab, world, rank, local, alloc=False)
         bwd = Transition(ba, world, rank, local, alloc=False)
         keep = []
-        for side_ab in (A.SIDE_SRC, A.SIDE_DST):
+        if vmm:
+            from paper_2605_18815_b200.runtime import share_buffers
+            tag = f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}"
+            keep.append(share_buffers(fwd, rank, world, local, tag=tag + "-f"))
+            keep.append(share_buffers(bwd, rank, world, local, tag=tag + "-b",
+                                      adopt={(1 - k[0], k[1], k[2]): v for k, v in keep[0].items()
+                                             if k[0] in (A.SIDE_SRC, A.SIDE_DST)}))
+        for side_ab in ((A.SIDE_SRC, A.SIDE_DST) if not vmm else ()):
             nr = ab.summary.src_world if side_ab == A.SIDE_SRC else ab.summary.dst_world
             for r in range(nr):
                 for b in range(6):
@@ -43,7 +51,11 @@ def main():
                         keep.append(t)
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
                         bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
-        if staged:
+        if vmm:
+            fwd.ex.prepare()
+            bwd.ex.prepare()
+            fwd_run, bwd_run = fwd.run, bwd.run
+        elif staged:
             from paper_2605_18815_b200.runtime import StagedTransition
             fwd_run = StagedTransition(ab, fwd.ex, world, rank).run
             bwd_run = StagedTransition(ba, bwd.ex, world, rank).run
@@ -63,7 +75,7 @@ def main():
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {'staged' if staged else 'fused'} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep

@@ -257,3 +257,19 @@ def test_broadcast_groups_need_two_remote_gpus():
     assert all(g.payload_bytes == g4[0].payload_bytes for g in g4)
     ex2 = Executor(plan, n_gpus=2, gpu=0, device=0)
     assert not [g for g in ex2.bcast_groups() if g.payload_bytes > 1 << 20]
+
+
+def test_multi_gpu_vmm_shared_buffers():
+    """N>1 with shareable VMM state buffers mapped by POSIX descriptor (share_buffers)
+    instead of cudaIpc; the way back adopts the forward's buffers. Skipped on one GPU."""
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29537",
+                        os.path.join(root, "tests", "mgpu_check.py"), "2", "--vmm"],
+                       capture_output=True, text=True, timeout=900)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
