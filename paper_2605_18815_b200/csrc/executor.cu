@@ -364,6 +364,8 @@ Executor::~Executor() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (mc_stream_) cudaStreamDestroy(mc_stream_);
+    for (size_t i = 1; i < ce_streams_.size(); ++i) cudaStreamDestroy(ce_streams_[i]);
+    for (cudaEvent_t e : ce_join_) cudaEventDestroy(e);
     for (cudaEvent_t e : mc_ev_)
         if (e) cudaEventDestroy(e);
 }
@@ -968,14 +970,35 @@ int Executor::run_fused(cudaStream_t stream) {
     // measured on B200 (profiles/r01_nvlink.md): with peer-bound tiles, one mixed launch
     // of the 16-B vector kernel keeps NVLink busiest (685 GB/s at N=2, 620 at N=4)
     if (!split_remote_) {
-        const int n = fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, remote_bulk_);
         if (!ce_ops_.empty()) {
-            for (const CeOp& c : ce_ops_)
+            // copy engines first (they start while the kernel launches), round-robin over
+            // RS_CE_STREAMS streams so several engines work at once
+            if (ce_streams_.empty()) {
+                const char* ks = std::getenv("RS_CE_STREAMS");
+                const int k = std::max(1, ks ? std::atoi(ks) : 2);
+                ce_streams_.push_back(aux_);
+                for (int i = 1; i < k; ++i) {
+                    cudaStream_t x;
+                    RS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+                    ce_streams_.push_back(x);
+                }
+                ce_join_.resize(ce_streams_.size());
+                for (auto& e : ce_join_) RS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            for (size_t i = 1; i < ce_streams_.size(); ++i) RS_CUDA(cudaStreamWaitEvent(ce_streams_[i], ev_fork_, 0));
+            for (size_t i = 0; i < ce_ops_.size(); ++i) {
+                const CeOp& c = ce_ops_[i];
                 RS_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(c.dst), reinterpret_cast<const void*>(c.src),
-                                        static_cast<size_t>(c.bytes), cudaMemcpyDeviceToDevice, aux_));
-            RS_CUDA(cudaEventRecord(ev_join_, aux_));
-            RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
+                                        static_cast<size_t>(c.bytes), cudaMemcpyDeviceToDevice,
+                                        ce_streams_[i % ce_streams_.size()]));
+            }
         }
+        const int n = fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, remote_bulk_);
+        if (!ce_ops_.empty())
+            for (size_t i = 0; i < ce_streams_.size(); ++i) {
+                RS_CUDA(cudaEventRecord(ce_join_[i], ce_streams_[i]));
+                RS_CUDA(cudaStreamWaitEvent(stream, ce_join_[i], 0));
+            }
         return n;
     }
     // NVLink-bound part (vector stores: full 16-B warps to peer HBM) on the caller's

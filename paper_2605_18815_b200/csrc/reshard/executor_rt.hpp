@@ -202,6 +202,8 @@ private:
         std::int64_t bytes;
     };
     std::vector<CeOp> ce_ops_;          // large contiguous peer-bound blocks for the copy engines
+    std::vector<cudaStream_t> ce_streams_;  // [0] = aux_
+    std::vector<cudaEvent_t> ce_join_;
     std::int64_t ce_min_bytes_ = 4 << 20;  // RS_CE_MIN_BYTES (0 disables)
     int remote_ctas_per_sm_ = 2;   // RS_REMOTE_CTAS_PER_SM
     std::vector<int> stage_of_dst_;
