@@ -251,13 +251,14 @@ typedef struct rs_arena rs_arena_t;
 typedef struct {
     int64_t physical_bytes, a_bytes, b_bytes, aliased_bytes, chunks;
     int64_t stage_groups[2]; /* concurrent stage groups (barriers) per direction */
+    int64_t bands;           /* layer bands per destination rank in the stage units */
 } rs_arena_stats_t;
 int rs_arena_create(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int device, int64_t cap_bytes,
                     int64_t chunk_bytes, int with_grads, rs_arena_t** out);
 void rs_arena_destroy(rs_arena_t* a);
 /* layout 0 = A (src of plan_ab), 1 = B (dst of plan_ab) */
 int rs_arena_buffer(const rs_arena_t* a, int layout, int rank, int buf, void** dptr, int64_t* bytes);
-/* destination-rank stage order of direction 0 (A->B) or 1 (B->A) */
+/* stage order of direction 0 (A->B) or 1 (B->A): units rank * bands + layer band */
 int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n);
 /* per position of that order: 1 = a barrier must precede it (positions between two cuts
  * share one stage and run concurrently); position 0 is always 1 */
@@ -272,14 +273,24 @@ int rs_memory_min_groups(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int
 /* the same for the buffers GPU `gpu` of n_gpus hosts, with the stage order coarsened
  * into `groups` concurrency groups (0 = one per stage) */
 int rs_memory_plan_ex(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads, int n_gpus,
-                      int gpu, int groups, rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba,
-                      int cap);
+                      int gpu, int groups, int bands, rs_arena_stats_t* stats, int64_t* violations, int* order_ab,
+                      int* order_ba, int cap);
+/* the schedule ladder (arena.hpp schedule_levels): the first level whose plan for `gpu`
+ * fits cap_bytes (*level = -1: none); rs_memory_schedule_level gives its (bands, groups) */
+int rs_memory_schedule(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                       int gpu, int64_t cap_bytes, int* level, int64_t* physical_bytes);
+int rs_memory_schedule_level(const rs_plan_t* plan_ab, int level, int* bands, int* groups);
+/* physical bytes GPU `gpu` needs at every level of the ladder (*n = number of levels):
+ * across GPUs, take the first level whose footprint fits on every rank */
+int rs_memory_schedule_footprints(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
+                                  int n_gpus, int gpu, int64_t* out, int cap, int* n);
 int rs_memory_plan(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                    rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap);
 /* multi-GPU arena: this process maps the buffers of the virtual ranks placed on GPU
  * `gpu` of `n_gpus` (shareable VMM); peers' buffers are imported from their export */
 int rs_arena_create_multi(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int n_gpus, int gpu, int device,
-                          int64_t cap_bytes, int64_t chunk_bytes, int with_grads, int groups, rs_arena_t** out);
+                          int64_t cap_bytes, int64_t chunk_bytes, int with_grads, int groups, int bands,
+                          rs_arena_t** out);
 /* POSIX-FD export of this GPU's physical allocations + mapping table (malloc'd; rs_free) */
 int rs_arena_export(const rs_arena_t* a, int** fds, int* n_fds, void** table, size_t* table_len);
 /* map a peer's buffers (consumes the descriptors) */

@@ -95,7 +95,8 @@ class ScheduleSummary_t(C.Structure):
 
 class ArenaStats_t(C.Structure):
     _fields_ = [("physical_bytes", C.c_int64), ("a_bytes", C.c_int64), ("b_bytes", C.c_int64),
-                ("aliased_bytes", C.c_int64), ("chunks", C.c_int64), ("stage_groups", C.c_int64 * 2)]
+                ("aliased_bytes", C.c_int64), ("chunks", C.c_int64), ("stage_groups", C.c_int64 * 2),
+                ("bands", C.c_int64)]
 
 
 _lib = None
@@ -203,8 +204,11 @@ def take_string(ptr: C.c_void_p, n: C.c_size_t) -> str:
 def _late_bindings(L):
     vp, i64, P = C.c_void_p, C.c_int64, C.POINTER
     for name, args in (
-        ("rs_arena_create_multi", [vp, vp, C.c_int, C.c_int, C.c_int, i64, i64, C.c_int, C.c_int, P(vp)]),
-        ("rs_memory_plan_ex", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int),
+        ("rs_arena_create_multi", [vp, vp, C.c_int, C.c_int, C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, P(vp)]),
+        ("rs_memory_schedule", [vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, P(C.c_int), P(i64)]),
+        ("rs_memory_schedule_level", [vp, C.c_int, P(C.c_int), P(C.c_int)]),
+        ("rs_memory_schedule_footprints", [vp, vp, i64, C.c_int, C.c_int, C.c_int, P(i64), C.c_int, P(C.c_int)]),
+        ("rs_memory_plan_ex", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int),
                                P(C.c_int), C.c_int]),
         ("rs_memory_min_groups", [vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, P(C.c_int), P(i64)]),
         ("rs_arena_export", [vp, P(P(C.c_int)), P(C.c_int), P(vp), P(C.c_size_t)]),

@@ -216,9 +216,9 @@ class Arena:
         return p.value or 0, n.value
 
     def stage_order(self, direction: int) -> List[int]:
-        out = (C.c_int * 1024)()
+        out = (C.c_int * 65536)()
         n = C.c_int()
-        A.check(A.lib().rs_arena_stage_order(self.h, direction, out, 1024, C.byref(n)))
+        A.check(A.lib().rs_arena_stage_order(self.h, direction, out, 65536, C.byref(n)))
         return list(out[: n.value])
 
     def stats(self) -> A.ArenaStats_t:
@@ -229,9 +229,9 @@ class Arena:
     def stage_cuts(self, direction: int) -> List[int]:
         """1 where a barrier must precede that stage position; the positions in between
         share one stage (run concurrently)."""
-        out = (C.c_int * 1024)()
+        out = (C.c_int * 65536)()
         n = C.c_int()
-        A.check(A.lib().rs_arena_stage_cuts(self.h, direction, out, 1024, C.byref(n)))
+        A.check(A.lib().rs_arena_stage_cuts(self.h, direction, out, 65536, C.byref(n)))
         return list(out[: n.value])
 
     def bind(self, fwd: "Executor", bwd: Optional["Executor"] = None, cuts=None) -> None:
@@ -356,13 +356,14 @@ _exec_staged_methods()
 
 
 def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False,
-                n_gpus: int = 1, gpu: int = 0, groups: int = 0):
+                n_gpus: int = 1, gpu: int = 0, groups: int = 0, bands: int = 1):
     """Host-only arena plan of the buffers `gpu` hosts: (stats, simulated violations,
-    stage orders); `groups` coarsens the stage order (0 = one group per stage)."""
+    stage orders over units rank * bands + band); `groups` coarsens the unit order
+    (0 = one group per unit), `bands` splits destination ranks into layer bands."""
     st, viol = A.ArenaStats_t(), C.c_int64()
-    oa, ob = (C.c_int * 1024)(), (C.c_int * 1024)()
+    oa, ob = (C.c_int * 65536)(), (C.c_int * 65536)()
     A.check(A.lib().rs_memory_plan_ex(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, groups,
-                                      C.byref(st), C.byref(viol), oa, ob, 1024))
+                                      bands, C.byref(st), C.byref(viol), oa, ob, 65536))
     return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
 
 
@@ -422,12 +423,39 @@ def memory_min_groups(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, g
     return g.value, phys.value
 
 
+def memory_schedule(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
+                    chunk_bytes: int = 0, with_grads: bool = False):
+    """(first schedule level that fits cap_bytes on `gpu` or -1, its physical bytes)."""
+    lv, phys = C.c_int(), C.c_int64()
+    A.check(A.lib().rs_memory_schedule(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, cap_bytes,
+                                       C.byref(lv), C.byref(phys)))
+    return lv.value, phys.value
+
+
+def memory_schedule_footprints(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int,
+                               chunk_bytes: int = 0, with_grads: bool = False) -> List[int]:
+    """Physical bytes `gpu` needs at every level of the schedule ladder."""
+    n = C.c_int()
+    out = (C.c_int64 * 4096)()
+    A.check(A.lib().rs_memory_schedule_footprints(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
+                                                  out, 4096, C.byref(n)))
+    return list(out[: n.value])
+
+
+def memory_schedule_level(ab: RoutingPlan, level: int):
+    """(bands, groups) of a schedule level."""
+    b, g = C.c_int(), C.c_int()
+    A.check(A.lib().rs_memory_schedule_level(ab.h, level, C.byref(b), C.byref(g)))
+    return b.value, g.value
+
+
 def _arena_multi(cls, ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, device: int,
-                 cap_bytes: int = 0, chunk_bytes: int = 0, with_grads: bool = False, groups: int = 0) -> "Arena":
+                 cap_bytes: int = 0, chunk_bytes: int = 0, with_grads: bool = False, groups: int = 0,
+                 bands: int = 1) -> "Arena":
     self = cls.__new__(cls)
     h = C.c_void_p()
     A.check(A.lib().rs_arena_create_multi(ab.h, ba.h if ba else None, n_gpus, gpu, device, cap_bytes, chunk_bytes,
-                                          int(with_grads), groups, C.byref(h)))
+                                          int(with_grads), groups, bands, C.byref(h)))
     self.h, self.ab, self.ba = h.value, ab, ba
     return self
 

@@ -834,7 +834,7 @@ int rs_arena_create(const rs_plan_t* ab, const rs_plan_t* ba, int device, int64_
 void rs_arena_destroy(rs_arena_t* a) { delete a; }
 
 int rs_arena_create_multi(const rs_plan_t* ab, const rs_plan_t* ba, int n_gpus, int gpu, int device, int64_t cap_bytes,
-                          int64_t chunk_bytes, int with_grads, int groups, rs_arena_t** out) {
+                          int64_t chunk_bytes, int with_grads, int groups, int bands, rs_arena_t** out) {
     return guarded([&] {
         *out = nullptr;
         int ndev = 0;
@@ -845,6 +845,7 @@ int rs_arena_create_multi(const rs_plan_t* ab, const rs_plan_t* ba, int n_gpus, 
         cfg.cap_bytes = cap_bytes;
         if (chunk_bytes > 0) cfg.chunk_bytes = chunk_bytes;
         cfg.groups = groups;
+        cfg.bands = bands;
         auto a = std::make_unique<rs_arena>();
         a->a = std::make_unique<mem::Arena>(ab->core, ba ? &ba->core : nullptr, cfg, with_grads != 0, n_gpus, gpu);
         *out = a.release();
@@ -955,12 +956,47 @@ int rs_memory_min_groups(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk
     });
 }
 
+int rs_memory_schedule(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                       int gpu, int64_t cap_bytes, int* level, int64_t* physical_bytes) {
+    return guarded([&] {
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad arena placement");
+        *level = mem::choose_schedule(ab->core, ba ? &ba->core : nullptr, chunk_bytes > 0 ? chunk_bytes : (32ll << 20),
+                                      with_grads != 0, n_gpus, gpu, cap_bytes, physical_bytes);
+        return RS_OK;
+    });
+}
+
+int rs_memory_schedule_footprints(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                                  int gpu, int64_t* out, int cap, int* n) {
+    return guarded([&] {
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad arena placement");
+        const std::vector<std::int64_t> f =
+            mem::schedule_footprints(ab->core, ba ? &ba->core : nullptr, chunk_bytes > 0 ? chunk_bytes : (32ll << 20),
+                                     with_grads != 0, n_gpus, gpu);
+        *n = static_cast<int>(f.size());
+        for (int i = 0; i < *n && i < cap; ++i) out[i] = f[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
+int rs_memory_schedule_level(const rs_plan_t* ab, int level, int* bands, int* groups) {
+    return guarded([&] {
+        const std::vector<mem::ScheduleLevel> L = mem::schedule_levels(ab->core);
+        if (level < 0 || level >= static_cast<int>(L.size())) throw ConfigError("schedule level out of range");
+        *bands = L[static_cast<size_t>(level)].bands;
+        *groups = L[static_cast<size_t>(level)].groups;
+        return RS_OK;
+    });
+}
+
 int rs_memory_plan_ex(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus, int gpu,
-                      int groups, rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap) {
+                      int groups, int bands, rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba,
+                      int cap) {
     return guarded([&] {
         const mem::MemoryPlan mp = mem::plan_memory(ab->core, ba ? &ba->core : nullptr,
                                                     chunk_bytes > 0 ? chunk_bytes : (32ll << 20), with_grads != 0,
-                                                    n_gpus, gpu, groups);
+                                                    n_gpus, gpu, groups, bands);
+        stats->bands = mp.bands;
         stats->physical_bytes = mp.stats.physical_bytes;
         stats->a_bytes = mp.stats.a_bytes;
         stats->b_bytes = mp.stats.b_bytes;
@@ -981,7 +1017,7 @@ int rs_memory_plan_ex(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_by
 
 int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, rs_arena_stats_t* stats,
                    int64_t* violations, int* order_ab, int* order_ba, int cap) {
-    return rs_memory_plan_ex(ab, ba, chunk_bytes, with_grads, 1, 0, 0, stats, violations, order_ab, order_ba, cap);
+    return rs_memory_plan_ex(ab, ba, chunk_bytes, with_grads, 1, 0, 0, 1, stats, violations, order_ab, order_ba, cap);
 }
 
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
@@ -991,6 +1027,7 @@ int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
         out->a_bytes = s.a_bytes;
         out->b_bytes = s.b_bytes;
         out->aliased_bytes = s.aliased_bytes;
+        out->bands = a->a->bands();
         out->chunks = s.chunks;
         for (int d = 0; d < 2; ++d) {
             out->stage_groups[d] = 0;

@@ -372,26 +372,42 @@ Executor::~Executor() {
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
 
-void Executor::set_stage_order(const std::vector<int>& dst_order, const std::vector<int>& cuts) {
+void Executor::set_stage_order(const std::vector<int>& order, const std::vector<int>& cuts) {
     const int nd = P_.dst_cfg.world_size();
-    if (dst_order.empty()) {
+    if (order.empty()) {
         stage_of_dst_.clear();
+        stage_bands_ = 1;
         return;
     }
-    if (static_cast<int>(dst_order.size()) != nd) throw ConfigError("stage order must list every destination rank once");
-    if (!cuts.empty() && cuts.size() != dst_order.size()) throw ConfigError("stage cuts must match the stage order");
-    std::vector<int> pos(static_cast<size_t>(nd), -1);
+    // units = (destination rank, layer band): order lists every unit once (arena.hpp UnitMap)
+    if (order.size() % static_cast<size_t>(nd)) throw ConfigError("stage order must list every unit once");
+    const int nb = static_cast<int>(order.size()) / nd;
+    if (!cuts.empty() && cuts.size() != order.size()) throw ConfigError("stage cuts must match the stage order");
+    std::vector<int> pos(order.size(), -1);
     int group = -1;
-    for (size_t s = 0; s < dst_order.size(); ++s) {
-        const int j = dst_order[s];
-        if (j < 0 || j >= nd || pos[static_cast<size_t>(j)] >= 0) throw ConfigError("bad stage order");
+    for (size_t s = 0; s < order.size(); ++s) {
+        const int u = order[s];
+        if (u < 0 || u >= static_cast<int>(order.size()) || pos[static_cast<size_t>(u)] >= 0)
+            throw ConfigError("bad stage order");
         // without cuts every position is its own stage; with cuts, positions between two
         // cuts share one stage (they may run concurrently)
         if (cuts.empty() || s == 0 || cuts[s]) ++group;
-        pos[static_cast<size_t>(j)] = group;
+        pos[static_cast<size_t>(u)] = group;
     }
     stage_of_dst_ = pos;
+    stage_bands_ = nb;
     prepared_ = false;
+}
+
+int Executor::stage_of(const CopyOp& op) const {
+    if (stage_of_dst_.empty()) return 0;
+    int band = 0;
+    if (stage_bands_ > 1 && op.tensor >= 0) {
+        const int L = std::max(1, P_.space->num_layers());
+        const int nb = std::min(stage_bands_, L);
+        band = P_.space->entries()[static_cast<size_t>(op.tensor)].spec.layer * nb / L;
+    }
+    return stage_of_dst_[static_cast<size_t>(op.dst_rank * stage_bands_ + band)];
 }
 
 void Executor::alloc() {
@@ -840,7 +856,7 @@ void Executor::prepare(bool staged) {
             throw ConfigError(strfmt("prepare: buffer not bound (src rank %d buf %d -> dst rank %d buf %d)",
                                      op.src_side_rank, op.src_buf, op.dst_rank, op.dst_buf));
         (dst_here ? stats_.local_bytes : stats_.remote_bytes) += total;
-        const int stage = stage_of_dst_.empty() ? 0 : stage_of_dst_[static_cast<size_t>(op.dst_rank)];
+        const int stage = stage_of(op);
         if (!dst_here) has_remote_ = true;
         const bool contiguous = op.rows == 1 || (op.src_pitch == op.row_bytes && op.dst_pitch == op.row_bytes);
         if (!dst_here && ce_min_bytes_ > 0 && contiguous && total >= ce_min_bytes_) {

@@ -1,5 +1,6 @@
-// Host side of the memory-aware arena (arena.hpp): stage orders, chunk lifetimes,
-// the aliasing assignment, and an independent execution simulation that checks it.
+// Host side of the memory-aware arena (arena.hpp): stage units and their order, chunk
+// lifetimes, the aliasing assignment, concurrency groups, and an independent execution
+// simulation that checks it.
 #include <algorithm>
 #include <limits>
 #include <map>
@@ -29,55 +30,148 @@ std::vector<int> positions(const std::vector<int>& order, size_t n) {
     return pos;
 }
 
+int gpu_block(const core::PlanCore& P, int n_gpus) {
+    int max_phys = 0;
+    for (const auto& r : P.routes) max_phys = std::max(max_phys, r.phys);
+    return (max_phys + 1 + n_gpus - 1) / n_gpus;
+}
+
 }  // namespace
 
-std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops) {
+UnitMap::UnitMap(const core::PlanCore& P, int bands) : nb(std::max(1, bands)), nd(P.dst_cfg.world_size()) {
+    const auto& ents = P.space->entries();
+    const int L = std::max(1, P.space->num_layers());
+    nb = std::min(nb, L);
+    band_of_tensor.resize(ents.size());
+    for (size_t t = 0; t < ents.size(); ++t) band_of_tensor[t] = ents[t].spec.layer * nb / L;
+}
+
+namespace {
+
+// One greedy pass over the units. peak_first: among the stages that keep their GPU under
+// the running peak, the one freeing the most old bytes on its own GPU, else the lowest
+// peak; otherwise: the stage freeing the most old bytes anywhere. Returns the order and
+// the modeled peak (max over GPUs of live bytes: old data still to be read + new data
+// written so far).
+std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops,
+                                                      int bands, int n_gpus, bool peak_first) {
+    const UnitMap U(P, bands);
     const int ns = P.src_cfg.world_size(), nd = P.dst_cfg.world_size();
-    std::vector<std::vector<char>> reads(static_cast<size_t>(ns), std::vector<char>(static_cast<size_t>(nd), 0));
-    for (const exec::CopyOp& op : ops) reads[static_cast<size_t>(op.src_side_rank)][static_cast<size_t>(op.dst_rank)] = 1;
-    std::vector<std::int64_t> sbytes(static_cast<size_t>(ns), 0);
-    for (int i = 0; i < ns; ++i) {
-        std::int64_t b[exec::kNumBufs];
-        exec::buffer_sizes(P, 0, i, false, b);
-        for (int k = 0; k < exec::kNumBufs; ++k) sbytes[static_cast<size_t>(i)] += b[k];
+    const int nsu = ns * U.nb, ndu = nd * U.nb;
+    const int per = gpu_block(P, std::max(1, n_gpus));
+    auto gpu_src = [&](int r) { return P.wm.src_phys[static_cast<size_t>(r)] / per; };
+    auto gpu_dst = [&](int r) { return P.wm.dst_phys[static_cast<size_t>(r)] / per; };
+    // bytes read from each source unit (what dies with it) and written into each
+    // destination unit (what its stage needs), and which source units each stage reads
+    std::vector<std::int64_t> w_src(static_cast<size_t>(nsu), 0), w_dst(static_cast<size_t>(ndu), 0);
+    std::vector<std::vector<int>> reads(static_cast<size_t>(ndu));
+    for (const exec::CopyOp& op : ops) {
+        if (op.tensor < 0) continue;  // the scalar blob (a plain allocation) never frees memory
+        const int su = U.unit(op.src_side_rank, op.tensor), du = U.unit(op.dst_rank, op.tensor);
+        const std::int64_t b = op.rows * op.row_bytes;
+        w_src[static_cast<size_t>(su)] += b;
+        w_dst[static_cast<size_t>(du)] += b;
+        reads[static_cast<size_t>(du)].push_back(su);
     }
-    std::vector<char> done(static_cast<size_t>(nd), 0), dead(static_cast<size_t>(ns), 0);
-    auto all_consumers_done = [&](int i, int extra) {
-        for (int d = 0; d < nd; ++d)
-            if (reads[static_cast<size_t>(i)][static_cast<size_t>(d)] && !done[static_cast<size_t>(d)] && d != extra) return false;
-        return true;
-    };
+    std::vector<int> remaining(static_cast<size_t>(nsu), 0);
+    for (auto& v : reads) {
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        for (int su : v) ++remaining[static_cast<size_t>(su)];
+    }
+    // per-GPU live bytes (ties: lower unit index, so every rank derives the same order)
+    const int G = std::max(1, n_gpus);
+    std::vector<std::int64_t> live(static_cast<size_t>(G), 0);
+    for (int su = 0; su < nsu; ++su)
+        if (remaining[static_cast<size_t>(su)]) live[static_cast<size_t>(gpu_src(su / U.nb))] += w_src[static_cast<size_t>(su)];
+    std::int64_t peak = *std::max_element(live.begin(), live.end());
+    std::vector<char> done(static_cast<size_t>(ndu), 0);
     std::vector<int> order;
-    for (int step = 0; step < nd; ++step) {
+    order.reserve(static_cast<size_t>(ndu));
+    for (int step = 0; step < ndu; ++step) {
         int best = -1;
-        std::int64_t best_freed = -1;
-        for (int j = 0; j < nd; ++j) {
-            if (done[static_cast<size_t>(j)]) continue;
+        bool best_under = false;
+        std::int64_t best_freed = -1, best_peak = 0;
+        for (int du = 0; du < ndu; ++du) {
+            if (done[static_cast<size_t>(du)]) continue;
+            const int g = gpu_dst(du / U.nb);
+            const std::int64_t during = live[static_cast<size_t>(g)] + w_dst[static_cast<size_t>(du)];
             std::int64_t freed = 0;
-            for (int i = 0; i < ns; ++i)
-                if (!dead[static_cast<size_t>(i)] && all_consumers_done(i, j)) freed += sbytes[static_cast<size_t>(i)];
-            if (freed > best_freed) best = j, best_freed = freed;
+            for (int su : reads[static_cast<size_t>(du)])
+                if (remaining[static_cast<size_t>(su)] == 1 && gpu_src(su / U.nb) == g) freed += w_src[static_cast<size_t>(su)];
+            if (!peak_first) {
+                freed = 0;
+                for (int su : reads[static_cast<size_t>(du)])
+                    if (remaining[static_cast<size_t>(su)] == 1) freed += w_src[static_cast<size_t>(su)];
+            }
+            const bool under = during <= peak;
+            bool take;
+            if (best < 0) take = true;
+            else if (!peak_first) take = freed > best_freed;
+            else if (under != best_under) take = under;
+            else if (under) take = freed > best_freed;
+            else take = during < best_peak || (during == best_peak && freed > best_freed);
+            if (take) best = du, best_under = under, best_freed = freed, best_peak = during;
         }
         done[static_cast<size_t>(best)] = 1;
         order.push_back(best);
-        for (int i = 0; i < ns; ++i)
-            if (all_consumers_done(i, -1)) dead[static_cast<size_t>(i)] = 1;
+        const int g = gpu_dst(best / U.nb);
+        live[static_cast<size_t>(g)] += w_dst[static_cast<size_t>(best)];
+        peak = std::max(peak, live[static_cast<size_t>(g)]);
+        for (int su : reads[static_cast<size_t>(best)])
+            if (--remaining[static_cast<size_t>(su)] == 0) live[static_cast<size_t>(gpu_src(su / U.nb))] -= w_src[static_cast<size_t>(su)];
     }
-    return order;
+    return {order, peak};
 }
 
+}  // namespace
+
+std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops, int bands,
+                                    int n_gpus) {
+    // both heuristics, keep the lower modeled peak (a global criterion: every rank picks
+    // the same order)
+    auto a = greedy_pass(P, ops, bands, n_gpus, false);
+    auto b = greedy_pass(P, ops, bands, n_gpus, true);
+    return b.second < a.second ? b.first : a.first;
+}
+
+namespace {
+MemoryPlan plan_with_order(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
+                           const std::vector<exec::CopyOp>& ops_ba, std::int64_t C, bool with_grads, int n_gpus, int gpu,
+                           int groups, int bands, const std::vector<int>& order_ab);
+}  // namespace
+
 MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t C, bool with_grads, int n_gpus,
-                       int gpu, int groups) {
+                       int gpu, int groups, int bands) {
+    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
+    const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
+    return plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands);
+}
+
+MemoryPlan plan_memory_ops(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
+                           const std::vector<exec::CopyOp>& ops_ba, std::int64_t C, bool with_grads, int n_gpus, int gpu,
+                           int groups, int bands) {
+    if (n_gpus > 1)  // the order must be global: the modeled-peak choice
+        return plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
+                               greedy_stage_order(ab, ops_ab, bands, n_gpus));
+    // one GPU: both greedy orders, keep the smaller footprint
+    MemoryPlan a = plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
+                                   greedy_pass(ab, ops_ab, bands, n_gpus, false).first);
+    MemoryPlan b = plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
+                                   greedy_pass(ab, ops_ab, bands, n_gpus, true).first);
+    return b.stats.physical_bytes < a.stats.physical_bytes ? b : a;
+}
+
+namespace {
+MemoryPlan plan_with_order(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
+                           const std::vector<exec::CopyOp>& ops_ba, std::int64_t C, bool with_grads, int n_gpus, int gpu,
+                           int groups, int bands, const std::vector<int>& order_ab) {
     MemoryPlan mp;
     mp.chunk = C;
-    // stage position -> concurrency group (MemoryAwareChunk: as many
-    // steps per stage as memory allows); lifetimes are measured in groups, so a chunk is
-    // reused only by a LATER group
-    auto group_of = [groups](int s, int n) { return groups <= 0 || groups >= n ? s : s * groups / n; };
+    const UnitMap Uab(ab, bands);
+    mp.bands = Uab.nb;
     // contiguous-block placement of the plan's devices (executor.cu gpu_of_phys)
-    int max_phys = 0;
-    for (const auto& r : ab.routes) max_phys = std::max(max_phys, r.phys);
-    const int per = (max_phys + 1 + n_gpus - 1) / n_gpus;
+    const int per = gpu_block(ab, n_gpus);
     for (int l = 0; l < 2; ++l) {
         const int nr = l == 0 ? ab.src_cfg.world_size() : ab.dst_cfg.world_size();
         mp.bufs[l].resize(static_cast<size_t>(nr) * exec::kNumBufs);
@@ -95,10 +189,14 @@ MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::
             }
         }
     }
-    // ---- lifetimes: last read (A) / first write (B) stage of every chunk
-    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
-    mp.order[0] = greedy_stage_order(ab, ops_ab);
-    const std::vector<int> pos_ab = positions(mp.order[0], static_cast<size_t>(ab.dst_cfg.world_size()));
+    // ---- stage units (destination rank x layer band) and their order; concurrency
+    // groups: position -> group (MemoryAwareChunk: as many steps per
+    // stage as memory allows). Lifetimes are measured in groups, so a chunk is reused
+    // only by a LATER group.
+    auto group_of = [groups](int s, int n) { return groups <= 0 || groups >= n ? s : s * groups / n; };
+    mp.order[0] = order_ab;
+    const int nu_ab = Uab.count();
+    const std::vector<int> pos_ab = positions(mp.order[0], static_cast<size_t>(nu_ab));
     auto chunk_vec = [&](int l, int init) {
         std::vector<std::vector<int>> v(mp.bufs[l].size());
         for (size_t i = 0; i < mp.bufs[l].size(); ++i) v[i].assign(mp.bufs[l][i].phys.size(), init);
@@ -111,30 +209,34 @@ MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::
             x = is_max ? std::max(x, stage) : std::min(x, stage);
         }
     };
+    // last read (A) / first write (B) group of every chunk
     std::vector<std::vector<int>> lr_ab = chunk_vec(0, -1), fw_ab = chunk_vec(1, kNever);
     for (const exec::CopyOp& op : ops_ab) {
-        const int s = group_of(pos_ab[static_cast<size_t>(op.dst_rank)], ab.dst_cfg.world_size());
+        const int s = group_of(pos_ab[static_cast<size_t>(Uab.unit(op.dst_rank, op.tensor))], nu_ab);
         touch(lr_ab, op.src_side_rank, op.src_buf, src_extent(op), s, true);
         touch(fw_ab, op.dst_rank, op.dst_buf, dst_extent(op), s, false);
     }
     std::vector<std::vector<int>> lr_ba = chunk_vec(1, -1), fw_ba = chunk_vec(0, kNever);
     if (ba) {
-        // B->A writes A ranks; A ranks that die last in A->B are rebuilt first
-        const int na = ab.src_cfg.world_size();
-        std::vector<int> death(static_cast<size_t>(na), -1);
-        for (int r = 0; r < na; ++r)
-            for (int k = 0; k < exec::kNumBufs; ++k)
-                for (int x : lr_ab[static_cast<size_t>(r) * exec::kNumBufs + k])
-                    death[static_cast<size_t>(r)] = std::max(death[static_cast<size_t>(r)], x);
-        mp.order[1].resize(static_cast<size_t>(na));
-        for (int r = 0; r < na; ++r) mp.order[1][static_cast<size_t>(r)] = r;
+        // B->A writes A units; the A units that die last in A->B are rebuilt first
+        const UnitMap Uba(*ba, Uab.nb);
+        std::vector<int> death(static_cast<size_t>(Uba.count()), -1);
+        for (const exec::CopyOp& op : ops_ab) {
+            if (op.tensor < 0) continue;  // the scalar blob is not chunked memory
+            const int u = Uba.unit(op.src_side_rank, op.tensor);
+            death[static_cast<size_t>(u)] =
+                std::max(death[static_cast<size_t>(u)], pos_ab[static_cast<size_t>(Uab.unit(op.dst_rank, op.tensor))]);
+        }
+        mp.order[1].resize(static_cast<size_t>(Uba.count()));
+        for (int u = 0; u < Uba.count(); ++u) mp.order[1][static_cast<size_t>(u)] = u;
         std::sort(mp.order[1].begin(), mp.order[1].end(), [&](int a, int b) {
             const int da = death[static_cast<size_t>(a)], db = death[static_cast<size_t>(b)];
             return da != db ? da > db : a > b;
         });
-        const std::vector<int> pos_ba = positions(mp.order[1], static_cast<size_t>(na));
-        for (const exec::CopyOp& op : exec::build_ops(*ba)) {
-            const int s = group_of(pos_ba[static_cast<size_t>(op.dst_rank)], na);
+        const int nu_ba = Uba.count();
+        const std::vector<int> pos_ba = positions(mp.order[1], static_cast<size_t>(nu_ba));
+        for (const exec::CopyOp& op : ops_ba) {
+            const int s = group_of(pos_ba[static_cast<size_t>(Uba.unit(op.dst_rank, op.tensor))], nu_ba);
             touch(lr_ba, op.src_side_rank, op.src_buf, src_extent(op), s, true);
             touch(fw_ba, op.dst_rank, op.dst_buf, dst_extent(op), s, false);
         }
@@ -191,26 +293,102 @@ MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::
     mp.stats.physical_bytes = static_cast<std::int64_t>(mp.nphys) * C;
     for (const BufPlan& m : mp.bufs[1])
         if (!m.remote) mp.stats.b_bytes += m.bytes;
-    plan_stage_cuts(mp, ab, ba);
+    plan_stage_cuts(mp, ab, ba, ops_ab, ops_ba);
     return mp;
+}
+}  // namespace
+
+std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab) {
+    std::vector<ScheduleLevel> v;
+    const int nd = ab.dst_cfg.world_size();
+    const int L = std::max(1, ab.space->num_layers());
+    for (int nb = 1;; nb *= 2) {
+        const int n = std::min(nb, L);
+        const int units = nd * n;
+        // group counts 1, 2, 4, ... and finally one group per unit: each count refines the
+        // previous one (nested boundaries), so within a band count more groups never alias less
+        std::vector<int> ks;
+        for (int k = 1; k < units; k *= 2) ks.push_back(k);
+        ks.push_back(units);
+        for (int k : ks)
+            if (!(n > 1 && k == 1)) v.push_back({n, k});  // one group is the same at any band count
+        if (n >= L) break;
+    }
+    return v;
+}
+
+int choose_schedule(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t C, bool with_grads, int n_gpus,
+                    int gpu, std::int64_t cap, std::int64_t* physical) {
+    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
+    const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
+    const std::vector<ScheduleLevel> levels = schedule_levels(ab);
+    std::int64_t best = std::numeric_limits<std::int64_t>::max();
+    for (size_t i = 0; i < levels.size();) {
+        // a band count whose most-aliased plan does not fit is skipped whole: its other
+        // levels alias less
+        size_t last = i;
+        while (last + 1 < levels.size() && levels[last + 1].bands == levels[i].bands) ++last;
+        const MemoryPlan most =
+            plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, levels[last].groups, levels[last].bands);
+        best = std::min(best, most.stats.physical_bytes);
+        if (most.stats.physical_bytes <= cap)
+            for (size_t j = i; j <= last; ++j) {
+                const std::int64_t phys =
+                    j == last ? most.stats.physical_bytes
+                              : plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, levels[j].groups,
+                                                levels[j].bands)
+                                    .stats.physical_bytes;
+                if (phys <= cap) {
+                    if (physical) *physical = phys;
+                    return static_cast<int>(j);
+                }
+            }
+        i = last + 1;
+    }
+    if (physical) *physical = best;
+    return -1;
+}
+
+std::vector<std::int64_t> schedule_footprints(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t C,
+                                              bool with_grads, int n_gpus, int gpu) {
+    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
+    const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
+    std::vector<std::int64_t> out;
+    for (const ScheduleLevel& L : schedule_levels(ab))
+        out.push_back(plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, L.groups, L.bands).stats.physical_bytes);
+    return out;
+}
+
+int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t C, bool with_grads, int n_gpus,
+                     int gpu, std::int64_t cap, std::int64_t* physical) {
+    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
+    const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
+    const int n = std::max(ab.dst_cfg.world_size(), ba ? ba->dst_cfg.world_size() : 0);
+    for (int k = 1; k <= n; ++k) {
+        const MemoryPlan mp = plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, k, 1);
+        if (physical) *physical = mp.stats.physical_bytes;
+        if (mp.stats.physical_bytes <= cap) return k;
+    }
+    return -1;
 }
 
 namespace {
 
 // per stage position of one direction: physical chunks read, and (chunk, new owner) written
 struct StageIo {
-    std::vector<int> reads;
+    std::vector<int> reads;  // (chunk, expected owner buffer, expected owner chunk) triples
     std::vector<std::pair<int, Owner>> writes;
 };
 
-std::vector<StageIo> stage_io(const MemoryPlan& mp, const core::PlanCore& P, const std::vector<int>& order, int src_layout) {
+std::vector<StageIo> stage_io(const MemoryPlan& mp, const core::PlanCore& P, const std::vector<exec::CopyOp>& ops,
+                              const std::vector<int>& order, int src_layout) {
     const std::int64_t C = mp.chunk;
-    const std::vector<exec::CopyOp> ops = exec::build_ops(P);
-    const std::vector<int> pos = positions(order, static_cast<size_t>(P.dst_cfg.world_size()));
+    const UnitMap U(P, mp.bands);
+    const std::vector<int> pos = positions(order, static_cast<size_t>(U.count()));
     const int dst_layout = 1 - src_layout;
     std::vector<StageIo> io(order.size());
     for (const exec::CopyOp& op : ops) {
-        StageIo& st = io[static_cast<size_t>(pos[static_cast<size_t>(op.dst_rank)])];
+        StageIo& st = io[static_cast<size_t>(pos[static_cast<size_t>(U.unit(op.dst_rank, op.tensor))])];
         const size_t sb = static_cast<size_t>(op.src_side_rank) * exec::kNumBufs + op.src_buf;
         const size_t db = static_cast<size_t>(op.dst_rank) * exec::kNumBufs + op.dst_buf;
         const BufPlan& S = mp.bufs[src_layout][sb];
@@ -219,7 +397,7 @@ std::vector<StageIo> stage_io(const MemoryPlan& mp, const core::PlanCore& P, con
             const Extent e = src_extent(op);
             for (std::int64_t c = e.lo / C; c <= (e.hi - 1) / C; ++c) {
                 st.reads.push_back(S.phys[static_cast<size_t>(c)]);
-                st.reads.push_back(static_cast<int>(sb));  // (chunk, expected owner) pairs
+                st.reads.push_back(static_cast<int>(sb));
                 st.reads.push_back(static_cast<int>(c));
             }
         }
@@ -234,12 +412,13 @@ std::vector<StageIo> stage_io(const MemoryPlan& mp, const core::PlanCore& P, con
 
 }  // namespace
 
-void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba) {
+void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,
+                     const std::vector<exec::CopyOp>& ops_ab, const std::vector<exec::CopyOp>& ops_ba) {
     // greedy maximal groups of consecutive stages: a stage joins the running group unless
     // it writes a physical chunk that an earlier stage of the group reads (the aliased
     // old data would be clobbered while still being copied)
     for (int d = 0; d < (ba ? 2 : 1); ++d) {
-        const std::vector<StageIo> io = stage_io(mp, d == 0 ? ab : *ba, mp.order[d], d);
+        const std::vector<StageIo> io = stage_io(mp, d == 0 ? ab : *ba, d == 0 ? ops_ab : ops_ba, mp.order[d], d);
         mp.cut[d].assign(io.size(), 0);
         std::vector<char> read_in_group(static_cast<size_t>(mp.nphys), 0);
         std::vector<int> touched;
@@ -260,17 +439,6 @@ void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanC
     }
 }
 
-int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t C, bool with_grads, int n_gpus,
-                     int gpu, std::int64_t cap, std::int64_t* physical) {
-    const int n = std::max(ab.dst_cfg.world_size(), ba ? ba->dst_cfg.world_size() : 0);
-    for (int k = 1; k <= n; ++k) {
-        const MemoryPlan mp = plan_memory(ab, ba, C, with_grads, n_gpus, gpu, k);
-        if (physical) *physical = mp.stats.physical_bytes;
-        if (mp.stats.physical_bytes <= cap) return k;
-    }
-    return -1;
-}
-
 std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba) {
     // owner[p] = (layout, buffer index, chunk index) whose data physical chunk p holds;
     // stages between two cuts run concurrently (one group), groups run in order
@@ -279,12 +447,13 @@ std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab
         for (size_t c = 0; c < mp.bufs[0][i].phys.size(); ++c) owner[static_cast<size_t>(mp.bufs[0][i].phys[c])] = {0, i, c};
     std::int64_t violations = 0;
     for (int d = 0; d < (ba ? 2 : 1); ++d) {
-        const std::vector<StageIo> io = stage_io(mp, d == 0 ? ab : *ba, mp.order[d], d);
+        const core::PlanCore& P = d == 0 ? ab : *ba;
+        const std::vector<StageIo> io = stage_io(mp, P, exec::build_ops(P), mp.order[d], d);
         const int src_layout = d;
         size_t s = 0;
         while (s < io.size()) {
             size_t e = s + 1;
-            while (e < io.size() && !(d < 2 && e < mp.cut[d].size() && mp.cut[d][e])) ++e;
+            while (e < io.size() && !(e < mp.cut[d].size() && mp.cut[d][e])) ++e;
             std::vector<char> read_now(static_cast<size_t>(mp.nphys), 0);
             for (size_t t = s; t < e; ++t)
                 for (size_t k = 0; k < io[t].reads.size(); k += 3) {

@@ -61,6 +61,13 @@ struct Emitter {
         const LBox Bs = lift_seg(ts, S.blo, S.bhi), Bd = lift_seg(ts, D.blo, D.bhi);
         const std::int64_t es = elem_in(Bs, p, r0, c0), ed = elem_in(Bd, p, r0, c0);
         const std::int64_t rows = r1 - r0, w = c1 - c0;
+        const size_t first = out.size();
+        emit(kind, ts, S, D, Bs, Bd, k, j, es, ed, rows, w);
+        for (size_t i = first; i < out.size(); ++i) out[i].tensor = t;
+    }
+
+    void emit(int kind, const TensorSpec& ts, const Seg& S, const Seg& D, const LBox& Bs, const LBox& Bd, int k, int j,
+              std::int64_t es, std::int64_t ed, std::int64_t rows, std::int64_t w) {
         if (kind == 0) {
             const int dt = ts.dtype_bytes;
             out.push_back(CopyOp{k, kParam, j, kParam, S.param_byte_off + es * dt, D.param_byte_off + ed * dt, rows, w * dt,

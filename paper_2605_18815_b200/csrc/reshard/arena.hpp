@@ -29,7 +29,8 @@ struct ArenaConfig {
     int device = 0;
     std::int64_t cap_bytes = 0;             // physical budget; 0 -> free memory minus 1 GiB
     std::int64_t chunk_bytes = 32ll << 20;  // physical chunk (multiple of the VMM granularity)
-    int groups = 0;  // concurrency groups of the stage order; 0 -> fewest that fit the cap
+    int groups = 0;  // concurrency groups of the stage order; 0 -> the cheapest schedule level that fits the cap
+    int bands = 1;   // layer bands per destination rank (with groups > 0)
 };
 
 struct ArenaStats {
@@ -39,8 +40,23 @@ struct ArenaStats {
     std::int64_t chunks = 0;
 };
 
-/// Stage order of a direction: destination ranks, greedy so sources die early.
-std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops);
+/// Stage units: (destination rank, layer band), band(t) = layer(t) * bands / num_layers.
+/// With bands = 1 a unit is a whole destination rank; finer bands let a GPU rebuild its
+/// new layout band by band in the memory its old layout frees (PP-interleaved order,
+/// PAPER.md:782-802; config 5 on 8 GPUs needs it).
+struct UnitMap {
+    int nb = 1, nd = 0;
+    std::vector<int> band_of_tensor;
+    UnitMap(const core::PlanCore& P, int bands);
+    int unit(int rank, int tensor) const { return rank * nb + (tensor < 0 ? 0 : band_of_tensor[static_cast<size_t>(tensor)]); }
+    int count() const { return nd * nb; }
+};
+
+/// Stage order of a direction over units: greedy on the per-GPU live bytes (old data
+/// still to be read + new data written), keeping every GPU under the running peak and
+/// freeing the most old bytes first. Deterministic: every rank derives the same order.
+std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops, int bands = 1,
+                                    int n_gpus = 1);
 
 /// Host-side memory plan (no driver calls; CPU-testable).
 struct BufPlan {
@@ -51,28 +67,48 @@ struct BufPlan {
 };
 struct MemoryPlan {
     std::int64_t chunk = 0;
+    int bands = 1;
     std::vector<BufPlan> bufs[2];  // [layout][rank * kNumBufs + buf]
-    std::vector<int> order[2];     // stage orders (dst ranks) A->B, B->A
+    std::vector<int> order[2];     // stage orders (units) A->B, B->A
     std::vector<int> cut[2];       // per stage position: 1 = a barrier precedes it
     int nphys = 0;
     ArenaStats stats;
 };
 /// Plan the buffers hosted by `gpu` (contiguous-block placement over n_gpus). Stage
-/// orders are global, so with n_gpus > 1 every stage boundary is a cross-GPU barrier.
-/// `groups` (0 = one per stage) coarsens the stage order into that many concurrency
-/// groups: fewer barriers, less aliasing.
+/// orders are global, so with n_gpus > 1 every group boundary is a cross-GPU barrier.
+/// `groups` (0 = one per unit) coarsens the unit order into that many concurrency
+/// groups: fewer barriers, less aliasing. `bands` splits every destination rank into
+/// layer bands.
 MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads,
-                       int n_gpus = 1, int gpu = 0, int groups = 0);
-/// fewest groups whose plan fits `cap` bytes on `gpu` (-1: none does); the physical
-/// bytes of the last plan tried in *physical
+                       int n_gpus = 1, int gpu = 0, int groups = 0, int bands = 1);
+MemoryPlan plan_memory_ops(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
+                           const std::vector<exec::CopyOp>& ops_ba, std::int64_t chunk, bool with_grads, int n_gpus,
+                           int gpu, int groups, int bands);
+/// fewest groups (bands = 1) whose plan fits `cap` bytes on `gpu` (-1: none does); the
+/// physical bytes of the last plan tried in *physical
 int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads, int n_gpus,
                      int gpu, std::int64_t cap, std::int64_t* physical);
+/// The schedule ladder, cheapest first: for bands 1, 2, 4, ... (up to the layer count)
+/// group counts from one (no aliasing) to one per unit (most aliasing).
+struct ScheduleLevel {
+    int bands, groups;
+};
+std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab);
+/// first level of the ladder whose plan fits `cap` on `gpu` (-1: none; *physical = the
+/// smallest footprint seen). One GPU; across GPUs use schedule_footprints.
+int choose_schedule(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads, int n_gpus,
+                    int gpu, std::int64_t cap, std::int64_t* physical);
+/// physical bytes `gpu` needs at every level of the ladder (multi-GPU agreement: every
+/// rank marks its feasible levels, the group takes the first level feasible everywhere)
+std::vector<std::int64_t> schedule_footprints(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk,
+                                              bool with_grads, int n_gpus, int gpu);
 /// Group consecutive stages that may run concurrently (fills mp.cut): a barrier only
 /// where a stage overwrites a chunk an earlier stage of the running group still reads.
-void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba);
+void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,
+                     const std::vector<exec::CopyOp>& ops_ab, const std::vector<exec::CopyOp>& ops_ba);
 /// Replays the staged execution chunk by chunk (A->B, then B->A) tracking which
 /// logical chunk each physical chunk holds; counts reads of clobbered data and
-/// same-stage read/write races. 0 == the aliasing is safe.
+/// same-group read/write races. 0 == the aliasing is safe.
 std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba);
 
 class Arena {
@@ -90,6 +126,7 @@ public:
     std::int64_t bytes(int layout, int rank, int buf) const;
     const std::vector<int>& stage_order(int dir) const { return order_[dir]; }
     const std::vector<int>& stage_cuts(int dir) const { return cut_[dir]; }
+    int bands() const { return bands_; }
     const ArenaStats& stats() const { return stats_; }
 
     /// POSIX-FD export of every physical allocation backing this GPU's buffers, with a
@@ -116,6 +153,7 @@ private:
     std::vector<std::uint64_t> imported_;          // peers' physical allocations
     std::vector<std::pair<std::uint64_t, std::int64_t>> peer_maps_;  // (va, reserved) to unmap
     std::vector<int> order_[2], cut_[2];
+    int bands_ = 1;
     ArenaConfig cfg_;
     ArenaStats stats_;
     int nranks_[2] = {0, 0};

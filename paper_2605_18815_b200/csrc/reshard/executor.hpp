@@ -22,6 +22,7 @@ struct CopyOp {
     int src_side_rank, src_buf;  // src virtual rank, buffer
     int dst_rank, dst_buf;       // dst virtual rank, buffer
     std::int64_t src_off, dst_off, rows, row_bytes, src_pitch, dst_pitch;
+    int tensor = -1;             // model tensor the bytes belong to (-1: scalar blob)
 };
 
 /// Device tile: <= kTileBytes of one CopyOp, absolute pointers.

@@ -206,7 +206,9 @@ private:
     std::vector<cudaEvent_t> ce_join_;
     std::int64_t ce_min_bytes_ = 4 << 20;  // RS_CE_MIN_BYTES (0 disables)
     int remote_ctas_per_sm_ = 2;   // RS_REMOTE_CTAS_PER_SM
-    std::vector<int> stage_of_dst_;
+    std::vector<int> stage_of_dst_;  // stage of each unit (dst rank x layer band)
+    int stage_bands_ = 1;
+    int stage_of(const CopyOp& op) const;
     void* d_fill_ = nullptr;
     void* d_counters_ = nullptr;
     bool prepared_ = false;

@@ -208,23 +208,27 @@ def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
 def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: int, device: int, cap_bytes: int = 0,
                  tag: str = "0", chunk_bytes: int = 0):
     """Memory-aware arena over `world` GPUs: every GPU plans the buffers it hosts with the
-    same stage grouping (the fewest groups that fit every GPU's cap: max over ranks),
+    same schedule level (layer bands x concurrency groups: the cheapest level that fits
+    every GPU's cap, max over ranks),
     then the buffers are shared (exchange_arena). Returns (arena, global stage cuts)."""
     import torch
     import torch.distributed as dist
 
-    from .api import Arena, memory_min_groups
+    from .api import Arena, memory_schedule_footprints, memory_schedule_level
     if cap_bytes <= 0:
         cap_bytes = torch.cuda.mem_get_info(device)[0] - (1 << 30)
-    k, need = memory_min_groups(ab, ba, world, rank, cap_bytes, chunk_bytes)
+    # every rank marks the ladder levels that fit its cap; the first level feasible on all
+    need = memory_schedule_footprints(ab, ba, world, rank, chunk_bytes)
+    ok = torch.tensor([1 if x <= cap_bytes else 0 for x in need], dtype=torch.int32, device="cuda")
     if world > 1:
-        t = torch.tensor([k if k > 0 else 1 << 20], dtype=torch.int64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        k = int(t.item())
-    if k <= 0 or k >= 1 << 20:
-        raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs {need / 1e9:.2f} GB, "
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    fits = [i for i, v in enumerate(ok.tolist()) if v]
+    if not fits:
+        raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs >= {min(need) / 1e9:.2f} GB, "
                                               f"cap {cap_bytes / 1e9:.2f} GB)")
-    arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k)
+    lv = fits[0]
+    bands, k = memory_schedule_level(ab, lv)
+    arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k, bands=bands)
     exchange_arena(arena, rank, world, tag)
     return arena, global_stage_cuts(arena, world)
 

@@ -17,7 +17,8 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env, exchange_arena, global_stage_cuts, run_stages  # noqa: E402
+from paper_2605_18815_b200.runtime import (Transition, dist_env, exchange_arena, global_stage_cuts, run_stages,  # noqa: E402
+                                           shared_arena)
 
 
 def main():
@@ -28,14 +29,26 @@ def main():
     seed = 0xA7E4
     fails = 0
     # groups 0: one group per stage (most aliasing); 2: the stage order in two halves
-    for sc, groups in ((S.config2(layers), 0), (S.config2(layers), 2), (S.config3(2)[0], 0)):
-        ab = RoutingPlan.from_scenario(sc)
+    # groups < 0: the schedule ladder under a per-GPU cap (config 5 depth-scaled: old + new
+    # state does not fit, the arena has to rebuild it in layer bands; the analogue of the
+    # full 70B model on 8 GPUs under 180 GB)
+    c5cap = {2: 86e9, 4: 45e9}.get(world)
+    cases = [(S.config2(layers), 0), (S.config2(layers), 2), (S.config3(2)[0], 0)]
+    if c5cap:
+        cases.append((S.config5(8), -1))
+    for sc, groups in cases:
+        ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
-        arena = Arena.multi(ab, ba, world, rank, local, chunk_bytes=64 << 20, groups=groups or 64)
-        exchange_arena(arena, rank, world, tag=f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{groups}")
+        tag = f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{groups}"
+        if groups < 0:
+            arena, cuts = shared_arena(ab, ba, rank, world, local, cap_bytes=int(c5cap), tag=tag, chunk_bytes=64 << 20)
+        else:
+            arena = Arena.multi(ab, ba, world, rank, local, chunk_bytes=64 << 20, groups=groups or 64)
+            exchange_arena(arena, rank, world, tag=tag)
+            cuts = global_stage_cuts(arena, world)
         fwd = Transition(ab, world, rank, local, alloc=False)
         bwd = Transition(ba, world, rank, local, alloc=False)
-        arena.bind(fwd.ex, bwd.ex, global_stage_cuts(arena, world))
+        arena.bind(fwd.ex, bwd.ex, cuts)
         fwd.ex.prepare()
         bwd.ex.prepare()
         fwd.ex.fill(A.SIDE_SRC, seed)
@@ -52,7 +65,7 @@ def main():
             dist.barrier()
             bad.append(bwd.ex.verify(A.SIDE_DST, seed)[0])
         st = arena.stats()
-        print(f"[rank {rank}] {sc.name} groups={groups}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, physical {st.physical_bytes/1e9:.2f} GB "
+        print(f"[rank {rank}] {sc.name} groups={groups} bands={st.bands}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, physical {st.physical_bytes/1e9:.2f} GB "
               f"(old {st.a_bytes/1e9:.2f} + new {st.b_bytes/1e9:.2f}, aliased {st.aliased_bytes/1e9:.2f})", flush=True)
         fails += sum(1 for b in bad if b)
         del fwd, bwd, arena

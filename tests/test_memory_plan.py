@@ -65,3 +65,38 @@ def test_min_groups_fits_cap():
     k, need = memory_min_groups(ab, ba, 1, 0, most.physical_bytes)
     assert k > 1 and need <= most.physical_bytes
     assert memory_min_groups(ab, ba, 1, 0, most.physical_bytes - 1)[0] == -1
+
+
+def test_ladder_is_monotone_within_a_band_count():
+    """Group counts nest (1, 2, 4, ...), so within one band count more groups never need
+    more memory; the ladder starts with the no-aliasing plan."""
+    from paper_2605_18815_b200.api import memory_schedule_footprints, memory_schedule_level
+    sc = S.config2(2)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    for n_gpus, gpu in ((1, 0), (2, 1)):
+        f = memory_schedule_footprints(ab, ba, n_gpus, gpu, chunk_bytes=8 << 20)
+        levels = [memory_schedule_level(ab, i) for i in range(len(f))]
+        assert levels[0] == (1, 1)
+        for i in range(1, len(f)):
+            if levels[i][0] == levels[i - 1][0]:
+                assert f[i] <= f[i - 1], (levels[i - 1], levels[i], f[i - 1], f[i])
+
+
+def test_config5_full_fits_eight_gpus_under_the_cap():
+    """BASELINE config 5 (Llama-3-70B TP4xPP2 -> TP8, ZeRO-1): 247 GB of old + new state
+    per GPU on 8 GPUs. Rebuilding each new rank in layer bands inside the memory its old
+    layout frees brings every GPU under 180 GB; the plan replays without clobbering."""
+    from paper_2605_18815_b200.api import memory_schedule_footprints, memory_schedule_level
+    sc = S.config5(80)
+    ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+    cap = 179 * 10**9
+    f = [memory_schedule_footprints(ab, None, 8, g) for g in range(8)]
+    assert min(f[g][0] for g in range(8)) > 240e9  # no aliasing: does not fit
+    fits = [i for i in range(len(f[0])) if all(f[g][i] <= cap for g in range(8))]
+    assert fits
+    bands, groups = memory_schedule_level(ab, fits[0])
+    assert bands > 1
+    for g in range(8):
+        st, viol, _, _ = memory_plan(ab, None, n_gpus=8, gpu=g, groups=groups, bands=bands)
+        assert viol == 0 and st.physical_bytes <= cap and st.bands == bands
