@@ -23,7 +23,7 @@ from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
 
-NVLINK_GBS = 900.0
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
 
 def peaks():
