@@ -273,3 +273,18 @@ def test_multi_gpu_vmm_shared_buffers():
                         os.path.join(root, "tests", "mgpu_check.py"), "2", "--vmm"],
                        capture_output=True, text=True, timeout=900)
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_pack_unpack_single_gpu_staged_channels():
+    """Staged (Algorithm 1 buffered) channels packed and unpacked on one GPU: the
+    destinations are bit-exact and both kernels move their bytes."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "pack_bench.py"), "--layers", "2", "--reps", "1"],
+                       capture_output=True, text=True, timeout=600)
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    d = json.loads(line[-1])
+    assert d["verified_mismatches"] == 0 and d["channels"] > 0 and d["channel_bytes"] > 0
