@@ -276,10 +276,11 @@ int rs_memory_plan_ex(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_
                       int gpu, int groups, int bands, rs_arena_stats_t* stats, int64_t* violations, int* order_ab,
                       int* order_ba, int cap);
 /* the schedule ladder (arena.hpp schedule_levels): the first level whose plan for `gpu`
- * fits cap_bytes (*level = -1: none); rs_memory_schedule_level gives its (bands, groups) */
+ * fits cap_bytes (*level = -1: none); rs_memory_schedule_level gives its (bands, groups),
+ * groups -1 = rounds (one unit per GPU per group) */
 int rs_memory_schedule(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads, int n_gpus,
                        int gpu, int64_t cap_bytes, int* level, int64_t* physical_bytes);
-int rs_memory_schedule_level(const rs_plan_t* plan_ab, int level, int* bands, int* groups);
+int rs_memory_schedule_level(const rs_plan_t* plan_ab, int n_gpus, int level, int* bands, int* groups);
 /* physical bytes GPU `gpu` needs at every level of the ladder (*n = number of levels):
  * across GPUs, take the first level whose footprint fits on every rank */
 int rs_memory_schedule_footprints(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,

@@ -442,10 +442,10 @@ def memory_schedule_footprints(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpu
     return list(out[: n.value])
 
 
-def memory_schedule_level(ab: RoutingPlan, level: int):
-    """(bands, groups) of a schedule level."""
+def memory_schedule_level(ab: RoutingPlan, level: int, n_gpus: int = 1):
+    """(bands, groups) of a schedule level of the n_gpus ladder (groups -1: rounds)."""
     b, g = C.c_int(), C.c_int()
-    A.check(A.lib().rs_memory_schedule_level(ab.h, level, C.byref(b), C.byref(g)))
+    A.check(A.lib().rs_memory_schedule_level(ab.h, n_gpus, level, C.byref(b), C.byref(g)))
     return b.value, g.value
 
 

@@ -102,13 +102,13 @@ Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConf
         cap = static_cast<std::int64_t>(fr) - (1ll << 30);
     }
     int groups = cfg.groups, bands = std::max(1, cfg.bands);
-    if (groups <= 0) {
+    if (groups == 0) {
         std::int64_t need = 0;
         const int level = choose_schedule(ab, ba, C, with_grads, n_gpus, gpu, cap, &need);
         if (level < 0)
             throw exec::BudgetError(strfmt("infeasible budget: memory plan needs %.2f GB of HBM on GPU %d, cap %.2f GB",
                                            need / 1e9, gpu, cap / 1e9));
-        const ScheduleLevel L = schedule_levels(ab)[static_cast<size_t>(level)];
+        const ScheduleLevel L = schedule_levels(ab, n_gpus)[static_cast<size_t>(level)];
         groups = L.groups;
         bands = L.bands;
     }

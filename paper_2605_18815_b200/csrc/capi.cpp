@@ -979,9 +979,9 @@ int rs_memory_schedule_footprints(const rs_plan_t* ab, const rs_plan_t* ba, int6
     });
 }
 
-int rs_memory_schedule_level(const rs_plan_t* ab, int level, int* bands, int* groups) {
+int rs_memory_schedule_level(const rs_plan_t* ab, int n_gpus, int level, int* bands, int* groups) {
     return guarded([&] {
-        const std::vector<mem::ScheduleLevel> L = mem::schedule_levels(ab->core);
+        const std::vector<mem::ScheduleLevel> L = mem::schedule_levels(ab->core, n_gpus);
         if (level < 0 || level >= static_cast<int>(L.size())) throw ConfigError("schedule level out of range");
         *bands = L[static_cast<size_t>(level)].bands;
         *groups = L[static_cast<size_t>(level)].groups;

@@ -48,13 +48,16 @@ UnitMap::UnitMap(const core::PlanCore& P, int bands) : nb(std::max(1, bands)), n
 
 namespace {
 
-// One greedy pass over the units. peak_first: among the stages that keep their GPU under
-// the running peak, the one freeing the most old bytes on its own GPU, else the lowest
-// peak; otherwise: the stage freeing the most old bytes anywhere. Returns the order and
-// the modeled peak (max over GPUs of live bytes: old data still to be read + new data
-// written so far).
+// One greedy pass over the units. kFreed: the stage freeing the most old bytes anywhere.
+// kPeak: among the stages that keep their GPU under the running peak, the one freeing the
+// most old bytes on its own GPU, else the lowest peak. kRounds: kPeak restricted to the
+// GPUs in turn, so every G consecutive positions hold one unit per GPU (rounds: all links
+// busy in every group). Returns the order and the modeled peak (max over GPUs of live
+// bytes: old data still to be read + new data written so far).
+enum PassMode { kFreed = 0, kPeak = 1, kRounds = 2 };
 std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops,
-                                                      int bands, int n_gpus, bool peak_first) {
+                                                      int bands, int n_gpus, int mode) {
+    const bool peak_first = mode != kFreed;
     const UnitMap U(P, bands);
     const int ns = P.src_cfg.world_size(), nd = P.dst_cfg.world_size();
     const int nsu = ns * U.nb, ndu = nd * U.nb;
@@ -88,13 +91,22 @@ std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, c
     std::vector<char> done(static_cast<size_t>(ndu), 0);
     std::vector<int> order;
     order.reserve(static_cast<size_t>(ndu));
+    std::vector<int> left(static_cast<size_t>(G), 0);
+    for (int du = 0; du < ndu; ++du) ++left[static_cast<size_t>(gpu_dst(du / U.nb))];
+    int turn = 0;
     for (int step = 0; step < ndu; ++step) {
         int best = -1;
         bool best_under = false;
         std::int64_t best_freed = -1, best_peak = 0;
+        int target = -1;
+        if (mode == kRounds) {
+            while (!left[static_cast<size_t>(turn % G)]) ++turn;
+            target = turn++ % G;
+        }
         for (int du = 0; du < ndu; ++du) {
             if (done[static_cast<size_t>(du)]) continue;
             const int g = gpu_dst(du / U.nb);
+            if (target >= 0 && g != target) continue;
             const std::int64_t during = live[static_cast<size_t>(g)] + w_dst[static_cast<size_t>(du)];
             std::int64_t freed = 0;
             for (int su : reads[static_cast<size_t>(du)])
@@ -116,6 +128,7 @@ std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, c
         done[static_cast<size_t>(best)] = 1;
         order.push_back(best);
         const int g = gpu_dst(best / U.nb);
+        --left[static_cast<size_t>(g)];
         live[static_cast<size_t>(g)] += w_dst[static_cast<size_t>(best)];
         peak = std::max(peak, live[static_cast<size_t>(g)]);
         for (int su : reads[static_cast<size_t>(best)])
@@ -130,8 +143,8 @@ std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<e
                                     int n_gpus) {
     // both heuristics, keep the lower modeled peak (a global criterion: every rank picks
     // the same order)
-    auto a = greedy_pass(P, ops, bands, n_gpus, false);
-    auto b = greedy_pass(P, ops, bands, n_gpus, true);
+    auto a = greedy_pass(P, ops, bands, n_gpus, kFreed);
+    auto b = greedy_pass(P, ops, bands, n_gpus, kPeak);
     return b.second < a.second ? b.first : a.first;
 }
 
@@ -151,14 +164,20 @@ MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::
 MemoryPlan plan_memory_ops(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
                            const std::vector<exec::CopyOp>& ops_ba, std::int64_t C, bool with_grads, int n_gpus, int gpu,
                            int groups, int bands) {
+    if (groups < 0) {  // rounds: one unit per GPU per group
+        const int G = std::max(1, n_gpus);
+        const int units = UnitMap(ab, bands).count();
+        return plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, (units + G - 1) / G, bands,
+                               greedy_pass(ab, ops_ab, bands, n_gpus, kRounds).first);
+    }
     if (n_gpus > 1)  // the order must be global: the modeled-peak choice
         return plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
                                greedy_stage_order(ab, ops_ab, bands, n_gpus));
     // one GPU: both greedy orders, keep the smaller footprint
     MemoryPlan a = plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
-                                   greedy_pass(ab, ops_ab, bands, n_gpus, false).first);
+                                   greedy_pass(ab, ops_ab, bands, n_gpus, kFreed).first);
     MemoryPlan b = plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, groups, bands,
-                                   greedy_pass(ab, ops_ab, bands, n_gpus, true).first);
+                                   greedy_pass(ab, ops_ab, bands, n_gpus, kPeak).first);
     return b.stats.physical_bytes < a.stats.physical_bytes ? b : a;
 }
 
@@ -298,20 +317,30 @@ MemoryPlan plan_with_order(const core::PlanCore& ab, const core::PlanCore* ba, c
 }
 }  // namespace
 
-std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab) {
+std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab, int n_gpus) {
     std::vector<ScheduleLevel> v;
     const int nd = ab.dst_cfg.world_size();
     const int L = std::max(1, ab.space->num_layers());
+    const int G = std::max(1, n_gpus);
     for (int nb = 1;; nb *= 2) {
         const int n = std::min(nb, L);
         const int units = nd * n;
+        const int rounds = (units + G - 1) / G;
         // group counts 1, 2, 4, ... and finally one group per unit: each count refines the
-        // previous one (nested boundaries), so within a band count more groups never alias less
+        // previous one (nested boundaries), so within a band count more groups never alias
+        // less. Across GPUs the rounds order (one unit per GPU per group, groups = -1) comes
+        // before the levels with as many or more groups: same barriers, every link busy.
         std::vector<int> ks;
         for (int k = 1; k < units; k *= 2) ks.push_back(k);
         ks.push_back(units);
-        for (int k : ks)
+        bool rounds_done = G < 2 || rounds < 2;
+        for (int k : ks) {
+            if (!rounds_done && k >= rounds) {
+                v.push_back({n, -1});
+                rounds_done = true;
+            }
             if (!(n > 1 && k == 1)) v.push_back({n, k});  // one group is the same at any band count
+        }
         if (n >= L) break;
     }
     return v;
@@ -321,7 +350,7 @@ int choose_schedule(const core::PlanCore& ab, const core::PlanCore* ba, std::int
                     int gpu, std::int64_t cap, std::int64_t* physical) {
     const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
     const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
-    const std::vector<ScheduleLevel> levels = schedule_levels(ab);
+    const std::vector<ScheduleLevel> levels = schedule_levels(ab, n_gpus);
     std::int64_t best = std::numeric_limits<std::int64_t>::max();
     for (size_t i = 0; i < levels.size();) {
         // a band count whose most-aliased plan does not fit is skipped whole: its other
@@ -354,7 +383,7 @@ std::vector<std::int64_t> schedule_footprints(const core::PlanCore& ab, const co
     const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
     const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
     std::vector<std::int64_t> out;
-    for (const ScheduleLevel& L : schedule_levels(ab))
+    for (const ScheduleLevel& L : schedule_levels(ab, n_gpus))
         out.push_back(plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, L.groups, L.bands).stats.physical_bytes);
     return out;
 }

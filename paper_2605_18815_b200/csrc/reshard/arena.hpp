@@ -29,7 +29,8 @@ struct ArenaConfig {
     int device = 0;
     std::int64_t cap_bytes = 0;             // physical budget; 0 -> free memory minus 1 GiB
     std::int64_t chunk_bytes = 32ll << 20;  // physical chunk (multiple of the VMM granularity)
-    int groups = 0;  // concurrency groups of the stage order; 0 -> the cheapest schedule level that fits the cap
+    int groups = 0;  // concurrency groups of the unit order; 0 -> the cheapest schedule level that fits the cap;
+                     // -1 -> rounds (one unit per GPU per group)
     int bands = 1;   // layer bands per destination rank (with groups > 0)
 };
 
@@ -91,9 +92,9 @@ int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::in
 /// The schedule ladder, cheapest first: for bands 1, 2, 4, ... (up to the layer count)
 /// group counts from one (no aliasing) to one per unit (most aliasing).
 struct ScheduleLevel {
-    int bands, groups;
+    int bands, groups;  // groups -1: rounds (one unit per GPU per group)
 };
-std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab);
+std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab, int n_gpus = 1);
 /// first level of the ladder whose plan fits `cap` on `gpu` (-1: none; *physical = the
 /// smallest footprint seen). One GPU; across GPUs use schedule_footprints.
 int choose_schedule(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk, bool with_grads, int n_gpus,

@@ -227,7 +227,7 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
         raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs >= {min(need) / 1e9:.2f} GB, "
                                               f"cap {cap_bytes / 1e9:.2f} GB)")
     lv = fits[0]
-    bands, k = memory_schedule_level(ab, lv)
+    bands, k = memory_schedule_level(ab, lv, world)
     arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k, bands=bands)
     exchange_arena(arena, rank, world, tag)
     return arena, global_stage_cuts(arena, world)

@@ -35,13 +35,18 @@ def main():
     c5cap = {2: 86e9, 4: 45e9}.get(world)
     cases = [(S.config2(layers), 0), (S.config2(layers), 2), (S.config3(2)[0], 0)]
     if c5cap:
-        cases.append((S.config5(8), -1))
+        cases.append((S.config5(8), "cap"))
+        cases.append((S.config5(8), "rounds"))
     for sc, groups in cases:
         ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
         tag = f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{groups}"
-        if groups < 0:
+        if groups == "cap":
             arena, cuts = shared_arena(ab, ba, rank, world, local, cap_bytes=int(c5cap), tag=tag, chunk_bytes=64 << 20)
+        elif groups == "rounds":  # one unit per GPU per group, 4 layer bands
+            arena = Arena.multi(ab, ba, world, rank, local, chunk_bytes=64 << 20, groups=-1, bands=4)
+            exchange_arena(arena, rank, world, tag=tag)
+            cuts = global_stage_cuts(arena, world)
         else:
             arena = Arena.multi(ab, ba, world, rank, local, chunk_bytes=64 << 20, groups=groups or 64)
             exchange_arena(arena, rank, world, tag=tag)
@@ -55,17 +60,21 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         bad = []
+        import time
+        ms = []
         for _ in range(2):
+            t0 = time.perf_counter()
             run_stages(fwd.ex, 0, world)
             torch.cuda.synchronize()
             dist.barrier()
+            ms.append(round(1e3 * (time.perf_counter() - t0), 1))
             bad.append(fwd.ex.verify(A.SIDE_DST, seed)[0])
             run_stages(bwd.ex, 0, world)
             torch.cuda.synchronize()
             dist.barrier()
             bad.append(bwd.ex.verify(A.SIDE_DST, seed)[0])
         st = arena.stats()
-        print(f"[rank {rank}] {sc.name} groups={groups} bands={st.bands}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, physical {st.physical_bytes/1e9:.2f} GB "
+        print(f"[rank {rank}] {sc.name} groups={groups} bands={st.bands}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, forward {ms} ms, physical {st.physical_bytes/1e9:.2f} GB "
               f"(old {st.a_bytes/1e9:.2f} + new {st.b_bytes/1e9:.2f}, aliased {st.aliased_bytes/1e9:.2f})", flush=True)
         fails += sum(1 for b in bad if b)
         del fwd, bwd, arena
