@@ -138,6 +138,21 @@ def cpu_baseline(layers_sample: int = 1, reps: int = 2):
     return cb.describe(cb.bytes / min(ts) / 1e9)
 
 
+def nvlink_wire(user_gbs: float) -> dict:
+    """NVLink protocol overhead of the 16-byte peer stores, measured by ncu (nvltx bytes
+    of user data vs protocol, profiles/r01_p2p_nvlink_ncu.json): user GB/s -> wire GB/s."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_p2p_nvlink_ncu.json")
+    try:
+        with open(p) as f:
+            ov = float(json.load(f)["nvlink_protocol_overhead"])
+    except (OSError, ValueError, KeyError):
+        return {}
+    wire = user_gbs * (1 + ov)
+    return {"nvlink_protocol_overhead": ov, "nvlink_wire_gbs": round(wire, 1),
+            "nvlink_wire_frac_of_nominal_900": round(wire / NVLINK_GBS, 4),
+            "nvlink_wire_source": "profiles/r01_p2p_nvlink_ncu.json (ncu nvltx__bytes_data_user / _protocol)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -375,6 +390,7 @@ def run_ours(args):
                     "traffic": None, "kernel": "copy_tiles_kernel<16> mixed local/peer launch (forward transition, binding GPU)",
                     "algorithmic_bytes_per_launch": link, "t_roof_s": round(t_roof, 5),
                     "per_gpu_out_in_gb": [[round(p.out_bytes / 1e9, 2), round(p.in_bytes / 1e9, 2)] for p in pl],
+                    **nvlink_wire(nv),
                     "hbm_achieved_gbs_rank0": round(achieved_hbm, 1)}
         # planner: ZeRO transfer-list expansion (1.84 M reference SliceTransfers at L=32) on the
         # GPU planner vs the host sweep; the reference's own O(n*m) planner needs hours at L=32

@@ -112,6 +112,9 @@ typedef struct {
 
 const char* rs_last_error(void);
 const char* rs_version(void);
+/* one process driving several GPUs: let `device` store into `peer`'s memory directly
+ * (cudaDeviceEnablePeerAccess; already-enabled is not an error) */
+int rs_enable_peer_access(int device, int peer);
 void rs_free(void* p);
 
 /* build_model_space (model.hpp:127-144), validate_model (model.hpp:95-123) */

@@ -610,3 +610,8 @@ class VmmBuffer:
 
     def __del__(self):
         self.close()
+
+
+def enable_peer_access(device: int, peer: int) -> None:
+    """One process driving several GPUs: direct stores from `device` into `peer`."""
+    A.check(A.lib().rs_enable_peer_access(device, peer))

@@ -761,6 +761,19 @@ int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t*
     });
 }
 
+int rs_enable_peer_access(int device, int peer) {
+    return guarded([&] {
+        if (cudaSetDevice(device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+        const cudaError_t r = cudaDeviceEnablePeerAccess(peer, 0);
+        if (r == cudaErrorPeerAccessAlreadyEnabled) {
+            cudaGetLastError();
+        } else if (r != cudaSuccess) {
+            throw exec::CudaError(strfmt("cudaDeviceEnablePeerAccess(%d -> %d): %s", device, peer, cudaGetErrorString(r)));
+        }
+        return RS_OK;
+    });
+}
+
 int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream) {
     return guarded([&] {
         if (side < 0 || side > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");

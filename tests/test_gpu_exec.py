@@ -288,3 +288,18 @@ def test_pack_unpack_single_gpu_staged_channels():
     assert line, r.stdout[-2000:] + r.stderr[-2000:]
     d = json.loads(line[-1])
     assert d["verified_mismatches"] == 0 and d["channels"] > 0 and d["channel_bytes"] > 0
+
+
+def test_single_process_peer_push():
+    """One process drives 2 GPUs (peer access, no cudaIpc): the fused push is bit-exact."""
+    import json
+    import subprocess
+    import sys
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "p2p_profile.py"), "--layers", "1", "--reps", "1"],
+                       capture_output=True, text=True, timeout=600)
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert line, r.stdout[-2000:] + r.stderr[-2000:]
+    assert json.loads(line[-1])["verified_mismatches"] == 0

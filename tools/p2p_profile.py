@@ -1,0 +1,92 @@
+"""The fused push across GPUs driven from ONE process (so ncu can attach): each GPU's
+executor stores its peer-bound tiles straight into the other GPU's memory (peer access,
+no cudaIpc). Both halves of the north star's forward transition on 2 GPUs, bit-exact,
+with per-GPU NVLink GB/s from CUDA events.
+
+    python tools/p2p_profile.py [--layers 4] [--reps 3]
+    ncu --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,... \\
+        -k regex:copy_tiles python tools/p2p_profile.py --reps 1
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2605_18815_b200 import _capi as A  # noqa: E402
+from paper_2605_18815_b200 import scenarios as S  # noqa: E402
+from paper_2605_18815_b200.api import Executor, RoutingPlan, enable_peer_access  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    G = 2
+    if torch.cuda.device_count() < G:
+        print(json.dumps({"skipped": "needs 2 GPUs"}))
+        return
+    for a in range(G):
+        for b in range(G):
+            if a != b:
+                enable_peer_access(a, b)
+    plan = RoutingPlan.from_scenario(S.config2(args.layers))
+    ex = [Executor(plan, n_gpus=G, gpu=g, device=g) for g in range(G)]
+    keep = []
+    for side in (A.SIDE_SRC, A.SIDE_DST):
+        n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
+        for r in range(n):
+            for b in range(6):
+                _, nbytes, g = ex[0].buffer(side, r, b)
+                if not nbytes:
+                    continue
+                t = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
+                keep.append(t)
+                for e in ex:  # every executor sees every buffer (peer pointers for the other GPU's)
+                    e.bind(side, r, b, t.data_ptr(), nbytes)
+    seed = 0xD00D
+    streams = []
+    for g, e in enumerate(ex):
+        torch.cuda.set_device(g)
+        e.prepare()
+        e.fill(A.SIDE_SRC, seed)
+        streams.append(torch.cuda.Stream(device=g))
+    for g in range(G):
+        torch.cuda.synchronize(g)
+
+    def step():
+        evs = []
+        for g, e in enumerate(ex):
+            with torch.cuda.device(g):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(streams[g])
+                e.run(streams[g].cuda_stream)
+                e1.record(streams[g])
+                evs.append((e0, e1))
+        for g in range(G):
+            torch.cuda.synchronize(g)
+        return [a.elapsed_time(b) for a, b in evs]
+
+    step()
+    best = None
+    for _ in range(args.reps):
+        ts = step()
+        best = ts if best is None or max(ts) < max(best) else best
+    bad = sum(e.verify(A.SIDE_DST, seed)[0] for e in ex)
+    st = [e.stats() for e in ex]
+    out = {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1 forward, 2 GPUs from one process (peer access)",
+           "ms_per_gpu": [round(t, 3) for t in best],
+           "remote_gb_per_gpu": [round(s.remote_bytes / 1e9, 3) for s in st],
+           "local_gb_per_gpu": [round(s.local_bytes / 1e9, 3) for s in st],
+           "nvlink_out_gbs_per_gpu": [round(s.remote_bytes / (t / 1e3) / 1e9, 1) for s, t in zip(st, best)],
+           "verified_mismatches": int(bad)}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
