@@ -22,6 +22,11 @@ def _cfg_t(c: Cfg, keep: list) -> A.Cfg_t:
     return A.Cfg_t(c.dp, c.tp, c.pp, c.ep, int(c.zero), order)
 
 
+def _alive() -> bool:
+    """The library is still loaded (destructors may run during interpreter shutdown)."""
+    return A is not None and A._lib is not None
+
+
 class RoutingPlan:
     """plan_parameters + plan_optimizer + plan_scalars + resolve_peers (routing.hpp:231-396)."""
 
@@ -40,7 +45,7 @@ class RoutingPlan:
         return cls(h.value)
 
     def __del__(self):
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_plan_destroy(self.h)
             self.h = None
 
@@ -83,6 +88,18 @@ class RoutingPlan:
         A.lib().rs_free(p)
         return out
 
+    def expand_timed(self, device: int = 0):
+        """(milliseconds, runs) of expanding the ZeRO transfer list: GPU planner or host."""
+        ms, n = C.c_double(), C.c_int64()
+        A.check(A.lib().rs_plan_expand_timed(self.h, device, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def validate(self, drop: int = -1) -> List[str]:
+        """validate_plan: violation lines, empty on success."""
+        p, n, k = C.c_void_p(), C.c_size_t(), C.c_int64()
+        A.check(A.lib().rs_plan_validate(self.h, drop, C.byref(p), C.byref(n), C.byref(k)))
+        return [x for x in A.take_string(p, n).splitlines() if x]
+
 
 class ModelSpace:
     """build_model_space (model.hpp:127-144)."""
@@ -102,7 +119,7 @@ class ModelSpace:
         self.model = model
 
     def __del__(self):
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_model_destroy(self.h)
             self.h = None
 
@@ -141,10 +158,11 @@ class Executor:
         self.n_gpus, self.gpu, self.device = n_gpus, gpu, device
 
     def __del__(self):
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_exec_destroy(self.h)
             self.h = None
 
+    # ---- buffers
     def alloc(self) -> None:
         A.check(A.lib().rs_exec_alloc(self.h))
 
@@ -166,16 +184,65 @@ class Executor:
     def ipc_import(self, blob: bytes) -> None:
         A.check(A.lib().rs_exec_ipc_import(self.h, blob, len(blob)))
 
+    def read(self, side: int, rank: int, buf: int, offset: int, nbytes: int, stream: int = 0) -> bytes:
+        """Read `nbytes` of a buffer back to the host (synchronous on `stream`)."""
+        out = C.create_string_buffer(nbytes)
+        A.check(A.lib().rs_exec_read(self.h, side, rank, buf, offset, out, nbytes, C.c_void_p(stream)))
+        return out.raw
+
+    # ---- fused push
     def prepare(self) -> None:
         A.check(A.lib().rs_exec_prepare(self.h))
-
-    def fill(self, side: int, seed: int, stream: int = 0) -> None:
-        A.check(A.lib().rs_exec_fill(self.h, side, seed, C.c_void_p(stream)))
 
     def run(self, stream: int = 0) -> int:
         n = C.c_int()
         A.check(A.lib().rs_exec_run(self.h, C.c_void_p(stream), C.byref(n)))
         return n.value
+
+    def set_stages(self, dst_order) -> None:
+        arr = (C.c_int * max(1, len(dst_order)))(*dst_order)
+        A.check(A.lib().rs_exec_set_stages(self.h, arr, len(dst_order)))
+
+    def num_stages(self) -> int:
+        n = C.c_int()
+        A.check(A.lib().rs_exec_num_stages(self.h, C.byref(n)))
+        return n.value
+
+    def run_stage(self, stage: int, stream: int = 0) -> int:
+        n = C.c_int()
+        A.check(A.lib().rs_exec_run_stage(self.h, stage, C.c_void_p(stream), C.byref(n)))
+        return n.value
+
+    # ---- staged (Algorithm 1 buffered) channels
+    def prepare_staged(self) -> None:
+        A.check(A.lib().rs_exec_prepare_staged(self.h))
+
+    def channel_bytes(self, src_phys: int, dst_phys: int) -> int:
+        n = C.c_int64()
+        A.check(A.lib().rs_exec_channel_bytes(self.h, src_phys, dst_phys, C.byref(n)))
+        return n.value
+
+    def pack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_pack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
+
+    def unpack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_unpack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
+
+    # ---- broadcast promotion (NVLS multicast)
+    def bcast_groups(self) -> List[A.BcastGroup_t]:
+        """Broadcast groups of this plan and placement (identical on every rank)."""
+        n = C.c_int()
+        A.check(A.lib().rs_exec_bcast_groups(self.h, None, 0, C.byref(n)))
+        arr = (A.BcastGroup_t * max(1, n.value))()
+        A.check(A.lib().rs_exec_bcast_groups(self.h, arr, n.value, C.byref(n)))
+        return list(arr[: n.value])
+
+    def set_multicast(self, group_id: int, mc_va: int) -> None:
+        A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
+
+    # ---- synthetic state
+    def fill(self, side: int, seed: int, stream: int = 0) -> None:
+        A.check(A.lib().rs_exec_fill(self.h, side, seed, C.c_void_p(stream)))
 
     def verify(self, side: int, seed: int, stream: int = 0):
         bad, first = C.c_int64(), C.c_int64()
@@ -189,13 +256,10 @@ class Executor:
         A.check(A.lib().rs_exec_stats(self.h, C.byref(s)))
         return s
 
-    def set_stages(self, dst_order) -> None:
-        arr = (C.c_int * max(1, len(dst_order)))(*dst_order)
-        A.check(A.lib().rs_exec_set_stages(self.h, arr, len(dst_order)))
-
 
 class Arena:
-    """VMM old/new layouts on one GPU with plan-time eager-free aliasing (arena.hpp)."""
+    """VMM old/new layouts with plan-time eager-free aliasing (arena.hpp): one GPU, or
+    (Arena.multi) the buffers one GPU of several hosts, shared by POSIX descriptor."""
 
     def __init__(self, ab: RoutingPlan, ba: Optional[RoutingPlan] = None, device: int = 0, cap_bytes: int = 0,
                  chunk_bytes: int = 0, with_grads: bool = False):
@@ -205,8 +269,20 @@ class Arena:
         self.h = h.value
         self.ab, self.ba = ab, ba
 
+    @classmethod
+    def multi(cls, ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, device: int,
+              cap_bytes: int = 0, chunk_bytes: int = 0, with_grads: bool = False, groups: int = 0,
+              bands: int = 1) -> "Arena":
+        """groups 0: the cheapest schedule level that fits cap_bytes; -1: rounds."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        A.check(A.lib().rs_arena_create_multi(ab.h, ba.h if ba else None, n_gpus, gpu, device, cap_bytes, chunk_bytes,
+                                              int(with_grads), groups, bands, C.byref(h)))
+        self.h, self.ab, self.ba = h.value, ab, ba
+        return self
+
     def __del__(self):
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_arena_destroy(self.h)
             self.h = None
 
@@ -215,16 +291,17 @@ class Arena:
         A.check(A.lib().rs_arena_buffer(self.h, layout, rank, buf, C.byref(p), C.byref(n)))
         return p.value or 0, n.value
 
+    def bind_size(self, layout: int, rank: int, buf: int) -> int:
+        """Bytes a multicast object must span to bind that buffer whole."""
+        n = C.c_int64()
+        A.check(A.lib().rs_arena_bind_size(self.h, layout, rank, buf, C.byref(n)))
+        return n.value
+
     def stage_order(self, direction: int) -> List[int]:
         out = (C.c_int * 65536)()
         n = C.c_int()
         A.check(A.lib().rs_arena_stage_order(self.h, direction, out, 65536, C.byref(n)))
         return list(out[: n.value])
-
-    def stats(self) -> A.ArenaStats_t:
-        s = A.ArenaStats_t()
-        A.check(A.lib().rs_arena_stats(self.h, C.byref(s)))
-        return s
 
     def stage_cuts(self, direction: int) -> List[int]:
         """1 where a barrier must precede that stage position; the positions in between
@@ -234,10 +311,30 @@ class Arena:
         A.check(A.lib().rs_arena_stage_cuts(self.h, direction, out, 65536, C.byref(n)))
         return list(out[: n.value])
 
+    def stats(self) -> A.ArenaStats_t:
+        s = A.ArenaStats_t()
+        A.check(A.lib().rs_arena_stats(self.h, C.byref(s)))
+        return s
+
+    def export(self):
+        """(descriptors, mapping table) of this GPU's physical allocations (caller closes fds)."""
+        p_fds, n, p_t, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
+        A.check(A.lib().rs_arena_export(self.h, C.byref(p_fds), C.byref(n), C.byref(p_t), C.byref(ln)))
+        fds = [p_fds[i] for i in range(n.value)]
+        table = C.string_at(p_t.value, ln.value)
+        A.lib().rs_free(C.cast(p_fds, C.c_void_p))
+        A.lib().rs_free(p_t)
+        return fds, table
+
+    def import_peer(self, fds: Sequence[int], table: bytes) -> None:
+        """Map a peer's buffers (consumes the descriptors)."""
+        arr = (C.c_int * max(1, len(fds)))(*fds)
+        A.check(A.lib().rs_arena_import(self.h, arr, len(fds), table, len(table)))
+
     def bind(self, fwd: "Executor", bwd: Optional["Executor"] = None, cuts=None) -> None:
         """Bind A/B buffers into the forward (A->B) and backward (B->A) executors and
         set their stage orders, grouped by `cuts` (default: this arena's own; with
-        several GPUs pass the union over all GPUs, runtime.exchange_arena)."""
+        several GPUs pass the union over all GPUs, runtime.global_stage_cuts)."""
         for layout, nr in ((0, self.ab.summary.src_world), (1, self.ab.summary.dst_world)):
             for r in range(nr):
                 for b in range(6):
@@ -256,29 +353,6 @@ class Arena:
             A.check(A.lib().rs_exec_set_stage_groups(ex.h, arr_o, arr_c, len(order)))
 
 
-def xor_peer(i: int, s: int, n: int) -> int:
-    """Peer(i, s) = i XOR s, or -1 when outside the device set (SPEC.md:302-310)."""
-    return A.lib().rs_xor_peer(i, s, n)
-
-
-def memory_aware_chunk(steps: Sequence[int], costs: Sequence[int], mem_avail: Sequence[int]):
-    """MemoryAwareChunk (PAPER.md:696-717): returns (stages as lists of steps, budget)."""
-    n = len(steps)
-    st = (C.c_int * max(1, n))(*steps)
-    co = (C.c_int64 * max(1, n))(*costs)
-    av = (C.c_int64 * max(1, len(mem_avail)))(*mem_avail)
-    out = (C.c_int * max(1, n))()
-    budget = C.c_int64()
-    A.check(A.lib().rs_memory_aware_chunk(st, co, n, av, len(mem_avail), out, C.byref(budget)))
-    stages: List[List[int]] = []
-    for k in range(n):
-        g = out[k]
-        while len(stages) <= g:
-            stages.append([])
-        stages[g].append(steps[k])
-    return stages, budget.value
-
-
 class Schedule:
     """build_schedule over a RoutingPlan."""
 
@@ -295,7 +369,7 @@ class Schedule:
         self.summary = s
 
     def __del__(self):
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_schedule_destroy(self.h)
             self.h = None
 
@@ -331,205 +405,6 @@ class Schedule:
         return A.take_string(p, n)
 
 
-def _exec_staged_methods():
-    def prepare_staged(self) -> None:
-        A.check(A.lib().rs_exec_prepare_staged(self.h))
-
-    def channel_bytes(self, src_phys: int, dst_phys: int) -> int:
-        n = C.c_int64()
-        A.check(A.lib().rs_exec_channel_bytes(self.h, src_phys, dst_phys, C.byref(n)))
-        return n.value
-
-    def pack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
-        A.check(A.lib().rs_exec_pack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
-
-    def unpack(self, src_phys: int, dst_phys: int, ptr: int, stream: int = 0) -> None:
-        A.check(A.lib().rs_exec_unpack(self.h, src_phys, dst_phys, C.c_void_p(ptr), C.c_void_p(stream)))
-
-    Executor.prepare_staged = prepare_staged
-    Executor.channel_bytes = channel_bytes
-    Executor.pack = pack
-    Executor.unpack = unpack
-
-
-_exec_staged_methods()
-
-
-def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False,
-                n_gpus: int = 1, gpu: int = 0, groups: int = 0, bands: int = 1):
-    """Host-only arena plan of the buffers `gpu` hosts: (stats, simulated violations,
-    stage orders over units rank * bands + band); `groups` coarsens the unit order
-    (0 = one group per unit), `bands` splits destination ranks into layer bands."""
-    st, viol = A.ArenaStats_t(), C.c_int64()
-    oa, ob = (C.c_int * 65536)(), (C.c_int * 65536)()
-    A.check(A.lib().rs_memory_plan_ex(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, groups,
-                                      bands, C.byref(st), C.byref(viol), oa, ob, 65536))
-    return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
-
-
-def _plan_expand_timed(self, device: int = 0):
-    """(milliseconds, runs) of expanding the ZeRO transfer list: GPU planner or host."""
-    ms, n = C.c_double(), C.c_int64()
-    A.check(A.lib().rs_plan_expand_timed(self.h, device, C.byref(ms), C.byref(n)))
-    return ms.value, n.value
-
-
-RoutingPlan.expand_timed = _plan_expand_timed
-
-
-def _plan_validate(self, drop: int = -1) -> List[str]:
-    """validate_plan: violation lines, empty on success."""
-    p, n, k = C.c_void_p(), C.c_size_t(), C.c_int64()
-    A.check(A.lib().rs_plan_validate(self.h, drop, C.byref(p), C.byref(n), C.byref(k)))
-    return [x for x in A.take_string(p, n).splitlines() if x]
-
-
-RoutingPlan.validate = _plan_validate
-
-
-# ---- multi-GPU arena, descriptor exchange, staged runs -------------------------
-
-def fdx_listen(name: str) -> int:
-    s = C.c_int()
-    A.check(A.lib().rs_fdx_listen(name.encode(), C.byref(s)))
-    return s.value
-
-
-def fdx_send(peer: str, fds: Sequence[int], payload: bytes) -> None:
-    arr = (C.c_int * max(1, len(fds)))(*fds)
-    A.check(A.lib().rs_fdx_send(peer.encode(), arr, len(fds), payload, len(payload)))
-
-
-def fdx_recv(sock: int):
-    p_fds, n, p_pl, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
-    A.check(A.lib().rs_fdx_recv(sock, C.byref(p_fds), C.byref(n), C.byref(p_pl), C.byref(ln)))
-    fds = [p_fds[i] for i in range(n.value)]
-    payload = C.string_at(p_pl.value, ln.value) if ln.value else b""
-    A.lib().rs_free(C.cast(p_fds, C.c_void_p))
-    A.lib().rs_free(p_pl)
-    return fds, payload
-
-
-def fdx_close(fd: int) -> None:
-    A.lib().rs_fdx_close(fd)
-
-
-def memory_min_groups(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
-                      chunk_bytes: int = 0, with_grads: bool = False):
-    """(fewest stage groups whose plan fits cap_bytes on `gpu` or -1, physical bytes)."""
-    g, phys = C.c_int(), C.c_int64()
-    A.check(A.lib().rs_memory_min_groups(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
-                                         cap_bytes, C.byref(g), C.byref(phys)))
-    return g.value, phys.value
-
-
-def memory_schedule(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
-                    chunk_bytes: int = 0, with_grads: bool = False):
-    """(first schedule level that fits cap_bytes on `gpu` or -1, its physical bytes)."""
-    lv, phys = C.c_int(), C.c_int64()
-    A.check(A.lib().rs_memory_schedule(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, cap_bytes,
-                                       C.byref(lv), C.byref(phys)))
-    return lv.value, phys.value
-
-
-def memory_schedule_footprints(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int,
-                               chunk_bytes: int = 0, with_grads: bool = False) -> List[int]:
-    """Physical bytes `gpu` needs at every level of the schedule ladder."""
-    n = C.c_int()
-    out = (C.c_int64 * 4096)()
-    A.check(A.lib().rs_memory_schedule_footprints(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
-                                                  out, 4096, C.byref(n)))
-    return list(out[: n.value])
-
-
-def memory_schedule_level(ab: RoutingPlan, level: int, n_gpus: int = 1):
-    """(bands, groups) of a schedule level of the n_gpus ladder (groups -1: rounds)."""
-    b, g = C.c_int(), C.c_int()
-    A.check(A.lib().rs_memory_schedule_level(ab.h, n_gpus, level, C.byref(b), C.byref(g)))
-    return b.value, g.value
-
-
-def _arena_multi(cls, ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, device: int,
-                 cap_bytes: int = 0, chunk_bytes: int = 0, with_grads: bool = False, groups: int = 0,
-                 bands: int = 1) -> "Arena":
-    self = cls.__new__(cls)
-    h = C.c_void_p()
-    A.check(A.lib().rs_arena_create_multi(ab.h, ba.h if ba else None, n_gpus, gpu, device, cap_bytes, chunk_bytes,
-                                          int(with_grads), groups, bands, C.byref(h)))
-    self.h, self.ab, self.ba = h.value, ab, ba
-    return self
-
-
-def _arena_export(self):
-    p_fds, n, p_t, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
-    A.check(A.lib().rs_arena_export(self.h, C.byref(p_fds), C.byref(n), C.byref(p_t), C.byref(ln)))
-    fds = [p_fds[i] for i in range(n.value)]
-    table = C.string_at(p_t.value, ln.value)
-    A.lib().rs_free(C.cast(p_fds, C.c_void_p))
-    A.lib().rs_free(p_t)
-    return fds, table
-
-
-def _arena_import(self, fds: Sequence[int], table: bytes) -> None:
-    arr = (C.c_int * max(1, len(fds)))(*fds)
-    A.check(A.lib().rs_arena_import(self.h, arr, len(fds), table, len(table)))
-
-
-Arena.multi = classmethod(_arena_multi)
-Arena.export = _arena_export
-Arena.import_peer = _arena_import
-
-
-def _exec_num_stages(self) -> int:
-    n = C.c_int()
-    A.check(A.lib().rs_exec_num_stages(self.h, C.byref(n)))
-    return n.value
-
-
-def _exec_run_stage(self, stage: int, stream: int = 0) -> int:
-    n = C.c_int()
-    A.check(A.lib().rs_exec_run_stage(self.h, stage, C.c_void_p(stream), C.byref(n)))
-    return n.value
-
-
-Executor.num_stages = _exec_num_stages
-Executor.run_stage = _exec_run_stage
-
-
-def _exec_bcast_groups(self) -> List[A.BcastGroup_t]:
-    """Broadcast groups of this plan and placement (identical on every rank)."""
-    n = C.c_int()
-    A.check(A.lib().rs_exec_bcast_groups(self.h, None, 0, C.byref(n)))
-    arr = (A.BcastGroup_t * max(1, n.value))()
-    A.check(A.lib().rs_exec_bcast_groups(self.h, arr, n.value, C.byref(n)))
-    return list(arr[: n.value])
-
-
-def _exec_set_multicast(self, group_id: int, mc_va: int) -> None:
-    A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
-
-
-def _exec_read(self, side: int, rank: int, buf: int, offset: int, nbytes: int, stream: int = 0) -> bytes:
-    """Read `nbytes` of a buffer back to the host (synchronous on `stream`)."""
-    out = C.create_string_buffer(nbytes)
-    A.check(A.lib().rs_exec_read(self.h, side, rank, buf, offset, out, nbytes, C.c_void_p(stream)))
-    return out.raw
-
-
-Executor.read = _exec_read
-Executor.bcast_groups = _exec_bcast_groups
-Executor.set_multicast = _exec_set_multicast
-
-
-def _arena_bind_size(self, layout: int, rank: int, buf: int) -> int:
-    n = C.c_int64()
-    A.check(A.lib().rs_arena_bind_size(self.h, layout, rank, buf, C.byref(n)))
-    return n.value
-
-
-Arena.bind_size = _arena_bind_size
-
-
 class Multicast:
     """NVLS multicast object (rs_mc_*): created by the root, imported by the members."""
 
@@ -556,7 +431,7 @@ class Multicast:
     def add_device(self, device: int) -> None:
         A.check(A.lib().rs_mc_add_device(self.h, device))
 
-    def bind_arena(self, arena: "Arena", layout: int, rank: int, buf: int) -> None:
+    def bind_arena(self, arena: Arena, layout: int, rank: int, buf: int) -> None:
         A.check(A.lib().rs_mc_bind_arena(self.h, arena.h, layout, rank, buf))
 
     def bind_vmm(self, buf: "VmmBuffer", mc_offset: int = 0) -> None:
@@ -568,7 +443,7 @@ class Multicast:
         return va.value
 
     def close(self) -> None:
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_mc_destroy(self.h)
             self.h = None
 
@@ -604,12 +479,113 @@ class VmmBuffer:
         return fd.value
 
     def close(self) -> None:
-        if getattr(self, "h", None) and A is not None and A._lib is not None:
+        if getattr(self, "h", None) and _alive():
             A.lib().rs_vmm_free(self.h)
             self.h = None
 
     def __del__(self):
         self.close()
+
+
+# ---- schedule ------------------------------------------------------
+
+def xor_peer(i: int, s: int, n: int) -> int:
+    """Peer(i, s) = i XOR s, or -1 when outside the device set (SPEC.md:302-310)."""
+    return A.lib().rs_xor_peer(i, s, n)
+
+
+def memory_aware_chunk(steps: Sequence[int], costs: Sequence[int], mem_avail: Sequence[int]):
+    """MemoryAwareChunk (PAPER.md:696-717): returns (stages as lists of steps, budget)."""
+    n = len(steps)
+    st = (C.c_int * max(1, n))(*steps)
+    co = (C.c_int64 * max(1, n))(*costs)
+    av = (C.c_int64 * max(1, len(mem_avail)))(*mem_avail)
+    out = (C.c_int * max(1, n))()
+    budget = C.c_int64()
+    A.check(A.lib().rs_memory_aware_chunk(st, co, n, av, len(mem_avail), out, C.byref(budget)))
+    stages: List[List[int]] = []
+    for k in range(n):
+        g = out[k]
+        while len(stages) <= g:
+            stages.append([])
+        stages[g].append(steps[k])
+    return stages, budget.value
+
+
+# ---- host-only memory plans (arena.hpp) ----------------------------------------------
+
+def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False,
+                n_gpus: int = 1, gpu: int = 0, groups: int = 0, bands: int = 1):
+    """Host-only arena plan of the buffers `gpu` hosts: (stats, simulated violations,
+    stage orders over units rank * bands + band); `groups` coarsens the unit order
+    (0 = one group per unit, -1 = rounds), `bands` splits destination ranks into layer bands."""
+    st, viol = A.ArenaStats_t(), C.c_int64()
+    oa, ob = (C.c_int * 65536)(), (C.c_int * 65536)()
+    A.check(A.lib().rs_memory_plan_ex(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, groups,
+                                      bands, C.byref(st), C.byref(viol), oa, ob, 65536))
+    return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
+
+
+def memory_min_groups(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
+                      chunk_bytes: int = 0, with_grads: bool = False):
+    """(fewest stage groups, one band, whose plan fits cap_bytes on `gpu` or -1, physical bytes)."""
+    g, phys = C.c_int(), C.c_int64()
+    A.check(A.lib().rs_memory_min_groups(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
+                                         cap_bytes, C.byref(g), C.byref(phys)))
+    return g.value, phys.value
+
+
+def memory_schedule(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
+                    chunk_bytes: int = 0, with_grads: bool = False):
+    """(first schedule level that fits cap_bytes on `gpu` or -1, its physical bytes)."""
+    lv, phys = C.c_int(), C.c_int64()
+    A.check(A.lib().rs_memory_schedule(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, cap_bytes,
+                                       C.byref(lv), C.byref(phys)))
+    return lv.value, phys.value
+
+
+def memory_schedule_footprints(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int,
+                               chunk_bytes: int = 0, with_grads: bool = False) -> List[int]:
+    """Physical bytes `gpu` needs at every level of the schedule ladder."""
+    n = C.c_int()
+    out = (C.c_int64 * 4096)()
+    A.check(A.lib().rs_memory_schedule_footprints(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
+                                                  out, 4096, C.byref(n)))
+    return list(out[: n.value])
+
+
+def memory_schedule_level(ab: RoutingPlan, level: int, n_gpus: int = 1):
+    """(bands, groups) of a schedule level of the n_gpus ladder (groups -1: rounds)."""
+    b, g = C.c_int(), C.c_int()
+    A.check(A.lib().rs_memory_schedule_level(ab.h, n_gpus, level, C.byref(b), C.byref(g)))
+    return b.value, g.value
+
+
+# ---- process plumbing: descriptor exchange, peer access --------------------------------
+
+def fdx_listen(name: str) -> int:
+    s = C.c_int()
+    A.check(A.lib().rs_fdx_listen(name.encode(), C.byref(s)))
+    return s.value
+
+
+def fdx_send(peer: str, fds: Sequence[int], payload: bytes) -> None:
+    arr = (C.c_int * max(1, len(fds)))(*fds)
+    A.check(A.lib().rs_fdx_send(peer.encode(), arr, len(fds), payload, len(payload)))
+
+
+def fdx_recv(sock: int):
+    p_fds, n, p_pl, ln = C.POINTER(C.c_int)(), C.c_int(), C.c_void_p(), C.c_size_t()
+    A.check(A.lib().rs_fdx_recv(sock, C.byref(p_fds), C.byref(n), C.byref(p_pl), C.byref(ln)))
+    fds = [p_fds[i] for i in range(n.value)]
+    payload = C.string_at(p_pl.value, ln.value) if ln.value else b""
+    A.lib().rs_free(C.cast(p_fds, C.c_void_p))
+    A.lib().rs_free(p_pl)
+    return fds, payload
+
+
+def fdx_close(fd: int) -> None:
+    A.lib().rs_fdx_close(fd)
 
 
 def enable_peer_access(device: int, peer: int) -> None:
