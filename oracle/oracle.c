@@ -1400,6 +1400,7 @@ or_state* or_state_create(const or_scenario* s, int which, int with_grads, char*
         int64_t bo = 0;
         for (int i = 0; i < ns; ++i) {
             seg_t* g = rs_seg(R, i);
+            bo = (bo + 15) / 16 * 16; /* segments start 16-B aligned */
             R->seg_byte_off[i] = bo;
             bo += (g->hi - g->lo) * s->t[g->t].dtype;
         }

@@ -197,6 +197,9 @@ Side build_side(const ModelSpace& space, const ParallelConfig& cfg) {
         std::int64_t bytes = 0, elems = 0;
         for (std::vector<Seg>* list : {&dense, &expert})
             for (Seg& s : *list) {
+                // every segment starts 16-B aligned: natural alignment for any dtype and
+                // full 16-B vectors for the copy kernels (no padding at these models' shapes)
+                bytes = (bytes + 15) / 16 * 16;
                 s.param_byte_off = bytes;
                 s.elem_off = elems;
                 bytes += (s.local_hi - s.local_lo) * space.entries()[static_cast<size_t>(s.tensor)].spec.dtype_bytes;

@@ -289,3 +289,37 @@ def random_cfg(rng: random.Random, model: Model, max_world: int = 16, zero: Opti
         return Cfg(dp=dp, tp=tp, pp=pp, ep=ep, zero=bool(rng.random() < 0.5) if zero is None else zero,
                    order=order)
     return Cfg()
+
+
+def ragged_model() -> Model:
+    """Edge-case model: byte rows of 1, 3, 6, 12, 14, 20 B (every alignment class) and odd
+    element counts, so ZeRO shard boundaries fall mid-row."""
+    return Model("ragged", [
+        Tensor("emb", (12, 7), 0, tp=0, dtype=2),
+        Tensor("w1", (10, 6), 0, tp=1, dtype=2),
+        Tensor("n1", (7,), 0, dtype=4),
+        Tensor("b1", (4, 3), 1, tp=0, dtype=1),
+        Tensor("w2", (6, 5), 1, tp=0, dtype=4),
+        Tensor("n2", (9,), 1, dtype=2),
+        Tensor("head", (8, 10), 1, tp=0, dtype=2),
+    ], layers=2)
+
+
+def edge_scenarios() -> List[Scenario]:
+    """Identity transitions (everything retained), ragged widths, odd ZeRO boundaries, a
+    single-tensor model, join/leave world maps, migrated gradients, one scalar word."""
+    m = ragged_model()
+    out = [
+        Scenario(m, Cfg(tp=2), Cfg(tp=2), name="edge.identity-tp2"),
+        Scenario(m, Cfg(dp=2, zero=True), Cfg(dp=2, zero=True), name="edge.identity-zero"),
+        Scenario(m, Cfg(tp=2), Cfg(dp=2), name="edge.ragged-tp2-to-dp2"),
+        Scenario(m, Cfg(dp=2, zero=True), Cfg(tp=2, zero=True), name="edge.ragged-dp2-zero-to-tp2"),
+        Scenario(m, Cfg(dp=3, zero=True), Cfg(dp=2, zero=True), name="edge.ragged-dp3-zero-to-dp2-zero"),
+        Scenario(m, Cfg(pp=2), Cfg(tp=2), grads="migrate", name="edge.ragged-pp2-to-tp2-grads"),
+        Scenario(Model("one", [Tensor("w", (16, 8), 0, tp=0, dtype=2)]), Cfg(tp=4), Cfg(tp=2),
+                 name="edge.single-tensor"),
+        Scenario(m, Cfg(dp=2, zero=True), Cfg(dp=3, zero=True), world_src=[0, 2], world_dst=[1, 2, 3],
+                 name="edge.join-leave"),
+        Scenario(m, Cfg(tp=2), Cfg(tp=2), scalar_words=1, name="edge.scalars-one-word"),
+    ]
+    return out

@@ -105,10 +105,17 @@ def campaign_scenarios(n: int = 80, seed: int = 2605):
 
 
 def main() -> None:
+    """Regenerate every group, or with `--append GROUP` add/replace one group in place."""
     if not pyoracle.ref_available():
         subprocess.check_call(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"])
+    all_groups = {"kat": kat_scenarios, "baseline": baseline_scenarios, "campaign": campaign_scenarios,
+                  "edge": S.edge_scenarios}
     entries = []
-    groups = [("kat", kat_scenarios()), ("baseline", baseline_scenarios()), ("campaign", campaign_scenarios())]
+    groups = [(g, f()) for g, f in all_groups.items()]
+    if len(sys.argv) > 2 and sys.argv[1] == "--append":
+        with open(os.path.join(OUT, "ref_plans.json")) as f:
+            entries = [e for e in json.load(f)["entries"] if e["group"] != sys.argv[2]]
+        groups = [(sys.argv[2], all_groups[sys.argv[2]]())]
     for group, scs in groups:
         for sc in scs:
             text = sc.text()
