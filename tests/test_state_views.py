@@ -12,7 +12,9 @@ from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.state import RankState, buffer_bytes, model_tensors  # noqa: E402
 
 CASES = [("config1", lambda: S.config1()), ("config1-zero-ext", lambda: S.config1(zero=True)),
-         ("config2-L1", lambda: S.config2(1)), ("config4-L1", lambda: S.config4(1))]
+         ("config2-L1", lambda: S.config2(1)), ("config4-L1", lambda: S.config4(1)),
+         ("ragged-dp2-zero-to-tp2", lambda: [x for x in S.edge_scenarios() if x.name == "edge.ragged-dp2-zero-to-tp2"][0]),
+         ("ragged-pp2-to-tp2", lambda: [x for x in S.edge_scenarios() if x.name == "edge.ragged-pp2-to-tp2-grads"][0])]
 
 
 def _plan(sc):
@@ -39,16 +41,17 @@ def test_views_tile_the_buffers(name, make):
                 if v is not None:
                     assert v.numel() == b - a and 0 <= a < b <= p.numel()
                     opieces.append((v.storage_offset(), v.numel()))
-            assert _tiles(pieces, nbytes[A.BUF_PARAM]), "param views must tile the buffer"
+            assert _tiles(pieces, nbytes[A.BUF_PARAM], align=16), "param views must tile the buffer"
             assert _tiles(opieces, st.geom.optim_len), "optimizer slices must tile the shard"
 
 
-def _tiles(pieces, total):
+def _tiles(pieces, total, align=1):
+    """Pieces cover [0, total) in order, each starting at the next `align`-aligned offset."""
     pos = 0
     for off, n in sorted(pieces):
-        if off != pos:
+        if off != (pos + align - 1) // align * align:
             return False
-        pos += n
+        pos = off + n
     return pos == total
 
 
@@ -56,8 +59,11 @@ def _full_state(sc, seed):
     g = torch.Generator().manual_seed(seed)
     full = {}
     for t in sc.model.tensors:
-        dt = torch.bfloat16 if t.dtype == 2 else torch.float32
-        full[t.id] = {"param": torch.randn(t.shape, generator=g).to(dt),
+        if t.dtype == 1:
+            param = torch.randint(0, 256, t.shape, generator=g, dtype=torch.uint8)
+        else:
+            param = torch.randn(t.shape, generator=g).to(torch.bfloat16 if t.dtype == 2 else torch.float32)
+        full[t.id] = {"param": param,
                       "master": torch.randn(t.shape, generator=g), "m": torch.randn(t.shape, generator=g),
                       "v": torch.rand(t.shape, generator=g)}
     return full
@@ -95,15 +101,22 @@ def test_torch_state_survives_transition(name, make):
     sc = make()
     plan = _plan(sc)
     full = _full_state(sc, 1234)
-    ex = Executor(plan)
-    src = [RankState.alloc(plan, A.SIDE_SRC, r) for r in range(sc.src.world())]
-    dst = [RankState.alloc(plan, A.SIDE_DST, r) for r in range(sc.dst.world())]
+    grads = sc.grads == "migrate"
+    ex = Executor(plan, with_grads=grads)
+    src = [RankState.alloc(plan, A.SIDE_SRC, r, with_grads=grads) for r in range(sc.src.world())]
+    dst = [RankState.alloc(plan, A.SIDE_DST, r, with_grads=grads) for r in range(sc.dst.world())]
     for st in src + dst:
         st.bind(ex)
     for st in src:
         _load(st, full)
+        if grads:
+            for tid in st.seg_of:
+                st.grad(tid).copy_(full[tid]["master"][st.box(tid)])
     ex.prepare()
     ex.run()
     torch.cuda.synchronize()
     bad = [b for st in dst for b in _check(st, full)]
+    if grads:
+        bad += [(st.rank, tid, "grad") for st in dst for tid in st.seg_of
+                if not torch.equal(st.grad(tid).cpu(), full[tid]["master"][st.box(tid)])]
     assert not bad, bad[:10]
