@@ -28,8 +28,9 @@ def main():
     seed = 0xBEEF
     failures = 0
     scenarios = [S.config2(layers), S.config4(1), S.config3(2)[0], S.config3(2)[1]]
+    scenarios += [sc for sc in S.edge_scenarios() if sc.grads == "drop"]  # ragged, identity, join/leave
     for sc in scenarios:
-        ab = RoutingPlan.from_scenario(sc)
+        ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
         fwd = Transition(ab, world, rank, local, alloc=False)
         bwd = Transition(ba, world, rank, local, alloc=False)
