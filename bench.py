@@ -396,7 +396,10 @@ def run_ours(args):
         # GPU planner vs the host sweep; the reference's own O(n*m) planner needs hours at L=32
         g_ms, g_runs = ab.expand_timed(dev)
         h_ms, h_runs = ab.expand_timed(-1)
-        planner = {"gpu_planner_ms": round(g_ms, 3), "gpu_planner_what": "kernels: count + CUB scan + write",
+        b_ms, b_n, b_eq = ab.box_routes_timed(dev)
+        planner = {"gpu_planner_ms": round(g_ms + b_ms, 3),
+                   "gpu_planner_what": "kernels: ZeRO runs (count + CUB scan + write) + box intersections",
+                   "gpu_box_kernel_ms": round(b_ms, 3), "gpu_box_transfers": b_n, "gpu_boxes_equal_host": b_eq,
                    "host_sweep_ms": round(h_ms, 2), "runs": g_runs,
                    "same_run_count_as_host": g_runs == h_runs, "plan_build_s": round(plan_s, 4)}
         try:

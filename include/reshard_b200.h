@@ -175,6 +175,9 @@ int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stat
  * injection: box transfers are indexed first, then ZeRO runs). */
 int rs_plan_validate(const rs_plan_t* p, int64_t drop, char** report, size_t* len, int64_t* n_violations);
 /* host expansion of the ZeRO runs with the GPU planner's per-row algorithm (tests) */
+/* the GPU box planner (batched (dst rank, tensor, src rank) intersections) on `device`:
+ * kernel milliseconds, number of box transfers, and whether they equal the host plan's */
+int rs_plan_box_routes_timed(const rs_plan_t* p, int device, double* ms, int64_t* n_boxes, int* equal_host);
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len);
 /* expand the ZeRO optimizer transfers (1.84 M runs for Llama-3-8B) and report the
  * time: device >= 0 -> GPU planner kernels (ms of device time), < 0 -> host sweep */

@@ -94,6 +94,12 @@ class RoutingPlan:
         A.check(A.lib().rs_plan_expand_timed(self.h, device, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def box_routes_timed(self, device: int = 0):
+        """(kernel ms, box transfers, equal to the host plan) of the GPU box planner."""
+        ms, n, eq = C.c_double(), C.c_int64(), C.c_int()
+        A.check(A.lib().rs_plan_box_routes_timed(self.h, device, C.byref(ms), C.byref(n), C.byref(eq)))
+        return ms.value, n.value, bool(eq.value)
+
     def validate(self, drop: int = -1) -> List[str]:
         """validate_plan: violation lines, empty on success."""
         p, n, k = C.c_void_p(), C.c_size_t(), C.c_int64()

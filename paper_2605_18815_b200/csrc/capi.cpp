@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -22,6 +23,7 @@
 namespace reshard {
 namespace gpuplan {
 std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device, double* kernel_ms);
+std::vector<core::BoxXfer> box_routes_gpu(const core::PlanCore& P, int device, double* kernel_ms);
 }
 }  // namespace reshard
 
@@ -305,7 +307,9 @@ int rs_plan_summary(const rs_plan_t* p, rs_plan_summary_t* out) {
 
 int rs_plan_dump(const rs_plan_t* p, int device, char** out, size_t* len) {
     return guarded([&] {
-        *out = dup_string(core::dump(p->core, expand(p, device)), len);
+        *out = dup_string(device >= 0 ? core::dump(p->core, gpuplan::box_routes_gpu(p->core, device, nullptr), expand(p, device))
+                                      : core::dump(p->core, expand(p, device)),
+                          len);
         return RS_OK;
     });
 }
@@ -338,6 +342,23 @@ int rs_plan_expand_timed(const rs_plan_t* p, int device, double* ms, int64_t* n_
     });
 }
 
+int rs_plan_box_routes_timed(const rs_plan_t* p, int device, double* ms, int64_t* n_boxes, int* equal_host) {
+    return guarded([&] {
+        double t = 0;
+        const std::vector<core::BoxXfer> v = gpuplan::box_routes_gpu(p->core, device, &t);
+        *ms = t;
+        *n_boxes = static_cast<int64_t>(v.size());
+        bool eq = v.size() == p->core.box.size();
+        for (size_t i = 0; eq && i < v.size(); ++i) {
+            const core::BoxXfer &a = v[i], &b = p->core.box[i];
+            eq = a.kind == b.kind && a.tensor == b.tensor && a.src == b.src && a.dst == b.dst && a.count == b.count &&
+                 a.bytes == b.bytes && std::equal(a.lo, a.lo + 4, b.lo) && std::equal(a.hi, a.hi + 4, b.hi);
+        }
+        *equal_host = eq ? 1 : 0;
+        return RS_OK;
+    });
+}
+
 int rs_plan_dump_rows_host(const rs_plan_t* p, char** out, size_t* len) {
     return guarded([&] {
         *out = dup_string(core::dump(p->core, core::expand_flat_rows_host(p->core)), len);
@@ -349,22 +370,24 @@ int rs_plan_transfers(const rs_plan_t* p, int device, rs_transfer_t** out, int64
     return guarded([&] {
         const core::PlanCore& c = p->core;
         const std::vector<core::FlatXfer> flat = expand(p, device);
-        const size_t total = c.box.size() + flat.size();
+        // device >= 0: both planner halves on the GPU (box intersections + ZeRO runs)
+        const std::vector<core::BoxXfer> boxes = device >= 0 ? gpuplan::box_routes_gpu(c, device, nullptr) : c.box;
+        const size_t total = boxes.size() + flat.size();
         rs_transfer_t* arr = static_cast<rs_transfer_t*>(std::calloc(total ? total : 1, sizeof(rs_transfer_t)));
         if (!arr) throw std::bad_alloc();
         size_t bi = 0, fi = 0, k = 0;
-        while (bi < c.box.size() || fi < flat.size()) {
+        while (bi < boxes.size() || fi < flat.size()) {
             bool take_box;
-            if (bi == c.box.size()) take_box = false;
+            if (bi == boxes.size()) take_box = false;
             else if (fi == flat.size()) take_box = true;
             else {
-                const auto& b = c.box[bi];
+                const auto& b = boxes[bi];
                 const auto& f = flat[fi];
                 take_box = b.src != f.src ? b.src < f.src : b.dst != f.dst ? b.dst < f.dst : b.kind < 1;
             }
             rs_transfer_t& t = arr[k++];
             if (take_box) {
-                const auto& b = c.box[bi++];
+                const auto& b = boxes[bi++];
                 t.kind = b.kind;
                 t.tensor = b.tensor;
                 t.flat = 0;

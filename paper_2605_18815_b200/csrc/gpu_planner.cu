@@ -4,6 +4,15 @@
 // :360-396) — which takes hours on the reference's O(n*m) interval lists at
 // Llama-3-8B scale.
 //
+// Boxes (params, grads, replicated optimizer): one thread per (dst rank j, tensor t,
+// src rank k) intersects the two ranks' boxes of t — the batched hyper-rectangle
+// intersection over all (old shard, new shard) pairs. The reference splits
+// D_j \ S_own(j) at the source projection grid and collects the candidates holding each
+// cell (routing.hpp:197-279); since the source positions partition every tensor, its
+// cells are exactly the non-empty D_j ∩ S_p over source positions p other than own(j)'s,
+// with the ranks sharing position p as candidates. The lowest rank of a
+// position emits the cell; resolve_peers' proximity rule picks the source on the host.
+//
 // One thread per tensor row of every triple. A row yields 0..2 runs
 // ((J ∩ K) \ I, stair.hpp); it continues the previous run when its first piece
 // starts exactly where the previous row's last piece ended (same src/dst), which is
@@ -94,7 +103,180 @@ __global__ void write_kernel(const stair::Triple* __restrict__ T, const long lon
     }
 }
 
+struct DevBox {
+    long long lo[4], hi[4];
+    int valid;
+};
+
+struct DevCell {
+    long long lo[4], hi[4];
+    unsigned long long cands;  // source ranks holding the cell (bit k)
+    int j, t;
+};
+
+__device__ __forceinline__ bool same_box(const DevBox& a, const DevBox& b, int nd) {
+    for (int d = 0; d < nd; ++d)
+        if (a.lo[d] != b.lo[d] || a.hi[d] != b.hi[d]) return false;
+    return true;
+}
+
+__global__ void box_cells_kernel(const DevBox* __restrict__ S, const DevBox* __restrict__ D, const int* __restrict__ nd_of,
+                                 const int* __restrict__ own, int ns, int ndst, int nt, DevCell* __restrict__ out,
+                                 unsigned long long* __restrict__ count) {
+    const long long total = static_cast<long long>(ndst) * nt * ns;
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total; g += (long long)gridDim.x * blockDim.x) {
+        const int k = static_cast<int>(g % ns);
+        const int t = static_cast<int>((g / ns) % nt);
+        const int j = static_cast<int>(g / (static_cast<long long>(ns) * nt));
+        const DevBox& db = D[static_cast<long long>(j) * nt + t];
+        const DevBox& sb = S[static_cast<long long>(k) * nt + t];
+        if (!db.valid || !sb.valid) continue;
+        const int nd = nd_of[t];
+        bool lowest = true;  // k is the lowest rank of its source position
+        unsigned long long cands = 0;
+        for (int q = 0; q < ns; ++q) {
+            const DevBox& x = S[static_cast<long long>(q) * nt + t];
+            if (x.valid && same_box(x, sb, nd)) {
+                if (q < k) lowest = false;
+                cands |= 1ull << q;
+            }
+        }
+        if (!lowest) continue;
+        const int o = own[j];
+        if (o >= 0 && S[static_cast<long long>(o) * nt + t].valid && same_box(S[static_cast<long long>(o) * nt + t], sb, nd))
+            continue;  // retained on the device, not moved
+        DevCell c;
+        bool empty = false;
+        for (int d = 0; d < nd; ++d) {
+            c.lo[d] = db.lo[d] > sb.lo[d] ? db.lo[d] : sb.lo[d];
+            c.hi[d] = db.hi[d] < sb.hi[d] ? db.hi[d] : sb.hi[d];
+            empty = empty || c.lo[d] >= c.hi[d];
+        }
+        if (empty) continue;
+        for (int d = nd; d < 4; ++d) c.lo[d] = c.hi[d] = 0;
+        c.cands = cands;
+        c.j = j;
+        c.t = t;
+        out[atomicAdd(count, 1ull)] = c;
+    }
+}
+
 }  // namespace
+
+std::vector<core::BoxXfer> box_routes_gpu(const core::PlanCore& P, int device, double* kernel_ms) {
+    const int ns = P.src_cfg.world_size(), ndst = P.dst_cfg.world_size();
+    const int nt = P.ntensors();
+    if (ns > 64) throw ConfigError("GPU box planner: more than 64 source ranks");
+    if (P.opts.balance_fanout) {  // the round-robin cursor follows the reference's pending order
+        if (kernel_ms) *kernel_ms = 0;
+        return P.box;
+    }
+    std::vector<DevBox> S(static_cast<size_t>(ns) * nt), D(static_cast<size_t>(ndst) * nt);
+    auto fill = [&](const core::Side& side, std::vector<DevBox>& v) {
+        for (size_t r = 0; r < side.ranks.size(); ++r)
+            for (int t = 0; t < nt; ++t) {
+                DevBox& b = v[r * static_cast<size_t>(nt) + static_cast<size_t>(t)];
+                const int si = side.ranks[r].seg_of[static_cast<size_t>(t)];
+                b.valid = si >= 0;
+                for (int d = 0; d < 4; ++d) b.lo[d] = b.hi[d] = 0;
+                if (si >= 0)
+                    for (int d = 0; d < 4; ++d) {
+                        b.lo[d] = side.ranks[r].segs[static_cast<size_t>(si)].blo[d];
+                        b.hi[d] = side.ranks[r].segs[static_cast<size_t>(si)].bhi[d];
+                    }
+            }
+    };
+    fill(P.src, S);
+    fill(P.dst, D);
+    std::vector<int> nd_of(static_cast<size_t>(nt)), own(static_cast<size_t>(ndst), -1);
+    for (int t = 0; t < nt; ++t) nd_of[static_cast<size_t>(t)] = static_cast<int>(P.space->entries()[static_cast<size_t>(t)].spec.shape.size());
+    for (int j = 0; j < ndst; ++j) own[static_cast<size_t>(j)] = P.wm.src_rank_of(P.wm.dst_phys[static_cast<size_t>(j)]);
+    const long long total = static_cast<long long>(ndst) * nt * ns;
+    std::vector<DevCell> cells;
+    {
+        RS_CUDA_P(cudaSetDevice(device));
+        DevBox *dS = nullptr, *dD = nullptr;
+        int *dNd = nullptr, *dOwn = nullptr;
+        DevCell* dOut = nullptr;
+        unsigned long long* dCount = nullptr;
+        cudaStream_t st = nullptr;
+        cudaEvent_t e0, e1;
+        RS_CUDA_P(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        RS_CUDA_P(cudaEventCreate(&e0));
+        RS_CUDA_P(cudaEventCreate(&e1));
+        auto release = [&] {
+            cudaFree(dS), cudaFree(dD), cudaFree(dNd), cudaFree(dOwn), cudaFree(dOut), cudaFree(dCount);
+            cudaEventDestroy(e0), cudaEventDestroy(e1);
+            cudaStreamDestroy(st);
+        };
+        try {
+            RS_CUDA_P(cudaMalloc(&dS, S.size() * sizeof(DevBox)));
+            RS_CUDA_P(cudaMalloc(&dD, D.size() * sizeof(DevBox)));
+            RS_CUDA_P(cudaMalloc(&dNd, nd_of.size() * sizeof(int)));
+            RS_CUDA_P(cudaMalloc(&dOwn, own.size() * sizeof(int)));
+            RS_CUDA_P(cudaMalloc(&dOut, static_cast<size_t>(total > 0 ? total : 1) * sizeof(DevCell)));
+            RS_CUDA_P(cudaMalloc(&dCount, sizeof(unsigned long long)));
+            RS_CUDA_P(cudaMemcpyAsync(dS, S.data(), S.size() * sizeof(DevBox), cudaMemcpyHostToDevice, st));
+            RS_CUDA_P(cudaMemcpyAsync(dD, D.data(), D.size() * sizeof(DevBox), cudaMemcpyHostToDevice, st));
+            RS_CUDA_P(cudaMemcpyAsync(dNd, nd_of.data(), nd_of.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            RS_CUDA_P(cudaMemcpyAsync(dOwn, own.data(), own.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+            RS_CUDA_P(cudaMemsetAsync(dCount, 0, sizeof(unsigned long long), st));
+            const int threads = 256;
+            const long long want = (total + threads - 1) / threads;
+            const int blocks = static_cast<int>(want < 148 * 16 ? (want > 0 ? want : 1) : 148 * 16);
+            RS_CUDA_P(cudaEventRecord(e0, st));
+            box_cells_kernel<<<blocks, threads, 0, st>>>(dS, dD, dNd, dOwn, ns, ndst, nt, dOut, dCount);
+            RS_CUDA_P(cudaEventRecord(e1, st));
+            RS_CUDA_P(cudaGetLastError());
+            unsigned long long n = 0;
+            RS_CUDA_P(cudaMemcpyAsync(&n, dCount, sizeof n, cudaMemcpyDeviceToHost, st));
+            RS_CUDA_P(cudaStreamSynchronize(st));
+            cells.resize(static_cast<size_t>(n));
+            RS_CUDA_P(cudaMemcpyAsync(cells.data(), dOut, static_cast<size_t>(n) * sizeof(DevCell), cudaMemcpyDeviceToHost, st));
+            RS_CUDA_P(cudaStreamSynchronize(st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (kernel_ms) *kernel_ms = ms;
+        } catch (...) {
+            release();
+            throw;
+        }
+        release();
+    }
+    // resolve_peers' proximity rule (routing.hpp:360-396): the first candidate on the
+    // destination's node, else the lowest rank; then every kind the plan moves as boxes
+    std::vector<core::BoxXfer> out;
+    const bool grads = P.opts.gradients == GradientPolicy::Migrate;
+    const bool optim_boxes = !P.src_cfg.zero_enabled;
+    out.reserve(cells.size() * (1 + grads + optim_boxes));
+    for (const DevCell& c : cells) {
+        const int dphys = P.wm.dst_phys[static_cast<size_t>(c.j)];
+        int chosen = -1;
+        for (int k = 0; k < ns && chosen < 0; ++k)
+            if ((c.cands >> k) & 1ull)
+                if (P.topo.same_node(P.wm.src_phys[static_cast<size_t>(k)], dphys)) chosen = k;
+        for (int k = 0; k < ns && chosen < 0; ++k)
+            if ((c.cands >> k) & 1ull) chosen = k;
+        core::BoxXfer x;
+        x.tensor = c.t;
+        x.count = 1;
+        for (int d = 0; d < 4; ++d) {
+            x.lo[d] = c.lo[d];
+            x.hi[d] = c.hi[d];
+        }
+        for (int d = 0; d < nd_of[static_cast<size_t>(c.t)]; ++d) x.count *= c.hi[d] - c.lo[d];
+        x.src = chosen;
+        x.dst = c.j;
+        for (int kind : {0, 2, 1}) {
+            if ((kind == 2 && !grads) || (kind == 1 && !optim_boxes)) continue;
+            x.kind = kind;
+            x.bytes = x.count * core::payload_width(*P.space, kind, c.t);
+            out.push_back(x);
+        }
+    }
+    std::sort(out.begin(), out.end(), [&](const core::BoxXfer& a, const core::BoxXfer& b) { return core::box_xfer_less(P, a, b); });
+    return out;
+}
 
 /// Expand on `device`. Runs of D2-overridden destinations come from the host plan.
 std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device, double* kernel_ms) {

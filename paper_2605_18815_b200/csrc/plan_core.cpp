@@ -139,15 +139,6 @@ std::int64_t triple_count(const stair::Triple& T) {
     return n;
 }
 
-int payload_width(const ModelSpace& space, int kind, int tensor) {
-    switch (kind) {
-        case 0: return space.entries()[static_cast<size_t>(tensor)].spec.dtype_bytes;
-        case 1: return kOptimStateBytes;
-        case 2: return kGradBytes;
-        default: return kScalarWordBytes;
-    }
-}
-
 Box box_of(const Seg& s, int nd) {
     Box b;
     b.dims.resize(static_cast<size_t>(nd));
@@ -164,6 +155,28 @@ struct Pending {
 };
 
 }  // namespace
+
+int payload_width(const ModelSpace& space, int kind, int tensor) {
+    switch (kind) {
+        case 0: return space.entries()[static_cast<size_t>(tensor)].spec.dtype_bytes;
+        case 1: return kOptimStateBytes;
+        case 2: return kGradBytes;
+        default: return kScalarWordBytes;
+    }
+}
+
+bool box_xfer_less(const PlanCore& P, const BoxXfer& a, const BoxXfer& b) {
+    if (a.src != b.src) return a.src < b.src;
+    if (a.dst != b.dst) return a.dst < b.dst;
+    if (a.kind != b.kind) return a.kind < b.kind;
+    if (a.tensor != b.tensor) return P.id_rank[static_cast<size_t>(a.tensor)] < P.id_rank[static_cast<size_t>(b.tensor)];
+    const int nd = static_cast<int>(P.space->entries()[static_cast<size_t>(a.tensor)].spec.shape.size());
+    for (int d = 0; d < nd; ++d) {
+        if (a.lo[d] != b.lo[d]) return a.lo[d] < b.lo[d];
+        if (a.hi[d] != b.hi[d]) return a.hi[d] < b.hi[d];
+    }
+    return false;
+}
 
 Side build_side(const ModelSpace& space, const ParallelConfig& cfg) {
     Side S;
@@ -462,18 +475,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         x.bytes = x.count * payload_width(space, p.kind, p.tensor);
         P.box.push_back(x);
     }
-    std::sort(P.box.begin(), P.box.end(), [&](const BoxXfer& a, const BoxXfer& b) {
-        if (a.src != b.src) return a.src < b.src;
-        if (a.dst != b.dst) return a.dst < b.dst;
-        if (a.kind != b.kind) return a.kind < b.kind;
-        if (a.tensor != b.tensor) return P.id_rank[static_cast<size_t>(a.tensor)] < P.id_rank[static_cast<size_t>(b.tensor)];
-        const int nd = static_cast<int>(space.entries()[static_cast<size_t>(a.tensor)].spec.shape.size());
-        for (int d = 0; d < nd; ++d) {
-            if (a.lo[d] != b.lo[d]) return a.lo[d] < b.lo[d];
-            if (a.hi[d] != b.hi[d]) return a.hi[d] < b.hi[d];
-        }
-        return false;
-    });
+    std::sort(P.box.begin(), P.box.end(), [&](const BoxXfer& a, const BoxXfer& b) { return box_xfer_less(P, a, b); });
 
     // ---- retained boxes (routing.hpp:98 retain = R_src ∩ R_dst), same device
     std::int64_t retained = 0;
@@ -687,10 +689,12 @@ std::vector<FlatXfer> expand_flat_rows_host(const PlanCore& P) {
     return merge_with_d2(P, std::move(out));
 }
 
-std::string dump(const PlanCore& P, const std::vector<FlatXfer>& flat) {
+std::string dump(const PlanCore& P, const std::vector<FlatXfer>& flat) { return dump(P, P.box, flat); }
+
+std::string dump(const PlanCore& P, const std::vector<BoxXfer>& boxes, const std::vector<FlatXfer>& flat) {
     const ModelSpace& space = *P.space;
     std::string out;
-    out.reserve(static_cast<size_t>(P.box.size() + flat.size()) * 56);
+    out.reserve(static_cast<size_t>(boxes.size() + flat.size()) * 56);
     char line[1024];
     auto box_line = [&](const BoxXfer& b) {
         const TensorSpec& ts = space.entries()[static_cast<size_t>(b.tensor)].spec;
@@ -715,17 +719,17 @@ std::string dump(const PlanCore& P, const std::vector<FlatXfer>& flat) {
         if (d1 != d2) return d1 < d2;
         return k1 < k2;
     };
-    while (bi < P.box.size() || fi < flat.size()) {
+    while (bi < boxes.size() || fi < flat.size()) {
         bool take_box;
-        if (bi == P.box.size()) take_box = false;
+        if (bi == boxes.size()) take_box = false;
         else if (fi == flat.size()) take_box = true;
         else {
-            const BoxXfer& b = P.box[bi];
+            const BoxXfer& b = boxes[bi];
             const FlatXfer& f = flat[fi];
             // for equal (src,dst,kind=optim) flat ("" id) sorts before any box id
             take_box = key_less(b.src, b.dst, b.kind, f.src, f.dst, 1);
         }
-        if (take_box) box_line(P.box[bi++]);
+        if (take_box) box_line(boxes[bi++]);
         else flat_line(flat[fi++]);
     }
     return out;

@@ -150,6 +150,13 @@ std::vector<FlatXfer> expand_flat_rows_host(const PlanCore& P);
 /// Reference dump (routing.hpp:86-90 format_transfer lines, canonical order),
 /// given the ZeRO runs (from expand_flat_host or the GPU planner).
 std::string dump(const PlanCore& P, const std::vector<FlatXfer>& flat);
+/// The same with the box transfers given explicitly (e.g. from the GPU planner).
+std::string dump(const PlanCore& P, const std::vector<BoxXfer>& boxes, const std::vector<FlatXfer>& flat);
+
+/// bytes per element of a state kind (param: the tensor's dtype_bytes)
+int payload_width(const ModelSpace& space, int kind, int tensor);
+/// canonical transfer order (routing.hpp:79 transfer_order_less) for box transfers
+bool box_xfer_less(const PlanCore& P, const BoxXfer& a, const BoxXfer& b);
 
 /// Visit the band rectangles of a triple: emit(p[2], r_lo, r_hi, cols[2], n).
 template <class F>

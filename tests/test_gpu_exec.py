@@ -303,3 +303,13 @@ def test_single_process_peer_push():
     line = [x for x in r.stdout.splitlines() if x.startswith("{")]
     assert line, r.stdout[-2000:] + r.stderr[-2000:]
     assert json.loads(line[-1])["verified_mismatches"] == 0
+
+
+def test_gpu_box_planner_equals_host():
+    """The batched (dst rank, tensor, src rank) box intersections on the GPU give exactly
+    the host plan's box transfers (params, grads, replicated optimizer) — the golden test
+    above compares the GPU planner's whole dump with the reference's."""
+    for sc in [S.config2(32), S.config4(4), S.config5(8), S.config1(), S.config3(4)[1]] + S.edge_scenarios():
+        p = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+        ms, n, eq = p.box_routes_timed(0)
+        assert eq, sc.name
