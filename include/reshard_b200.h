@@ -247,6 +247,7 @@ typedef struct {
     int64_t tiles_by_class[5];
     int64_t launches;      /* kernel launches per rs_exec_run */
     int64_t mc_bytes;      /* bytes delivered to peers by NVLS multicast stores */
+    int64_t dup_bytes;     /* replica bytes copied on this GPU by rs_exec_run_dup */
 } rs_exec_stats_t;
 
 /* ---- memory-aware arena (Algorithm 1 FreeObsoleteBuffers / eager free,
@@ -330,6 +331,10 @@ typedef struct {
 int rs_exec_bcast_groups(rs_exec_t* e, rs_bcast_group_t* out, int cap, int* n);
 /* root only; mc_va NULL reverts to per-destination pushes; takes effect at the next prepare */
 int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va);
+/* replica dedup: a region bound for several replica ranks on one GPU crosses NVLink once;
+ * after rs_exec_run on every GPU and a barrier, rs_exec_run_dup copies the other replicas */
+int rs_exec_set_replica_dedup(rs_exec_t* e, int on);
+int rs_exec_run_dup(rs_exec_t* e, void* stream, int* launches);
 
 typedef struct rs_mc rs_mc_t;
 int rs_mc_create(int64_t bytes, int n_devices, rs_mc_t** out);

@@ -71,7 +71,8 @@ class ExecOpts_t(C.Structure):
 
 class ExecStats_t(C.Structure):
     _fields_ = [("local_bytes", C.c_int64), ("remote_bytes", C.c_int64), ("tiles", C.c_int64),
-                ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64), ("mc_bytes", C.c_int64)]
+                ("tiles_by_class", C.c_int64 * 5), ("launches", C.c_int64), ("mc_bytes", C.c_int64),
+                ("dup_bytes", C.c_int64)]
 
 
 RS_MAX_MEMBERS = 64
@@ -224,6 +225,8 @@ def _late_bindings(L):
         ("rs_exec_bcast_groups", [vp, P(BcastGroup_t), C.c_int, P(C.c_int)]),
         ("rs_exec_set_multicast", [vp, C.c_int, vp]),
         ("rs_exec_read", [vp, C.c_int, C.c_int, C.c_int, i64, vp, i64, vp]),
+        ("rs_exec_set_replica_dedup", [vp, C.c_int]),
+        ("rs_exec_run_dup", [vp, vp, P(C.c_int)]),
         ("rs_enable_peer_access", [C.c_int, C.c_int]),
         ("rs_plan_box_routes_timed", [vp, C.c_int, P(C.c_double), P(i64), P(C.c_int)]),
         ("rs_mc_create", [i64, C.c_int, P(vp)]),

@@ -246,6 +246,16 @@ class Executor:
     def set_multicast(self, group_id: int, mc_va: int) -> None:
         A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
 
+    def set_replica_dedup(self, on: bool = True) -> None:
+        """A region bound for several replica ranks on one GPU crosses NVLink once; call
+        run_dup() on every GPU after run() and a cross-GPU barrier."""
+        A.check(A.lib().rs_exec_set_replica_dedup(self.h, int(on)))
+
+    def run_dup(self, stream: int = 0) -> int:
+        n = C.c_int()
+        A.check(A.lib().rs_exec_run_dup(self.h, C.c_void_p(stream), C.byref(n)))
+        return n.value
+
     # ---- synthetic state
     def fill(self, side: int, seed: int, stream: int = 0) -> None:
         A.check(A.lib().rs_exec_fill(self.h, side, seed, C.c_void_p(stream)))

@@ -821,6 +821,7 @@ int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
         for (int i = 0; i < 5; ++i) out->tiles_by_class[i] = s.tiles_by_class[i];
         out->launches = s.launches;
         out->mc_bytes = s.mc_bytes;
+        out->dup_bytes = s.dup_bytes;
         return RS_OK;
     });
 }
@@ -1106,6 +1107,20 @@ int rs_exec_bcast_groups(rs_exec_t* e, rs_bcast_group_t* out, int cap, int* n) {
 int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va) {
     return guarded([&] {
         e->ex->set_multicast(id, mc_va);
+        return RS_OK;
+    });
+}
+
+int rs_exec_set_replica_dedup(rs_exec_t* e, int on) {
+    return guarded([&] {
+        e->ex->set_replica_dedup(on != 0);
+        return RS_OK;
+    });
+}
+
+int rs_exec_run_dup(rs_exec_t* e, void* stream, int* launches) {
+    return guarded([&] {
+        *launches = e->ex->run_dup(static_cast<cudaStream_t>(stream));
         return RS_OK;
     });
 }

@@ -684,17 +684,52 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
     return launches;
 }
 
+void Executor::compute_dups(const std::vector<CopyOp>& ops) {
+    // replica dedup: peer-bound ops that bring the same source region to several
+    // destination ranks on ONE GPU, at identical destination geometry (DP replicas), cross
+    // NVLink once — to the lowest such rank (the primary) — and the others are copied from
+    // it on the destination GPU after a cross-GPU barrier (run_dup)
+    dup_primary_.assign(ops.size(), -1);
+    if (!dedup_) return;
+    using Key = std::tuple<int, int, std::int64_t, std::int64_t, std::int64_t, std::int64_t, int, int, std::int64_t,
+                           std::int64_t>;
+    std::map<Key, std::vector<size_t>> groups;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        const CopyOp& op = ops[i];
+        if (op.rows <= 0 || op.row_bytes <= 0) continue;
+        const int sg = bufs_[0][static_cast<size_t>(op.src_side_rank)].gpu, dg = bufs_[1][static_cast<size_t>(op.dst_rank)].gpu;
+        if (sg == dg) continue;
+        groups[Key{op.src_side_rank, op.src_buf, op.src_off, op.rows, op.row_bytes, op.rows > 1 ? op.src_pitch : 0, dg,
+                   op.dst_buf, op.dst_off, op.rows > 1 ? op.dst_pitch : 0}]
+            .push_back(i);
+    }
+    for (auto& kv : groups) {
+        auto& v = kv.second;
+        if (v.size() < 2) continue;
+        std::sort(v.begin(), v.end(), [&](size_t a, size_t b) { return ops[a].dst_rank < ops[b].dst_rank; });
+        for (size_t k = 1; k < v.size(); ++k) dup_primary_[v[k]] = ops[v[0]].dst_rank;
+    }
+}
+
+void Executor::set_replica_dedup(bool on) {
+    dedup_ = on;
+    bcast_ready_ = false;
+    mc_va_.clear();
+    prepared_ = false;
+}
+
 const std::vector<BcastGroup>& Executor::bcast_groups() {
     if (bcast_ready_) return bcast_;
     bcast_.clear();
     const std::vector<CopyOp> ops = build_ops(P_);
+    compute_dups(ops);
     // candidate ops: cross-GPU, destination at the source's own offset in an equally
     // sized buffer (replica layout), 16-B aligned (multimem.st.v4)
     using Key = std::tuple<int, int, std::int64_t, std::int64_t, std::int64_t, std::int64_t>;
     std::map<Key, std::vector<size_t>> by_src;
     for (size_t i = 0; i < ops.size(); ++i) {
         const CopyOp& op = ops[i];
-        if (op.rows <= 0 || op.row_bytes <= 0) continue;
+        if (op.rows <= 0 || op.row_bytes <= 0 || dup_primary_[i] >= 0) continue;  // dups never cross NVLink
         const RankBufs& S = bufs_[0][static_cast<size_t>(op.src_side_rank)];
         const RankBufs& D = bufs_[1][static_cast<size_t>(op.dst_rank)];
         if (S.gpu == D.gpu || op.dst_buf != op.src_buf || op.dst_off != op.src_off) continue;
@@ -785,6 +820,10 @@ void Executor::prepare(bool staged) {
     }
     const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
     if (!mc_) mc_ = std::make_unique<TileSet>();
+    if (!dup_) dup_ = std::make_unique<TileSet>();
+    dup_->buckets.clear();
+    dup_->lanes.clear();
+    compute_dups(ops);
     mc_src_bytes_ = 0;
     mc_->buckets.clear();
     mc_->lanes.clear();
@@ -839,6 +878,20 @@ void Executor::prepare(bool staged) {
             ch.op_bytes.push_back(total);
             continue;
         }
+        if (!staged && dup_primary_[oi] >= 0) {
+            // a replica of a region the primary rank on this destination GPU receives:
+            // copied there after the cross-GPU barrier (run_dup), never pushed
+            if (dst_here) {
+                const RankBufs& D0 = bufs_[1][static_cast<size_t>(dup_primary_[oi])];
+                if (!D0.ptr[op.dst_buf] || !D.ptr[op.dst_buf]) throw ConfigError("prepare: replica buffer not bound");
+                dup_->add(0, reinterpret_cast<std::uint64_t>(D0.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off),
+                          reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
+                          op.row_bytes, op.dst_pitch, op.dst_pitch, kTile);
+                stats_.local_bytes += total;
+                stats_.dup_bytes += total;
+            }
+            continue;
+        }
         if (!src_here) continue;  // pushed by the source's GPU
         if (op_mc[oi]) {
             if (!S.ptr[op.src_buf]) throw ConfigError("prepare: multicast source buffer not bound");
@@ -878,6 +931,7 @@ void Executor::prepare(bool staged) {
     if (!upload_) RS_CUDA(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
     fused_->finalize(&stats_, upload_, &staging_);
     mc_->finalize(&stats_, upload_, &staging_);
+    dup_->finalize(&stats_, upload_, &staging_);
     for (const TileSet::Group& g : mc_->groups)
         if (g.cls != 0) throw ConfigError("prepare: multicast tiles must be 16-byte aligned");
     for (auto& kv : channels_) {
@@ -1029,6 +1083,13 @@ int Executor::run_fused(cudaStream_t stream) {
     RS_CUDA(cudaEventRecord(ev_join_, aux_));
     RS_CUDA(cudaStreamWaitEvent(stream, ev_join_, 0));
     return n;
+}
+
+int Executor::run_dup(cudaStream_t stream) {
+    if (!prepared_) throw ConfigError("run before prepare");
+    if (!dup_ || dup_->groups.empty()) return 0;
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    return dup_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, use_bulk_);
 }
 
 int Executor::num_stages() const {

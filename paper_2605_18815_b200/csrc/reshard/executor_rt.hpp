@@ -42,6 +42,7 @@ struct ExecStats {
     std::int64_t launches = 0;                         // kernel launches per run()
     std::int64_t ce_bytes = 0;                         // peer-bound bytes moved by copy engines
     std::int64_t mc_bytes = 0;                         // bytes delivered by multicast stores
+    std::int64_t dup_bytes = 0;                        // replica bytes copied on the destination GPU
 };
 
 struct RankBufs {
@@ -144,6 +145,11 @@ public:
     /// the root's source buffer and every member's destination buffer at equal offsets);
     /// nullptr reverts to per-destination pushes. Takes effect at the next prepare().
     void set_multicast(int id, void* mc_va);
+    /// replica dedup: a source region bound for several replica ranks on one GPU crosses
+    /// NVLink once; run_dup() copies it to the others on that GPU — call it on every GPU
+    /// after run() and a cross-GPU barrier. Takes effect at the next prepare().
+    void set_replica_dedup(bool on);
+    int run_dup(cudaStream_t stream);
 
     void fill(int side, std::uint64_t seed, cudaStream_t stream);
     std::int64_t verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad);
@@ -153,6 +159,7 @@ public:
 
 private:
     std::vector<FillTask> fill_tasks(int side) const;
+    void compute_dups(const std::vector<CopyOp>& ops);
     int launch_multicast(cudaStream_t stream) const;
     int run_fused(cudaStream_t stream);
     void upload_tasks(const std::vector<FillTask>& tasks);
@@ -182,6 +189,9 @@ public:
 private:
     std::unique_ptr<TileSet> fused_;
     std::unique_ptr<TileSet> mc_;  // multicast tiles (dst = multicast address)
+    std::unique_ptr<TileSet> dup_;  // replica copies on this GPU (run_dup)
+    bool dedup_ = false;
+    std::vector<int> dup_primary_;  // per op: dst rank holding the primary copy, or -1
     std::vector<BcastGroup> bcast_;
     bool bcast_ready_ = false;
     std::map<int, void*> mc_va_;

@@ -4,9 +4,11 @@ go from the root GPU as ONE multicast store stream instead of one push per joine
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bcast_bench.py [--layers L]
 
-Both variants run on the same multi-GPU arena (VMM buffers, shared by descriptors) and
-are verified bit-exact against canon. Prints one JSON line (rank 0) with the forward
-transition time (max over ranks) of: per-destination pushes, and multicast.
+All variants run on the same multi-GPU arena (VMM buffers, shared by descriptors) and
+are verified bit-exact against canon (destinations cleared first). Prints one JSON line
+(rank 0) with the forward transition time (max over ranks) of: per-destination pushes,
+multicast, replica dedup (a region crosses NVLink once per destination GPU and is copied
+to the other replica ranks there after a barrier), and dedup + multicast.
 """
 import argparse
 import json
@@ -26,14 +28,24 @@ from paper_2605_18815_b200.runtime import (Transition, dist_env, exchange_arena,
                                            setup_multicast)
 
 
-def timed(ex, stream, reps, world):
+def run_once(ex, stream, world, dedup):
+    """One transition: fused/multicast pushes, then (replica dedup, on EVERY rank so the
+    collectives stay matched) a barrier and the copies on each destination GPU."""
+    ex.run(stream.cuda_stream)
+    if dedup:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ex.run_dup(stream.cuda_stream)
+
+
+def timed(ex, stream, reps, world, dedup):
     ts = []
     for _ in range(reps):
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ex.run(stream.cuda_stream)
+        run_once(ex, stream, world, dedup)
         e1.record(stream)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -68,50 +80,47 @@ def main():
            "chunk_mb": args.chunk_mb,
            "plan_bytes": plan.bytes_moved()}
 
-    ex.prepare()
-    ex.fill(A.SIDE_SRC, seed)
-    ex.run(stream.cuda_stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    bad_push = ex.verify(A.SIDE_DST, seed)[0]
-    push_min, push_avg, push_per = timed(ex, stream, args.reps, world)
-    st = ex.stats()
-    out["push"] = {"ms_min": round(push_min, 3), "ms_avg": round(push_avg, 3), "mismatches": int(bad_push), "ms_per_rank": push_per,
-                   "remote_gb_rank0": round(st.remote_bytes / 1e9, 2)}
-
-    groups = ex.bcast_groups()
-    out["bcast_groups"] = [{"id": g.id, "root_rank": g.root_rank, "root_gpu": g.root_gpu, "slot": g.slot,
-                            "member_gpus": list(g.member_gpu[: g.n_members]),
-                            "member_ranks": list(g.member_rank[: g.n_members]),
-                            "payload_gb": round(g.payload_bytes / 1e9, 3)} for g in groups]
-    mcs = []
-    if groups:
-        mcs = setup_multicast(arena, ex, rank, world, local, tag=f"{os.environ.get('MASTER_PORT', '0')}-bcast",
-                              min_payload=1 << 20)
+    def variant(name, dedup, multicast):
+        ex.set_replica_dedup(dedup)
+        mcs = []
+        groups = ex.bcast_groups()
+        if multicast and groups:
+            mcs = setup_multicast(arena, ex, rank, world, local, tag=f"{os.environ.get('MASTER_PORT', '0')}-{name}",
+                                  min_payload=1 << 20)
         ex.prepare()
-        # clear the destinations so the check proves the multicast delivered them
-        ex.fill(A.SIDE_DST, seed ^ 0x5A5A)
+        ex.fill(A.SIDE_DST, seed ^ 0x5A5A)  # cleared: the check proves this variant delivered them
         ex.fill(A.SIDE_SRC, seed)
         torch.cuda.synchronize()
         dist.barrier()
-        ex.run(stream.cuda_stream)
+        run_once(ex, stream, world, dedup)
         torch.cuda.synchronize()
         dist.barrier()
-        bad_mc = ex.verify(A.SIDE_DST, seed)[0]
-        bad_src = ex.verify(A.SIDE_SRC, seed)[0]  # the root's bound source is rewritten in place
-        mc_min, mc_avg, mc_per = timed(ex, stream, args.reps, world)
+        bad = ex.verify(A.SIDE_DST, seed)[0] + ex.verify(A.SIDE_SRC, seed)[0]
+        ms_min, ms_avg, per = timed(ex, stream, args.reps, world, dedup)
         st = ex.stats()
-        t = torch.tensor([bad_mc + bad_src], dtype=torch.float64, device="cuda")
+        t = torch.tensor([bad], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
-        out["multicast"] = {"ms_min": round(mc_min, 3), "ms_avg": round(mc_avg, 3), "mismatches": int(t.item()),
-                            "ms_per_rank": mc_per, "mc_gb_rank0": round(st.mc_bytes / 1e9, 2),
-                            "remote_gb_rank0": round(st.remote_bytes / 1e9, 2)}
-        out["speedup"] = round(push_min / mc_min, 3)
-    t = torch.tensor([bad_push], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t)
-    out["push"]["mismatches"] = int(t.item())
-    for m in mcs:
-        m.close()
+        out[name] = {"ms_min": round(ms_min, 3), "ms_avg": round(ms_avg, 3), "mismatches": int(t.item()),
+                     "ms_per_rank": per, "remote_gb_rank0": round(st.remote_bytes / 1e9, 2),
+                     "mc_gb_rank0": round(st.mc_bytes / 1e9, 2), "dup_gb_rank0": round(st.dup_bytes / 1e9, 2),
+                     "multicast_groups": len(mcs)}
+        if name == "multicast":
+            out["bcast_groups"] = [{"id": g.id, "root_rank": g.root_rank, "root_gpu": g.root_gpu, "slot": g.slot,
+                                    "member_gpus": list(g.member_gpu[: g.n_members]),
+                                    "member_ranks": list(g.member_rank[: g.n_members]),
+                                    "payload_gb": round(g.payload_bytes / 1e9, 3)} for g in groups]
+        for m in mcs:  # unbind before the next variant rebinds
+            m.close()
+        for g in groups:
+            if g.root_gpu == rank and mcs:
+                ex.set_multicast(g.id, 0)
+
+    variant("push", False, False)
+    variant("multicast", False, True)
+    variant("dedup", True, False)
+    variant("dedup_multicast", True, True)
+    out["speedup_vs_push"] = {k: round(out["push"]["ms_min"] / out[k]["ms_min"], 3)
+                              for k in ("multicast", "dedup", "dedup_multicast")}
     del ex, tr, arena
     torch.cuda.synchronize()
     dist.barrier()

@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--gemm", type=int, default=8192)
     ap.add_argument("--balance", action="store_true",
                     help="grow with balance_fanout (reference PlanOptions): joiners spread over the replicas")
+    ap.add_argument("--dedup", action="store_true",
+                    help="replica dedup: the grow's parameters cross NVLink once per destination GPU")
     ap.add_argument("--multicast", action="store_true",
                     help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
     args = ap.parse_args()
@@ -71,6 +73,7 @@ def main():
             plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
             t["plan_s"] = time.perf_counter() - t0
             tr = Transition(plan, world, rank, local, alloc=False)
+            tr.ex.set_replica_dedup(args.dedup)
             keep = []
             if args.multicast:
                 # VMM state buffers shared by descriptor; the current state is the source
@@ -85,8 +88,6 @@ def main():
                 tr.ex.prepare()
                 t["total_s"] = time.perf_counter() - t0
                 return tr, keep, t
-            tr = Transition(plan, world, rank, local, alloc=False)
-            keep = []
             for side in (A.SIDE_SRC, A.SIDE_DST):
                 nr = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
                 for r in range(nr):
@@ -109,6 +110,8 @@ def main():
                 for x in blobs:
                     tr.ex.ipc_import(x)
             tr.ex.prepare()
+            st = tr.ex.stats()
+            t["remote_gb"], t["dup_gb"] = round(st.remote_bytes / 1e9, 2), round(st.dup_bytes / 1e9, 2)
             t["total_s"] = time.perf_counter() - t0
             return tr, keep, t
         return build
@@ -164,6 +167,10 @@ def main():
             tr.run()
             torch.cuda.synchronize()
             dist.barrier()
+            if args.dedup:  # the replica copies on each destination GPU, after the pushes everywhere
+                tr.ex.run_dup()
+                torch.cuda.synchronize()
+                dist.barrier()
             switch_s = time.perf_counter() - t0
             bad = tr.ex.verify(A.SIDE_DST, seed)[0]
             init = torch.tensor([edm.init_s, window_s, switch_s, float(bad)], dtype=torch.float64, device="cuda")
@@ -206,7 +213,7 @@ def main():
         torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
-                          "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast,
+                          "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast, "dedup": args.dedup,
                           "results": results}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
