@@ -22,6 +22,7 @@ def main():
     layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     staged = "--staged" in sys.argv
     vmm = "--vmm" in sys.argv  # shareable VMM buffers mapped by descriptor instead of cudaIpc
+    dedup = "--dedup" in sys.argv  # replica dedup: one NVLink crossing per destination GPU
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -52,6 +53,9 @@ def main():
                         keep.append(t)
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
                         bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
+        if dedup:
+            fwd.ex.set_replica_dedup(True)
+            bwd.ex.set_replica_dedup(True)
         if vmm:
             fwd.ex.prepare()
             bwd.ex.prepare()
@@ -64,6 +68,15 @@ def main():
             fwd.connect()
             bwd.connect()
             fwd_run, bwd_run = fwd.run, bwd.run
+        if dedup:
+            def with_dup(tr):
+                def run():
+                    tr.run()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    tr.ex.run_dup()
+                return run
+            fwd_run, bwd_run = with_dup(fwd), with_dup(bwd)
         fwd.ex.fill(A.SIDE_SRC, seed)
         torch.cuda.synchronize()
         dist.barrier()
@@ -76,7 +89,7 @@ def main():
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep

@@ -241,6 +241,9 @@ def test_multicast_broadcast_grow():
     assert d["push"]["mismatches"] == 0
     assert d["bcast_groups"] and d["multicast"]["mismatches"] == 0
     assert d["multicast"]["mc_gb_rank0"] > 0
+    # replica dedup alone and with multicast: fewer NVLink bytes from the root, same state
+    assert d["dedup"]["mismatches"] == 0 and d["dedup_multicast"]["mismatches"] == 0
+    assert d["dedup"]["remote_gb_rank0"] < d["push"]["remote_gb_rank0"]
 
 
 def test_broadcast_groups_need_two_remote_gpus():
@@ -313,3 +316,19 @@ def test_gpu_box_planner_equals_host():
         p = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ms, n, eq = p.box_routes_timed(0)
         assert eq, sc.name
+
+
+def test_multi_gpu_replica_dedup():
+    """N>1 with replica dedup (one NVLink crossing per destination GPU, local copies after a
+    barrier): every scenario's round trip bit-exact. Skipped on one GPU."""
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29539",
+                        os.path.join(root, "tests", "mgpu_check.py"), "2", "--dedup"],
+                       capture_output=True, text=True, timeout=600)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
