@@ -38,10 +38,8 @@ def _compile(src: str, force: bool) -> str:
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
-    if src.endswith(".cu"):
-        cmd += ["-Xptxas", "-v"] if os.environ.get("RS_PTXAS_V") else []
-    else:
-        cmd += ["-x", "cu"] if False else []
+    if src.endswith(".cu") and os.environ.get("RS_PTXAS_V"):
+        cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
