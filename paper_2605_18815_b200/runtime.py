@@ -242,7 +242,7 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
     tr.ex. Collective over `group` (gloo in the EDM side thread). Returns
     {(side, rank, buf): VmmBuffer} for local buffers plus ("peer", side, rank, buf) keys
     for the mapped peers' buffers (keep it alive while the executor runs)."""
-    import pickle
+    import json
     import threading
 
     import torch.distributed as dist
@@ -277,7 +277,7 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
         try:
             for _ in range(world - 1):
                 fds, payload = fdx_recv(sock)
-                rows = pickle.loads(payload)
+                rows = json.loads(payload.decode())  # plain data: no code runs on receipt
                 for fd, (r, b, n) in zip(fds, rows):
                     received.append((r, b, n, VmmBuffer.import_fd(fd, n, device)))
         except BaseException as e:  # surfaced below
@@ -290,7 +290,7 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
             continue
         fds = [out[(A.SIDE_DST, r, b)].export_fd() for r, b, _ in table]
         try:
-            fdx_send(f"reshard-vmm-{tag}-{peer}", fds, pickle.dumps(table))
+            fdx_send(f"reshard-vmm-{tag}-{peer}", fds, json.dumps(table).encode())
         finally:
             for fd in fds:
                 os.close(fd)
