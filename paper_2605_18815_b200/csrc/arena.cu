@@ -244,6 +244,12 @@ void Arena::import_peer(const std::vector<int>& fds, const std::vector<std::uint
         Entry e;
         std::memcpy(&e, table.data() + at, sizeof e);
         at += sizeof e;
+        // the table comes from another process: validate before using any field
+        if (e.layout < 0 || e.layout > 1 || e.buf < 0 || e.buf >= exec::kNumBufs || e.rank < 0 || e.nh < 0 ||
+            e.piece <= 0 || e.reserved < 0 || e.bytes < 0 ||
+            at + static_cast<size_t>(e.nh) * sizeof(std::int32_t) > table.size() ||
+            static_cast<std::int64_t>(e.nh) * e.piece != e.reserved)
+            throw ConfigError("arena import: malformed mapping table");
         std::vector<std::int32_t> idx(static_cast<size_t>(e.nh));
         std::memcpy(idx.data(), table.data() + at, idx.size() * sizeof(std::int32_t));
         at += idx.size() * sizeof(std::int32_t);
