@@ -122,8 +122,20 @@ std::vector<int> recv_fds(int listener, std::vector<std::uint8_t>* payload) {
         s = ::accept4(listener, nullptr, nullptr, SOCK_CLOEXEC);
     } while (s < 0 && errno == EINTR);
     check(s >= 0, "accept");
+    // only processes of this user may hand us descriptors (abstract sockets have no
+    // filesystem permissions)
+    ucred cred{};
+    socklen_t cl = sizeof cred;
+    if (::getsockopt(s, SOL_SOCKET, SO_PEERCRED, &cred, &cl) != 0 || cred.uid != ::getuid()) {
+        ::close(s);
+        throw ConfigError("fdx: connection from another user refused");
+    }
     std::uint64_t hdr[2];
     read_all(s, hdr, sizeof hdr);
+    if (hdr[0] > (1u << 20) || hdr[1] > (1ull << 30)) {
+        ::close(s);
+        throw ConfigError("fdx: malformed header");
+    }
     if (payload) {
         payload->resize(static_cast<size_t>(hdr[1]));
         read_all(s, payload->data(), payload->size());
@@ -151,6 +163,7 @@ std::vector<int> recv_fds(int listener, std::vector<std::uint8_t>* payload) {
         cmsghdr* c = CMSG_FIRSTHDR(&m);
         check(c && c->cmsg_type == SCM_RIGHTS, "SCM_RIGHTS");
         const size_t got = (c->cmsg_len - CMSG_LEN(0)) / sizeof(int);
+        check(got > 0 && got <= static_cast<size_t>(n), "SCM_RIGHTS count");
         const int* p = reinterpret_cast<const int*>(CMSG_DATA(c));
         fds.insert(fds.end(), p, p + got);
     }
