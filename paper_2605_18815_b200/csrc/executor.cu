@@ -623,14 +623,18 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     buckets.clear();
     lanes.clear();
     if (!host.empty()) {
-        // keep the descriptor buffer across re-prepares: with peer access enabled every
+        // two descriptor buffers used in turn: a re-prepare uploads into the one the last
+        // launch did not read, so it may overlap kernels of the previous prepare still in
+        // flight. Both are kept across re-prepares: with peer access enabled every
         // cudaMalloc/cudaFree also edits the peers' mappings (measured: 0.6 s stalls)
-        if (host.size() * sizeof(Tile) > dev_bytes) {
-            if (dev) cudaFree(dev);
-            dev = nullptr;
-            dev_bytes = host.size() * sizeof(Tile) * 5 / 4;
-            RS_CUDA(cudaMalloc(&dev, dev_bytes));
+        cur ^= 1;
+        if (host.size() * sizeof(Tile) > dev_bytes[cur]) {
+            if (dev_buf[cur]) cudaFree(dev_buf[cur]);
+            dev_buf[cur] = nullptr;
+            dev_bytes[cur] = host.size() * sizeof(Tile) * 5 / 4;
+            RS_CUDA(cudaMalloc(&dev_buf[cur], dev_bytes[cur]));
         }
+        dev = dev_buf[cur];
         // private non-blocking stream: descriptor uploads never serialize with the
         // caller's (training) streams, so the EDM can prepare in the background
         const size_t bytes = host.size() * sizeof(Tile);
@@ -650,7 +654,8 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
 }
 
 TileSet::~TileSet() {
-    if (dev) cudaFree(dev);
+    for (void* p : dev_buf)
+        if (p) cudaFree(p);
 }
 
 int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm,

@@ -74,8 +74,10 @@ struct TileSet {
     bool interleave = false;  // finalize: interleave lanes in proportion to their bytes
     std::vector<Tile> host;
     std::vector<Group> groups;
-    void* dev = nullptr;
-    size_t dev_bytes = 0;
+    void* dev = nullptr;                    // descriptors of the last finalize (dev_buf[cur])
+    void* dev_buf[2] = {nullptr, nullptr};  // used in turn by successive finalizes
+    size_t dev_bytes[2] = {0, 0};
+    int cur = 1;
     TileSet() = default;
     TileSet(const TileSet&) = delete;
     TileSet& operator=(const TileSet&) = delete;
