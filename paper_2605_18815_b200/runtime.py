@@ -395,6 +395,11 @@ def run_stages(ex: Executor, stream: int, world: int) -> None:
         if world > 1:
             torch.cuda.synchronize()
             dist.barrier()
+    # replica dedup: the copies from each GPU's primary replica, once every stage has landed
+    # (a later write than planned never clobbers live data; the primary's chunks are final).
+    # Local to each GPU and ordered on its stream: whatever reads them next (a push from
+    # this GPU) follows in stream order, so no barrier is needed after.
+    ex.run_dup(stream)
 
 
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:
