@@ -214,6 +214,7 @@ MemoryPlan plan_with_order(const core::PlanCore& ab, const core::PlanCore* ba, c
     // only by a LATER group.
     auto group_of = [groups](int s, int n) { return groups <= 0 || groups >= n ? s : s * groups / n; };
     mp.order[0] = order_ab;
+    mp.groups = groups;
     const int nu_ab = Uab.count();
     const std::vector<int> pos_ab = positions(mp.order[0], static_cast<size_t>(nu_ab));
     auto chunk_vec = [&](int l, int init) {
@@ -451,18 +452,31 @@ void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanC
         mp.cut[d].assign(io.size(), 0);
         std::vector<char> read_in_group(static_cast<size_t>(mp.nphys), 0);
         std::vector<int> touched;
-        for (size_t s = 0; s < io.size(); ++s) {
-            bool conflict = false;
-            for (const auto& w : io[s].writes) conflict = conflict || read_in_group[static_cast<size_t>(w.first)];
-            if (conflict) {
-                mp.cut[d][s] = 1;
-                for (int p : touched) read_in_group[static_cast<size_t>(p)] = 0;
-                touched.clear();
-            }
+        auto add_reads = [&](size_t s) {
             for (size_t k = 0; k < io[s].reads.size(); k += 3) {
                 const int p = io[s].reads[k];
                 if (!read_in_group[static_cast<size_t>(p)]) read_in_group[static_cast<size_t>(p)] = 1, touched.push_back(p);
             }
+        };
+        // aliasing only crosses the plan's concurrency groups, so a needed cut may move back
+        // to the start of its group: every GPU then cuts on the same group boundaries and
+        // the union over GPUs (runtime.global_stage_cuts) stays at most one cut per group
+        const int n = static_cast<int>(io.size());
+        auto group = [&](int x) { return mp.groups <= 0 || mp.groups >= n ? x : x * mp.groups / n; };
+        int last_cut = 0;
+        for (size_t s = 0; s < io.size(); ++s) {
+            bool conflict = false;
+            for (const auto& w : io[s].writes) conflict = conflict || read_in_group[static_cast<size_t>(w.first)];
+            if (conflict) {
+                int b = static_cast<int>(s);
+                while (b - 1 > last_cut && group(b - 1) == group(static_cast<int>(s))) --b;
+                mp.cut[d][static_cast<size_t>(b)] = 1;
+                last_cut = b;
+                for (int p : touched) read_in_group[static_cast<size_t>(p)] = 0;
+                touched.clear();
+                for (int q = b; q < static_cast<int>(s); ++q) add_reads(static_cast<size_t>(q));
+            }
+            add_reads(s);
         }
         if (!mp.cut[d].empty()) mp.cut[d][0] = 1;
     }

@@ -69,6 +69,7 @@ struct BufPlan {
 struct MemoryPlan {
     std::int64_t chunk = 0;
     int bands = 1;
+    int groups = 0;                // concurrency groups of the unit order (0: one per unit)
     std::vector<BufPlan> bufs[2];  // [layout][rank * kNumBufs + buf]
     std::vector<int> order[2];     // stage orders (units) A->B, B->A
     std::vector<int> cut[2];       // per stage position: 1 = a barrier precedes it

@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, dist_env, run_stages, shared_arena  # noqa: E402
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
@@ -48,10 +48,21 @@ def scenario(cfg: int, layers: int):
     raise SystemExit(f"unknown config {cfg}")
 
 
-def run_one(sc, rank, world, local, reps):
+def run_one(sc, rank, world, local, reps, arena_cap=0.0):
     plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
-    tr = Transition(plan, world, rank, local)
-    tr.connect()
+    arena = None
+    if arena_cap:
+        # old + new state do not fit: the memory-aware arena under a per-GPU cap, stages
+        # with a barrier between them (runtime.run_stages)
+        arena, cuts = shared_arena(plan, None, rank, world, local, cap_bytes=int(arena_cap * 1e9),
+                                   tag=f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}")
+        tr = Transition(plan, world, rank, local, alloc=False)
+        arena.bind(tr.ex, None, cuts)
+        tr.ex.prepare()
+        tr.run = lambda stream=0: run_stages(tr.ex, stream, world)
+    else:
+        tr = Transition(plan, world, rank, local)
+        tr.connect()
     ex = tr.ex
     seed = 0x5EED5
     ex.fill(A.SIDE_SRC, seed)
@@ -59,7 +70,7 @@ def run_one(sc, rank, world, local, reps):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ex.run(stream.cuda_stream)
+    tr.run(stream.cuda_stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -71,7 +82,7 @@ def run_one(sc, rank, world, local, reps):
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        ex.run(stream.cuda_stream)
+        tr.run(stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -91,7 +102,12 @@ def run_one(sc, rank, world, local, reps):
                         "t_roof_ms": round(t_roof * 1e3, 3), "frac": round(t_roof * 1e3 / ms, 4),
                         "max_link_gb": round(link / 1e9, 2), "max_hbm_gb": round(hbm / 1e9, 2),
                         "peaks": {"nvlink_gbs": NVLINK_GBS, "hbm_gbs": hbm_gbs}}}
-    del tr, ex
+    if arena is not None:
+        st = arena.stats()
+        out["arena"] = {"cap_gb": arena_cap, "physical_gb": round(st.physical_bytes / 1e9, 2),
+                        "old_gb": round(st.a_bytes / 1e9, 2), "new_gb": round(st.b_bytes / 1e9, 2),
+                        "aliased_gb": round(st.aliased_bytes / 1e9, 2), "bands": st.bands, "stages": ex.num_stages()}
+    del tr, ex, arena
     torch.cuda.synchronize()
     return out
 
@@ -101,13 +117,15 @@ def main():
     ap.add_argument("--config", type=int, action="append")
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--arena-cap", type=float, default=0.0,
+                    help="GB per GPU: run under the memory-aware arena (old + new need not fit)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for cfg in args.config or [1, 4]:
-        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps)
+        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap)
         if rank == 0:
             print(json.dumps(res), flush=True)
     if world > 1:
