@@ -313,6 +313,9 @@ int rs_exec_num_stages(const rs_exec_t* e, int* n);
 int rs_exec_run_stage(rs_exec_t* e, int stage, void* stream, int* launches);
 /* run the plan as memory-aware stages: dst ranks in the given order */
 int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n);
+/* rs_exec_run replayed from a CUDA graph (captured at the first call after each prepare,
+ * per stream): small transitions are launch-bound */
+int rs_exec_run_graph(rs_exec_t* e, void* stream, int* launches);
 /* the same order, grouped: cuts[i] == 1 starts a new stage at position i (cuts may be NULL) */
 int rs_exec_set_stage_groups(rs_exec_t* e, const int* dst_order, const int* cuts, int n);
 

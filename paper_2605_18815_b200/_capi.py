@@ -226,6 +226,7 @@ def _late_bindings(L):
         ("rs_exec_set_multicast", [vp, C.c_int, vp]),
         ("rs_exec_read", [vp, C.c_int, C.c_int, C.c_int, i64, vp, i64, vp]),
         ("rs_exec_set_replica_dedup", [vp, C.c_int]),
+        ("rs_exec_run_graph", [vp, vp, P(C.c_int)]),
         ("rs_exec_run_dup", [vp, vp, P(C.c_int)]),
         ("rs_enable_peer_access", [C.c_int, C.c_int]),
         ("rs_plan_box_routes_timed", [vp, C.c_int, P(C.c_double), P(i64), P(C.c_int)]),

@@ -205,6 +205,12 @@ class Executor:
         A.check(A.lib().rs_exec_run(self.h, C.c_void_p(stream), C.byref(n)))
         return n.value
 
+    def run_graph(self, stream: int = 0) -> int:
+        """run() replayed from a CUDA graph (captured once per prepare and stream)."""
+        n = C.c_int()
+        A.check(A.lib().rs_exec_run_graph(self.h, C.c_void_p(stream), C.byref(n)))
+        return n.value
+
     def set_stages(self, dst_order) -> None:
         arr = (C.c_int * max(1, len(dst_order)))(*dst_order)
         A.check(A.lib().rs_exec_set_stages(self.h, arr, len(dst_order)))

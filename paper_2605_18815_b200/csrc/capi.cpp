@@ -826,6 +826,13 @@ int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
     });
 }
 
+int rs_exec_run_graph(rs_exec_t* e, void* stream, int* launches) {
+    return guarded([&] {
+        *launches = e->ex->run_graph(static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
 int rs_exec_set_stages(rs_exec_t* e, const int* dst_order, int n) {
     return guarded([&] {
         e->ex->set_stage_order(std::vector<int>(dst_order, dst_order + (dst_order ? n : 0)));

@@ -363,6 +363,7 @@ Executor::~Executor() {
     if (aux_) cudaStreamDestroy(aux_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (mc_stream_) cudaStreamDestroy(mc_stream_);
     for (size_t i = 1; i < ce_streams_.size(); ++i) cudaStreamDestroy(ce_streams_[i]);
     for (cudaEvent_t e : ce_join_) cudaEventDestroy(e);
@@ -823,7 +824,18 @@ void Executor::prepare(bool staged) {
         const char* to = std::getenv("RS_TILE_ORDER");
         fused_->interleave = !(to && std::string(to) == "op");
     }
-    const std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
+    // tile size: 512 KiB, unless the transition is too small to give every SM a few tiles
+    // (then latency-bound: smaller tiles, down to one 32 KiB bulk stage, spread it out)
+    std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
+    std::int64_t here = 0;  // bytes this GPU moves
+    for (const CopyOp& op : ops)
+        if (bufs_[0][static_cast<size_t>(op.src_side_rank)].gpu == cfg_.gpu) here += op.rows * op.row_bytes;
+    if (cfg_.tile_bytes <= 0) {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg_.device);
+        const std::int64_t want = here / (static_cast<std::int64_t>(nsm) * 4);
+        if (want < kTile) kTile = std::max<std::int64_t>(32 << 10, want / 16 * 16);
+    }
     if (!mc_) mc_ = std::make_unique<TileSet>();
     if (!dup_) dup_ = std::make_unique<TileSet>();
     dup_->buckets.clear();
@@ -956,7 +968,10 @@ void Executor::prepare(bool staged) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device);
     sms_ = sms;
     const char* kern = std::getenv("RS_COPY_KERNEL");
-    use_bulk_ = !(kern && std::string(kern) == "vector");
+    // the TMA bulk pipeline (one warp per SM) wins on large transitions (0.977 of the copy
+    // peak); below ~1 GiB its per-SM pipeline ramp dominates and the 512-thread vector
+    // kernel is ~2.8x faster (tiny GPT: 17 us vs 47 us for 27 MB, near the HBM roofline)
+    use_bulk_ = kern ? std::string(kern) != "vector" : here >= (1ll << 30);
     const char* rk = std::getenv("RS_REMOTE_KERNEL");
     remote_bulk_ = rk && std::string(rk) == "bulk";
     const char* rc = std::getenv("RS_REMOTE_CTAS_PER_SM");
@@ -964,6 +979,8 @@ void Executor::prepare(bool staged) {
     if (use_bulk_)
         RS_CUDA(cudaFuncSetAttribute(bulk_tiles_kernel<kBulkStages, kBulkStage>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkStage));
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);  // descriptors changed: recapture
+    graph_exec_ = nullptr;
     prepared_ = true;
 }
 
@@ -979,6 +996,33 @@ int Executor::launch_multicast(cudaStream_t stream) const {
     }
     RS_CUDA(cudaGetLastError());
     return n;
+}
+
+int Executor::run_graph(cudaStream_t stream) {
+    // the whole launch sequence of run() as one CUDA graph: small transitions are
+    // launch-bound (a few kernels of microseconds each); captured once per prepare()
+    if (!prepared_) throw ConfigError("run before prepare");
+    RS_CUDA(cudaSetDevice(cfg_.device));
+    if (!graph_exec_ || graph_stream_ != stream) {
+        if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+        cudaGraph_t g = nullptr;
+        RS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            graph_launches_ = run(stream);
+        } catch (...) {
+            cudaStreamEndCapture(stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        RS_CUDA(cudaStreamEndCapture(stream, &g));
+        const cudaError_t e = cudaGraphInstantiate(&graph_exec_, g, 0);
+        cudaGraphDestroy(g);
+        RS_CUDA(e);
+        graph_stream_ = stream;
+    }
+    RS_CUDA(cudaGraphLaunch(graph_exec_, stream));
+    return graph_launches_;
 }
 
 int Executor::run(cudaStream_t stream) {

@@ -131,6 +131,9 @@ public:
     void prepare(bool staged = false);
     /// launch the transition (fused part); returns the number of kernel launches
     int run(cudaStream_t stream);
+    /// the same launches replayed from a CUDA graph (captured at the first call after
+    /// each prepare, per stream): for launch-bound small transitions
+    int run_graph(cudaStream_t stream);
     /// memory-aware stages across GPUs: launch one stage; the caller puts a cross-GPU
     /// barrier between stages (a stage's writes may land in chunks freed by the last one)
     int run_stage(int stage, cudaStream_t stream);
@@ -199,6 +202,9 @@ private:
     std::map<int, void*> mc_va_;
     std::int64_t mc_src_bytes_ = 0;
     cudaStream_t mc_stream_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    cudaStream_t graph_stream_ = nullptr;
+    int graph_launches_ = 0;
     cudaEvent_t mc_ev_[3] = {nullptr, nullptr, nullptr};
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;

@@ -332,3 +332,22 @@ def test_multi_gpu_replica_dedup():
                         os.path.join(root, "tests", "mgpu_check.py"), "2", "--dedup"],
                        capture_output=True, text=True, timeout=600)
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_cuda_graph_replay_small_transition():
+    """The tiny-GPT transition (launch-bound) replayed from a CUDA graph: bit-exact, and
+    re-captured after a re-prepare."""
+    plan = RoutingPlan.from_scenario(S.config1())
+    ex = Executor(plan)
+    ex.alloc()
+    ex.fill(A.SIDE_SRC, SEED)
+    ex.prepare()
+    st = torch.cuda.Stream()
+    for _ in range(3):
+        ex.run_graph(st.cuda_stream)
+    st.synchronize()
+    assert ex.verify(A.SIDE_DST, SEED)[0] == 0
+    ex.prepare()
+    ex.run_graph(st.cuda_stream)
+    st.synchronize()
+    assert ex.verify(A.SIDE_DST, SEED)[0] == 0
