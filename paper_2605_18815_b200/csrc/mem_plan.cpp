@@ -52,9 +52,11 @@ namespace {
 // kPeak: among the stages that keep their GPU under the running peak, the one freeing the
 // most old bytes on its own GPU, else the lowest peak. kRounds: kPeak restricted to the
 // GPUs in turn, so every G consecutive positions hold one unit per GPU (rounds: all links
-// busy in every group). Returns the order and the modeled peak (max over GPUs of live
-// bytes: old data still to be read + new data written so far).
-enum PassMode { kFreed = 0, kPeak = 1, kRounds = 2 };
+// busy in every group). kSpread: kPeak, but among the stages under the peak the one on the
+// GPU furthest behind (fewest units taken, relative to its total) — a soft form of rounds,
+// so merged groups span several GPUs. Returns the order and the modeled peak (max over
+// GPUs of live bytes: old data still to be read + new data written so far).
+enum PassMode { kFreed = 0, kPeak = 1, kRounds = 2, kSpread = 3 };
 std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, const std::vector<exec::CopyOp>& ops,
                                                       int bands, int n_gpus, int mode) {
     const bool peak_first = mode != kFreed;
@@ -93,11 +95,18 @@ std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, c
     order.reserve(static_cast<size_t>(ndu));
     std::vector<int> left(static_cast<size_t>(G), 0);
     for (int du = 0; du < ndu; ++du) ++left[static_cast<size_t>(gpu_dst(du / U.nb))];
+    const std::vector<int> total_units = left;
+    auto progress = [&](int g) {  // fraction of GPU g's units already ordered
+        return total_units[static_cast<size_t>(g)]
+                   ? 1.0 - static_cast<double>(left[static_cast<size_t>(g)]) / total_units[static_cast<size_t>(g)]
+                   : 1.0;
+    };
     int turn = 0;
     for (int step = 0; step < ndu; ++step) {
         int best = -1;
         bool best_under = false;
         std::int64_t best_freed = -1, best_peak = 0;
+        double best_prog = 2.0;
         int target = -1;
         if (mode == kRounds) {
             while (!left[static_cast<size_t>(turn % G)]) ++turn;
@@ -121,9 +130,11 @@ std::pair<std::vector<int>, std::int64_t> greedy_pass(const core::PlanCore& P, c
             if (best < 0) take = true;
             else if (!peak_first) take = freed > best_freed;
             else if (under != best_under) take = under;
+            else if (under && mode == kSpread)
+                take = progress(g) < best_prog || (progress(g) == best_prog && freed > best_freed);
             else if (under) take = freed > best_freed;
             else take = during < best_peak || (during == best_peak && freed > best_freed);
-            if (take) best = du, best_under = under, best_freed = freed, best_peak = during;
+            if (take) best = du, best_under = under, best_freed = freed, best_peak = during, best_prog = progress(g);
         }
         done[static_cast<size_t>(best)] = 1;
         order.push_back(best);
@@ -145,7 +156,12 @@ std::vector<int> greedy_stage_order(const core::PlanCore& P, const std::vector<e
     // the same order)
     auto a = greedy_pass(P, ops, bands, n_gpus, kFreed);
     auto b = greedy_pass(P, ops, bands, n_gpus, kPeak);
-    return b.second < a.second ? b.first : a.first;
+    auto& best = b.second < a.second ? b : a;
+    if (n_gpus > 1) {  // across GPUs, spreading wins ties: merged groups keep more links busy
+        auto c = greedy_pass(P, ops, bands, n_gpus, kSpread);
+        if (c.second <= best.second) return c.first;
+    }
+    return best.first;
 }
 
 namespace {
