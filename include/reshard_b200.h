@@ -211,6 +211,31 @@ typedef struct {
 #define RS_COMM_SCATTER 2
 #define RS_COMM_GATHER 3
 /* xor_schedule: peer of device i at step s, or -1 */
+/* ---- Elastic Device Manager: cached communicator
+ * groups per configuration, the side thread preparing the next world, the accounting. */
+typedef struct rs_edm rs_edm_t;
+typedef struct {
+    double init_s, overlapped_s, switch_s, exposed_s, ratio; /* ratio -1: undefined */
+} rs_edm_accounting_t;
+#define RS_EDM_BLOCKING 0
+#define RS_EDM_OVERLAPPED 1
+#define RS_EDM_IN_PLACE 2
+int rs_edm_create(rs_edm_t** out);
+void rs_edm_destroy(rs_edm_t* e);
+/* get_or_create_groups for one dimension (cached; *cache_hit = 1 when it was) */
+int rs_edm_groups(rs_edm_t* e, const rs_cfg_t* cfg, int dim, int* out, int cap, int* n_groups, int* group_size,
+                  int* cache_hit);
+int rs_edm_cache_stats(const rs_edm_t* e, int64_t* hits, int64_t* misses, double* creation_s);
+/* run build(arg) on a side thread (new world's plan, executor, buffers, peer mappings) */
+int rs_edm_prepare_async(rs_edm_t* e, int (*build)(void* arg), void* arg);
+int rs_edm_ready(const rs_edm_t* e, int* ready);
+/* join the side thread: its preparation time and build's return code */
+int rs_edm_wait(rs_edm_t* e, double* init_s, int* build_rc);
+/* simulate_scale_event accounting: window_s >= 0 = measured overlap window, else whole
+ * training steps of train_step_s fit into init_s */
+int rs_edm_accounting(double init_s, double switch_s, double window_s, double train_step_s, int mode,
+                      rs_edm_accounting_t* out);
+
 int rs_xor_peer(int i, int s, int n);
 /* MemoryAwareChunk: stage index per step (steps ascending, cost[k]
  * for steps[k]); RS_ERR_BUDGET if one step exceeds min(mem_avail) */

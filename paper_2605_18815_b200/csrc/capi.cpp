@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "reshard/arena.hpp"
+#include "reshard/edm.hpp"
 #include "reshard/fdx.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
@@ -1235,6 +1236,84 @@ int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64
     return guarded([&] {
         if (layout < 0 || layout > 1 || buf < 0 || buf >= exec::kNumBufs) throw ConfigError("bad buffer id");
         *bytes = a->a->bind_size(layout, rank, buf);
+        return RS_OK;
+    });
+}
+
+struct rs_edm {
+    edm::Manager m;
+};
+
+int rs_edm_create(rs_edm_t** out) {
+    return guarded([&] {
+        *out = new rs_edm;
+        return RS_OK;
+    });
+}
+
+void rs_edm_destroy(rs_edm_t* e) { delete e; }
+
+int rs_edm_groups(rs_edm_t* e, const rs_cfg_t* cfg, int dim, int* out, int cap, int* n_groups, int* group_size,
+                  int* cache_hit) {
+    return guarded([&] {
+        if (dim < 0 || dim > 4) throw ConfigError("bad group dimension");
+        bool hit = false;
+        const auto& g = e->m.groups(to_cfg(*cfg), static_cast<GroupDim>(dim), &hit);
+        *n_groups = static_cast<int>(g.size());
+        *group_size = g.empty() ? 0 : static_cast<int>(g[0].size());
+        *cache_hit = hit ? 1 : 0;
+        int k = 0;
+        for (const auto& grp : g)
+            for (int r : grp) {
+                if (k < cap) out[k] = r;
+                ++k;
+            }
+        return RS_OK;
+    });
+}
+
+int rs_edm_cache_stats(const rs_edm_t* e, int64_t* hits, int64_t* misses, double* creation_s) {
+    return guarded([&] {
+        std::int64_t h = 0, m = 0;
+        e->m.cache_stats(&h, &m, creation_s);
+        *hits = h;
+        *misses = m;
+        return RS_OK;
+    });
+}
+
+int rs_edm_prepare_async(rs_edm_t* e, int (*build)(void* arg), void* arg) {
+    return guarded([&] {
+        if (!build) throw ConfigError("edm: no build function");
+        e->m.prepare_async(build, arg);
+        return RS_OK;
+    });
+}
+
+int rs_edm_ready(const rs_edm_t* e, int* ready) {
+    return guarded([&] {
+        *ready = e->m.ready() ? 1 : 0;
+        return RS_OK;
+    });
+}
+
+int rs_edm_wait(rs_edm_t* e, double* init_s, int* build_rc) {
+    return guarded([&] {
+        *build_rc = e->m.wait(init_s);
+        return RS_OK;
+    });
+}
+
+int rs_edm_accounting(double init_s, double switch_s, double window_s, double train_step_s, int mode,
+                      rs_edm_accounting_t* out) {
+    return guarded([&] {
+        if (mode < 0 || mode > 2) throw ConfigError("bad edm mode");
+        const edm::Accounting a = edm::account(init_s, switch_s, window_s, train_step_s, static_cast<edm::Mode>(mode));
+        out->init_s = a.init_s;
+        out->overlapped_s = a.overlapped_s;
+        out->switch_s = a.switch_s;
+        out->exposed_s = a.exposed_s;
+        out->ratio = a.ratio;
         return RS_OK;
     });
 }

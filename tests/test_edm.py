@@ -68,3 +68,36 @@ def test_prepare_async_overlaps_host_work():
         time.sleep(0.001)
     plan = edm.wait()
     assert plan.bytes_moved() > 0 and edm.init_s > 0
+
+
+def test_native_cache_counts_and_errors():
+    """The native EDM's cache counts hits/misses; a failing build surfaces at wait()."""
+    import ctypes as C
+
+    from paper_2605_18815_b200 import _capi as A
+    edm = ElasticDeviceManager()
+    cfg = S.Cfg(dp=4, tp=2)
+    edm.get_or_create_groups(cfg)
+    edm.get_or_create_groups(cfg)
+    hits, misses, cost = C.c_int64(), C.c_int64(), C.c_double()
+    A.check(edm._lib.rs_edm_cache_stats(edm.h, C.byref(hits), C.byref(misses), C.byref(cost)))
+    assert misses.value == 5 and hits.value == 5  # five dimensions, derived once, then served
+
+    def boom(ctrl):
+        raise ValueError("build failed")
+
+    edm.prepare_async(boom)
+    with pytest.raises(ValueError):
+        edm.wait()
+    edm.prepare_async(lambda ctrl: 42)  # the manager is reusable after a failure
+    while not edm.ready():
+        time.sleep(0.001)
+    assert edm.wait() == 42
+
+
+def test_accounting_modes():
+    r = overlap_accounting(init_s=4.0, switch_s=1.0, mode="in-place")
+    assert r["init_s"] == 0.0 and r["exposed_s"] == 1.0
+    r = overlap_accounting(init_s=4.0, switch_s=1.0, window_s=10.0, mode="blocking")
+    assert r["overlapped_s"] == 0.0 and r["exposed_s"] == 5.0 and r["overlap_ratio"] == 0.0
+    assert overlap_accounting(0.0, 0.0)["overlap_ratio"] is None
