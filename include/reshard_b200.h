@@ -387,6 +387,19 @@ void rs_vmm_free(rs_vmm_t* v);
 int rs_mc_bind_vmm(rs_mc_t* m, const rs_vmm_t* v, int64_t mc_offset);
 
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out);
+
+/* SPEC execute in one call, for FFI callers that own their buffers:
+ * builds the executor for opts' GPU, binds every listed buffer (this GPU's and the peers'
+ * it has mapped), prepares, runs on `stream` and waits. mode: RS_EXEC_FUSED (the push; the
+ * staged NCCL comparison and replica dedup need cross-rank steps: use rs_exec_*). */
+typedef struct {
+    int side, rank, buf;   /* RS_SIDE_*, virtual rank, RS_BUF_* */
+    void* ptr;
+    int64_t bytes;
+} rs_state_buffer_t;
+#define RS_EXEC_FUSED 0
+int rs_execute(const rs_plan_t* p, const rs_exec_opts_t* o, const rs_state_buffer_t* bufs, int n_bufs, void* stream,
+               int mode, int* launches);
 void rs_exec_destroy(rs_exec_t* e);
 int rs_exec_alloc(rs_exec_t* e);
 int rs_exec_bind(rs_exec_t* e, int side, int rank, int buf, void* dptr, int64_t bytes);

@@ -78,6 +78,10 @@ class ExecStats_t(C.Structure):
 RS_MAX_MEMBERS = 64
 
 
+class StateBuffer_t(C.Structure):
+    _fields_ = [("side", C.c_int), ("rank", C.c_int), ("buf", C.c_int), ("ptr", C.c_void_p), ("bytes", C.c_int64)]
+
+
 class BcastGroup_t(C.Structure):
     _fields_ = [("id", C.c_int), ("root_rank", C.c_int), ("root_gpu", C.c_int), ("buf", C.c_int), ("slot", C.c_int),
                 ("n_members", C.c_int), ("member_gpu", C.c_int * RS_MAX_MEMBERS),
@@ -227,6 +231,7 @@ def _late_bindings(L):
         ("rs_exec_read", [vp, C.c_int, C.c_int, C.c_int, i64, vp, i64, vp]),
         ("rs_exec_set_replica_dedup", [vp, C.c_int]),
         ("rs_exec_run_graph", [vp, vp, P(C.c_int)]),
+        ("rs_execute", [vp, P(ExecOpts_t), P(StateBuffer_t), C.c_int, vp, C.c_int, P(C.c_int)]),
         ("rs_exec_run_dup", [vp, vp, P(C.c_int)]),
         ("rs_enable_peer_access", [C.c_int, C.c_int]),
         ("rs_plan_box_routes_timed", [vp, C.c_int, P(C.c_double), P(i64), P(C.c_int)]),

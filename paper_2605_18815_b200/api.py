@@ -279,6 +279,17 @@ class Executor:
         return s
 
 
+def execute(plan: RoutingPlan, buffers, n_gpus: int = 1, gpu: int = 0, device: int = 0, stream: int = 0,
+            with_grads: bool = False) -> int:
+    """SPEC execute in one call (rs_execute): `buffers` = [(side, rank, buf, ptr, nbytes)]
+    for every buffer this GPU reads or writes; prepares, runs the push and waits."""
+    arr = (A.StateBuffer_t * max(1, len(buffers)))(*[A.StateBuffer_t(s, r, b, C.c_void_p(p), n) for s, r, b, p, n in buffers])
+    o = A.ExecOpts_t(n_gpus, gpu, device, int(with_grads), 0, 0)
+    n = C.c_int()
+    A.check(A.lib().rs_execute(plan.h, C.byref(o), arr, len(buffers), C.c_void_p(stream), 0, C.byref(n)))
+    return n.value
+
+
 class Arena:
     """VMM old/new layouts with plan-time eager-free aliasing (arena.hpp): one GPU, or
     (Arena.multi) the buffers one GPU of several hosts, shared by POSIX descriptor."""

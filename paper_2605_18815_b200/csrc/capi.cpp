@@ -645,6 +645,25 @@ int rs_schedule_dump(const rs_schedule_t* s, char** out, size_t* len) {
     });
 }
 
+int rs_execute(const rs_plan_t* p, const rs_exec_opts_t* o, const rs_state_buffer_t* bufs, int n_bufs, void* stream,
+               int mode, int* launches) {
+    return guarded([&] {
+        if (mode != RS_EXEC_FUSED) throw ConfigError("rs_execute: bad mode");
+        rs_exec_t* e = nullptr;
+        const int rc = rs_exec_create(p, o, &e);
+        if (rc != RS_OK) return rc;
+        std::unique_ptr<rs_exec_t, void (*)(rs_exec_t*)> guard(e, rs_exec_destroy);
+        for (int i = 0; i < n_bufs; ++i)
+            e->ex->bind(bufs[i].side, bufs[i].rank, bufs[i].buf, bufs[i].ptr, bufs[i].bytes);
+        e->ex->prepare();
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int n = e->ex->run(st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) throw exec::CudaError("rs_execute: stream failed");
+        if (launches) *launches = n;
+        return RS_OK;
+    });
+}
+
 int rs_exec_create(const rs_plan_t* p, const rs_exec_opts_t* o, rs_exec_t** out) {
     return guarded([&] {
         *out = nullptr;

@@ -351,3 +351,24 @@ def test_cuda_graph_replay_small_transition():
     ex.run_graph(st.cuda_stream)
     st.synchronize()
     assert ex.verify(A.SIDE_DST, SEED)[0] == 0
+
+
+def test_execute_one_call():
+    """rs_execute: the SPEC execute shape (buffers in, state moved) in one C call."""
+    from paper_2605_18815_b200.api import execute
+    plan = RoutingPlan.from_scenario(S.config1())
+    ex = Executor(plan)  # only to size the buffers and fill / verify the canon payloads
+    bufs, keep = [], []
+    for side, n in ((0, plan.summary.src_world), (1, plan.summary.dst_world)):
+        for r in range(n):
+            for b in range(6):
+                _, nbytes, _ = ex.buffer(side, r, b)
+                if nbytes:
+                    t = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+                    keep.append(t)
+                    ex.bind(side, r, b, t.data_ptr(), nbytes)
+                    bufs.append((side, r, b, t.data_ptr(), nbytes))
+    ex.fill(A.SIDE_SRC, SEED)
+    torch.cuda.synchronize()
+    assert execute(plan, bufs) >= 1
+    assert ex.verify(A.SIDE_DST, SEED)[0] == 0
