@@ -57,3 +57,23 @@ def test_c_caller_reproduces_reference_dumps(c_caller, golden, tmp_path):
             assert r.stdout.strip() == e["error"], e["name"]
         n += 1
     assert n >= 80
+
+
+def test_cpp_caller_of_the_reference_routing_api(golden, tmp_path):
+    """A C++ program written against the reference's routing API (plan_parameters,
+    plan_optimizer, plan_scalars, resolve_peers, format_transfer) builds against this repo
+    by switching its include path and prints the reference's own dump of config 1; with
+    ZeRO it throws the reference's ConfigError (D2)."""
+    exe = str(tmp_path / "routing_dump")
+    lib_dir = os.path.dirname(LIB)
+    subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-I", os.path.join(ROOT, "paper_2605_18815_b200", "csrc"),
+                    os.path.join(ROOT, "tools", "cpp_example", "routing_dump.cpp"), "-L", lib_dir, "-lreshard_b200",
+                    f"-Wl,-rpath,{lib_dir}", "-o", exe], check=True)
+    ref = {e["name"]: e for e in golden}
+    r = subprocess.run([exe], capture_output=True, text=True)
+    body, tail = r.stdout.rsplit("# transfers", 1)
+    e = ref["tiny-gpt.dp2tp2-to-tp4"]
+    assert r.returncode == 0 and body == e["dump"]
+    assert f"bytes_moved={e['bytes_moved']}" in tail and f"bytes_retained={e['bytes_retained']}" in tail
+    r = subprocess.run([exe, "zero"], capture_output=True, text=True)
+    assert r.returncode == 2 and r.stdout.strip() == ref["tiny-gpt.dp2tp2-to-tp4-zero1"]["error"]
