@@ -2,7 +2,7 @@
 // the tiny GPT of BASELINE config 1 (DP2xTP2 -> TP4), planned with plan_parameters +
 // plan_optimizer + plan_scalars + resolve_peers, printed with format_transfer.
 //
-//   g++ -std=c++20 -I paper_2605_18815_b200/csrc routing_dump.cpp \
+//   g++ -std=c++20 -I paper_2605_18815_b200/csrc routing_dump.cpp
 //       -L paper_2605_18815_b200/_lib -lreshard_b200 -o routing_dump
 #include <cstdio>
 #include <string>
