@@ -24,8 +24,15 @@ def main():
     vmm = "--vmm" in sys.argv  # shareable VMM buffers mapped by descriptor instead of cudaIpc
     dedup = "--dedup" in sys.argv  # replica dedup: one NVLink crossing per destination GPU
     rank, world, local = dist_env()
+    # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box) exercise the N=8 placement: ranks
+    # sharing a device still exchange cudaIpc handles and push through them
+    shared = world > torch.cuda.device_count()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if shared:  # NCCL refuses two ranks on one device; the push needs no collective anyway
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     seed = 0xBEEF
     failures = 0
     scenarios = [S.config2(layers), S.config4(1), S.config3(2)[0], S.config3(2)[1]]
@@ -95,7 +102,7 @@ def main():
         del fwd, bwd, keep
         torch.cuda.synchronize()
         dist.barrier()
-    t = torch.tensor([failures], device="cuda")
+    t = torch.tensor([failures], device="cpu" if shared else "cuda")
     dist.all_reduce(t)
     dist.destroy_process_group()
     if rank == 0:

@@ -372,3 +372,19 @@ def test_execute_one_call():
     torch.cuda.synchronize()
     assert execute(plan, bufs) >= 1
     assert ex.verify(A.SIDE_DST, SEED)[0] == 0
+
+
+def test_eight_rank_placement_oversubscribed():
+    """The N=8 placement (one virtual rank per rank process) with 8 processes on the GPUs
+    this box has (ranks share devices; gloo plumbing): every scenario bit-exact."""
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+                        "--master-addr", "127.0.0.1", "--master-port", "29541",
+                        os.path.join(root, "tests", "mgpu_check.py"), "2"],
+                       capture_output=True, text=True, timeout=900)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
