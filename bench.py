@@ -199,7 +199,7 @@ def run_reference(args):
     v = cb.bytes / mean_s / 1e9
     out = {"metric": METRIC, "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(mean_s * 1e3, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "u16/u32 payload copy", "data": "synthetic (canon payloads)",
+           "scaling": "strong", "vs_baseline": None, "dtype": "u16/u32 payload copy", "data": "synthetic (canon payloads)",
            "impl": "reference", "verified_mismatches": bad,
            "config": {"workload": f"llama3-8b tp8->dp2xtp4 zero1, CPU sample L={args.cpu_layers}",
                       "model": "Llama-3-8B", "parallelism": "tp8 -> dp2xtp4 + zero1"},
@@ -450,7 +450,10 @@ def run_ours(args):
             cpu = cpu_baseline(layers_sample=args.cpu_layers)
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
+            "scaling_note": ("the same 8-virtual-rank transition at every N: at N=1 it is an HBM-only permutation "
+                             "(roofline 39 ms), from N=2 on bytes cross NVLink (roofline 35.7 ms at N=2 and 4, "
+                             "17.8 ms at N=8, SURVEY 8d); roofline.frac is the per-N efficiency"),
             "vs_baseline": None, "dtype": "u16/u32 payload copy (bf16 params, fp32 master/m/v)",
             "data": "synthetic (canon payloads, bit-exact verified)",
             "transport": args.transport,
