@@ -441,8 +441,14 @@ def run_ours(args):
         try:
             with open(os.path.join(ROOT, "tests", "golden", "ref_plans.json")) as f:
                 ref = {e["name"]: e["ref_seconds"] for e in json.load(f)["entries"]}
-            planner["reference_planner_s_build_host"] = {"L=1": ref.get("llama3-8b-L1.tp8-to-dp2tp4-zero1"),
-                                                         "L=2": ref.get("llama3-8b-L2.tp8-to-dp2tp4-zero1")}
+            t1, t2 = ref.get("llama3-8b-L1.tp8-to-dp2tp4-zero1"), ref.get("llama3-8b-L2.tp8-to-dp2tp4-zero1")
+            planner["reference_planner_s_build_host"] = {"L=1": t1, "L=2": t2}
+            if t1 and t2:  # t = a * L^b through the two points (b ~ 2: O(n*m) interval lists, D3)
+                import math
+                b = math.log2(t2 / t1)
+                planner["reference_planner_s_fit"] = {"exponent": round(b, 3),
+                                                      f"L={args.layers}": round(t1 * args.layers ** b, 1),
+                                                      "ours_s": round(plan_s, 4)}
         except Exception:
             pass
         cpu = None
