@@ -558,7 +558,7 @@ or_scenario* or_scenario_parse(const char* text, char* err, size_t errlen) {
 #undef FEED
     s->total = off;
     s->fp = fp;
-    s->by_id = xrealloc(NULL, sizeof(int) * (size_t)(s->nt ? s->nt : 1));
+    s->by_id = xrealloc(NULL, sizeof(int) * (size_t)(s->nt > 0 ? s->nt : 1));
     for (int i = 0; i < s->nt; ++i) s->by_id[i] = i;
     g_sort_scn = s;
     (void)g_sort_names_base;
