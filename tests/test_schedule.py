@@ -6,7 +6,7 @@ import random
 import pytest
 
 from paper_2605_18815_b200 import scenarios as S
-from paper_2605_18815_b200.api import (ConfigError, ReshardError, RoutingPlan, Schedule, memory_aware_chunk,
+from paper_2605_18815_b200.api import (ReshardError, RoutingPlan, Schedule, memory_aware_chunk,
                                        xor_peer)
 
 

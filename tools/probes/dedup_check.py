@@ -1,6 +1,8 @@
+"""Replica dedup on one GPU standing in for a 2- and 4-GPU placement: the root's
+NVLink bytes with and without it (executor stats only)."""
 import torch, sys
 sys.path.insert(0, '/root/repo')
-from paper_2605_18815_b200 import _capi as A, scenarios as S
+from paper_2605_18815_b200 import scenarios as S
 from paper_2605_18815_b200.api import Executor, RoutingPlan
 _, grow = S.config3(2)
 plan = RoutingPlan.from_scenario(grow, allow_oversourced=True)
