@@ -317,6 +317,9 @@ int rs_memory_schedule_level(const rs_plan_t* plan_ab, int n_gpus, int level, in
  * across GPUs, take the first level whose footprint fits on every rank */
 int rs_memory_schedule_footprints(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                                   int n_gpus, int gpu, int64_t* out, int cap, int* n);
+/* the plan's stage cuts of direction `dir` (1 = a barrier precedes that position) */
+int rs_memory_plan_cuts(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
+                        int n_gpus, int gpu, int groups, int bands, int dir, int* cuts, int cap, int* n);
 int rs_memory_plan(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                    rs_arena_stats_t* stats, int64_t* violations, int* order_ab, int* order_ba, int cap);
 /* multi-GPU arena: this process maps the buffers of the virtual ranks placed on GPU

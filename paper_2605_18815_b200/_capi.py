@@ -212,6 +212,8 @@ def _late_bindings(L):
         ("rs_arena_create_multi", [vp, vp, C.c_int, C.c_int, C.c_int, i64, i64, C.c_int, C.c_int, C.c_int, P(vp)]),
         ("rs_memory_schedule", [vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, P(C.c_int), P(i64)]),
         ("rs_memory_schedule_level", [vp, C.c_int, C.c_int, P(C.c_int), P(C.c_int)]),
+        ("rs_memory_plan_cuts", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_int), C.c_int,
+                                 P(C.c_int)]),
         ("rs_memory_schedule_footprints", [vp, vp, i64, C.c_int, C.c_int, C.c_int, P(i64), C.c_int, P(C.c_int)]),
         ("rs_memory_plan_ex", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int),
                                P(C.c_int), C.c_int]),

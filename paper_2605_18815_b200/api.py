@@ -559,6 +559,15 @@ def memory_plan(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: 
     return st, viol.value, [x for x in oa if x >= 0], [x for x in ob if x >= 0]
 
 
+def memory_plan_cuts(ab: RoutingPlan, ba: Optional[RoutingPlan] = None, chunk_bytes: int = 0, with_grads: bool = False,
+                     n_gpus: int = 1, gpu: int = 0, groups: int = 0, bands: int = 1, direction: int = 0) -> List[int]:
+    """The plan's stage cuts (1 = a barrier precedes that unit position)."""
+    out, n = (C.c_int * 65536)(), C.c_int()
+    A.check(A.lib().rs_memory_plan_cuts(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu, groups,
+                                        bands, direction, out, 65536, C.byref(n)))
+    return list(out[: n.value])
+
+
 def memory_min_groups(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int, cap_bytes: int,
                       chunk_bytes: int = 0, with_grads: bool = False):
     """(fewest stage groups, one band, whose plan fits cap_bytes on `gpu` or -1, physical bytes)."""

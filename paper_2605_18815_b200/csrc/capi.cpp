@@ -1079,6 +1079,20 @@ int rs_memory_plan_ex(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_by
     });
 }
 
+int rs_memory_plan_cuts(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus, int gpu,
+                        int groups, int bands, int dir, int* cuts, int cap, int* n) {
+    return guarded([&] {
+        if (dir < 0 || dir > 1) throw ConfigError("bad direction");
+        const mem::MemoryPlan mp = mem::plan_memory(ab->core, ba ? &ba->core : nullptr,
+                                                    chunk_bytes > 0 ? chunk_bytes : (32ll << 20), with_grads != 0,
+                                                    n_gpus, gpu, groups, bands);
+        const std::vector<int>& c = mp.cut[dir];
+        *n = static_cast<int>(c.size());
+        for (int i = 0; i < *n && i < cap; ++i) cuts[i] = c[static_cast<size_t>(i)];
+        return RS_OK;
+    });
+}
+
 int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, rs_arena_stats_t* stats,
                    int64_t* violations, int* order_ab, int* order_ba, int cap) {
     return rs_memory_plan_ex(ab, ba, chunk_bytes, with_grads, 1, 0, 0, 1, stats, violations, order_ab, order_ba, cap);

@@ -102,3 +102,21 @@ def test_config5_full_fits_eight_gpus_under_the_cap():
     for g in range(8):
         st, viol, _, _ = memory_plan(ab, None, n_gpus=8, gpu=g, groups=groups, bands=bands)
         assert viol == 0 and st.physical_bytes <= cap and st.bands == bands
+
+
+def test_cuts_snap_to_group_starts_so_gpus_agree():
+    """With coarse groups (here: rounds) every GPU's cuts fall on group starts, so the
+    barriers all GPUs share stay at most one per group."""
+    from paper_2605_18815_b200.api import memory_plan_cuts
+    sc = S.config4(8)
+    ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+    n_gpus, bands = 4, 2
+    cuts = [memory_plan_cuts(ab, None, n_gpus=n_gpus, gpu=g, groups=-1, bands=bands) for g in range(n_gpus)]
+    units = len(cuts[0])
+    rounds = -(-units // n_gpus)
+    group_of = [x * rounds // units for x in range(units)]
+    union = [max(c[i] for c in cuts) for i in range(units)]
+    for i, u in enumerate(union):
+        if u:
+            assert i == 0 or group_of[i - 1] != group_of[i], (i, union)
+    assert sum(union) <= rounds
