@@ -388,3 +388,35 @@ def test_eight_rank_placement_oversubscribed():
                         os.path.join(root, "tests", "mgpu_check.py"), "2"],
                        capture_output=True, text=True, timeout=900)
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_north_star_full_size_round_trip():
+    """BASELINE config 2 at full size (Llama-3-8B, L=32, 112.42 GB of plan bytes; 240.9 GB
+    of old + new state) on one B200 through the memory-aware arena. Size-independent
+    properties: every destination element equals its canon value after the forward
+    transition, and the way back restores every source element bit for bit."""
+    import gc
+    from paper_2605_18815_b200.api import Arena
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' cached blocks would shrink the free-HBM cap
+    sc = S.config2(32)
+    ab = RoutingPlan.from_scenario(sc)
+    ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
+    assert ab.bytes_moved() == 112_419_930_560
+    arena = Arena(ab, ba, device=0, cap_bytes=0)  # cap 0: free HBM - 1 GiB
+    st = arena.stats()
+    assert st.a_bytes + st.b_bytes > torch.cuda.get_device_properties(0).total_memory
+    assert st.aliased_bytes > 0
+    e1, e2 = Executor(ab), Executor(ba)
+    arena.bind(e1, e2)
+    e1.fill(0, SEED)
+    e1.prepare()
+    e2.prepare()
+    e1.run()
+    torch.cuda.synchronize()
+    bad, first = e1.verify(1, SEED)
+    assert bad == 0, f"forward: {bad} mismatches, first flat index {first}"
+    e2.run()
+    torch.cuda.synchronize()
+    bad, first = e2.verify(1, SEED)
+    assert bad == 0, f"way back: {bad} mismatches, first flat index {first}"
