@@ -363,7 +363,10 @@ int rs_exec_bcast_groups(rs_exec_t* e, rs_bcast_group_t* out, int cap, int* n);
 /* root only; mc_va NULL reverts to per-destination pushes; takes effect at the next prepare */
 int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va);
 /* replica dedup: a region bound for several replica ranks on one GPU crosses NVLink once;
- * after rs_exec_run on every GPU and a barrier, rs_exec_run_dup copies the other replicas */
+ * after rs_exec_run on every GPU and a barrier, rs_exec_run_dup copies the other replicas.
+ * on = 2 (early): stage 1 is a tail of the other pushes sized to hide the copies, stage 0
+ * the rest incl. the primaries (rs_exec_num_stages = 2): run stage 0, barrier on it, then rs_exec_run_dup on a second
+ * stream overlaps stage 1. Needs a single memory stage. */
 int rs_exec_set_replica_dedup(rs_exec_t* e, int on);
 int rs_exec_run_dup(rs_exec_t* e, void* stream, int* launches);
 

@@ -252,10 +252,13 @@ class Executor:
     def set_multicast(self, group_id: int, mc_va: int) -> None:
         A.check(A.lib().rs_exec_set_multicast(self.h, group_id, C.c_void_p(mc_va or None)))
 
-    def set_replica_dedup(self, on: bool = True) -> None:
+    def set_replica_dedup(self, on: bool = True, early: bool = False) -> None:
         """A region bound for several replica ranks on one GPU crosses NVLink once; call
-        run_dup() on every GPU after run() and a cross-GPU barrier."""
-        A.check(A.lib().rs_exec_set_replica_dedup(self.h, int(on)))
+        run_dup() on every GPU after run() and a cross-GPU barrier. early: stage 1 is a
+        tail of the other pushes sized to hide the copies, stage 0 the rest incl. the
+        primaries (num_stages() = 2), so run_dup can follow a
+        barrier on stage 0 and overlap stage 1 (runtime.run_dedup_early)."""
+        A.check(A.lib().rs_exec_set_replica_dedup(self.h, 2 if (on and early) else int(on)))
 
     def run_dup(self, stream: int = 0) -> int:
         n = C.c_int()

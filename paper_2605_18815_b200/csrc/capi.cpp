@@ -1154,7 +1154,7 @@ int rs_exec_set_multicast(rs_exec_t* e, int id, void* mc_va) {
 
 int rs_exec_set_replica_dedup(rs_exec_t* e, int on) {
     return guarded([&] {
-        e->ex->set_replica_dedup(on != 0);
+        e->ex->set_replica_dedup(on != 0, on == 2);
         return RS_OK;
     });
 }

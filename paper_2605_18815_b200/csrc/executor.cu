@@ -696,6 +696,7 @@ void Executor::compute_dups(const std::vector<CopyOp>& ops) {
     // NVLink once — to the lowest such rank (the primary) — and the others are copied from
     // it on the destination GPU after a cross-GPU barrier (run_dup)
     dup_primary_.assign(ops.size(), -1);
+    dup_lead_.assign(ops.size(), 0);
     if (!dedup_) return;
     using Key = std::tuple<int, int, std::int64_t, std::int64_t, std::int64_t, std::int64_t, int, int, std::int64_t,
                            std::int64_t>;
@@ -714,11 +715,13 @@ void Executor::compute_dups(const std::vector<CopyOp>& ops) {
         if (v.size() < 2) continue;
         std::sort(v.begin(), v.end(), [&](size_t a, size_t b) { return ops[a].dst_rank < ops[b].dst_rank; });
         for (size_t k = 1; k < v.size(); ++k) dup_primary_[v[k]] = ops[v[0]].dst_rank;
+        dup_lead_[v[0]] = 1;
     }
 }
 
-void Executor::set_replica_dedup(bool on) {
+void Executor::set_replica_dedup(bool on, bool early) {
     dedup_ = on;
+    dup_early_ = on && early;
     bcast_ready_ = false;
     mc_va_.clear();
     prepared_ = false;
@@ -841,6 +844,31 @@ void Executor::prepare(bool staged) {
     dup_->buckets.clear();
     dup_->lanes.clear();
     compute_dups(ops);
+    // early dedup: launch 1 is a tail of this GPU's other peer pushes, long enough to hide the
+    // replica copies (HBM, ~4.5x the NVLink push rate; RS_DUP_TAIL_FRAC, default 0.4 of the
+    // largest per-GPU replica bytes); everything else, the primaries first, is launch 0
+    std::vector<char> tail(ops.size(), 0);
+    if (dup_early_ && !staged) {
+        std::map<int, std::int64_t> dup_bytes;
+        for (size_t oi = 0; oi < ops.size(); ++oi)
+            if (dup_primary_[oi] >= 0)
+                dup_bytes[bufs_[1][static_cast<size_t>(ops[oi].dst_rank)].gpu] += ops[oi].rows * ops[oi].row_bytes;
+        std::int64_t dmax = 0;
+        for (const auto& kv : dup_bytes) dmax = std::max(dmax, kv.second);
+        double frac = 0.4;
+        if (const char* f = std::getenv("RS_DUP_TAIL_FRAC")) frac = std::atof(f);
+        std::int64_t budget = static_cast<std::int64_t>(static_cast<double>(dmax) * frac);
+        for (size_t oi = ops.size(); oi-- > 0 && budget > 0;) {
+            const CopyOp& op = ops[oi];
+            if (op.rows <= 0 || op.row_bytes <= 0 || dup_lead_[oi] || dup_primary_[oi] >= 0) continue;
+            // peer-bound only: local HBM copies would finish long before the replica copies
+            if (bufs_[0][static_cast<size_t>(op.src_side_rank)].gpu != cfg_.gpu ||
+                bufs_[1][static_cast<size_t>(op.dst_rank)].gpu == cfg_.gpu)
+                continue;
+            tail[oi] = 1;
+            budget -= op.rows * op.row_bytes;
+        }
+    }
     mc_src_bytes_ = 0;
     mc_->buckets.clear();
     mc_->lanes.clear();
@@ -940,7 +968,11 @@ void Executor::prepare(bool staged) {
         }
         // key = stage * 2 + remote when split_remote_ (peer-bound tiles as their own launch on
         // the caller's stream, local HBM tiles on an aux stream); otherwise one mixed launch
-        fused_->add(split_remote_ ? stage * 2 + (dst_here ? 0 : 1) : stage, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+        // early dedup: the primaries' tiles are in launch 0 (run_stage(0)), a tail of the
+        // rest is launch 1, so run_dup can start after a barrier on launch 0 and overlap it
+        if (dup_early_ && stage != 0) throw ConfigError("early replica dedup needs a single memory stage");
+        const int key = split_remote_ ? stage * 2 + (dst_here ? 0 : 1) : dup_early_ ? (tail[oi] ? 1 : 0) : stage;
+        fused_->add(key, reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
                     reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
                     op.row_bytes, op.src_pitch, op.dst_pitch, kTile, D.gpu);
     }
@@ -1142,6 +1174,7 @@ int Executor::run_dup(cudaStream_t stream) {
 }
 
 int Executor::num_stages() const {
+    if (dup_early_) return 2;
     return stage_of_dst_.empty() ? 1 : *std::max_element(stage_of_dst_.begin(), stage_of_dst_.end()) + 1;
 }
 

@@ -153,7 +153,10 @@ public:
     /// replica dedup: a source region bound for several replica ranks on one GPU crosses
     /// NVLink once; run_dup() copies it to the others on that GPU — call it on every GPU
     /// after run() and a cross-GPU barrier. Takes effect at the next prepare().
-    void set_replica_dedup(bool on);
+    /// early: stage 1 is a tail of this GPU's non-replica pushes sized to hide the copies,
+    /// stage 0 everything else incl. the primaries (num_stages() = 2), so run_dup can
+    /// follow a barrier on stage 0 and overlap stage 1
+    void set_replica_dedup(bool on, bool early = false);
     int run_dup(cudaStream_t stream);
 
     void fill(int side, std::uint64_t seed, cudaStream_t stream);
@@ -197,6 +200,8 @@ private:
     std::unique_ptr<TileSet> dup_;  // replica copies on this GPU (run_dup)
     bool dedup_ = false;
     std::vector<int> dup_primary_;  // per op: dst rank holding the primary copy, or -1
+    std::vector<char> dup_lead_;    // per op: it carries a region other ranks on its GPU copy
+    bool dup_early_ = false;
     std::vector<BcastGroup> bcast_;
     bool bcast_ready_ = false;
     std::map<int, void*> mc_va_;

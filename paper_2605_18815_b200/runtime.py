@@ -402,6 +402,29 @@ def run_stages(ex: Executor, stream: int, world: int) -> None:
     ex.run_dup(stream)
 
 
+def run_dedup_early(ex: Executor, stream, side_stream, group=None) -> None:
+    """One transition with early replica dedup (Executor.set_replica_dedup(early=True)):
+    stage 0 = the pushes of regions other ranks on the destination GPU copy plus most of the
+    rest, stage 1 = a tail of this GPU's other pushes sized to hide the copies. The host waits for stage 0 only, meets every rank at a barrier (use a gloo
+    `group`: an NCCL barrier kernel would queue behind the stage-1 copy kernel, which holds
+    every SM), then runs the replica copies on `side_stream` while stage 1 is still
+    pushing. `stream` / `side_stream` are torch streams on this rank's device; on return
+    `stream` is ordered after the copies. Call it on EVERY rank."""
+    import torch
+    import torch.distributed as dist
+    if ex.num_stages() != 2:
+        raise A.ConfigError(A.RS_ERR_CONFIG, "run_dedup_early needs set_replica_dedup(True, early=True) before prepare")
+    done0 = torch.cuda.Event()
+    ex.run_stage(0, stream.cuda_stream)
+    done0.record(stream)
+    ex.run_stage(1, stream.cuda_stream)
+    done0.synchronize()
+    dist.barrier(group=group)
+    side_stream.wait_event(done0)
+    ex.run_dup(side_stream.cuda_stream)
+    stream.wait_stream(side_stream)
+
+
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:
     n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
     return [r for r in range(n) if ex.buffer(side, r, A.BUF_PARAM)[2] == ex.gpu]

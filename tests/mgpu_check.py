@@ -23,6 +23,8 @@ def main():
     staged = "--staged" in sys.argv
     vmm = "--vmm" in sys.argv  # shareable VMM buffers mapped by descriptor instead of cudaIpc
     dedup = "--dedup" in sys.argv  # replica dedup: one NVLink crossing per destination GPU
+    early = "--dedup-early" in sys.argv  # ... with the copies overlapping the non-replica pushes
+    dedup = dedup or early
     rank, world, local = dist_env()
     # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box) exercise the N=8 placement: ranks
     # sharing a device still exchange cudaIpc handles and push through them
@@ -35,6 +37,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     seed = 0xBEEF
     failures = 0
+    ctrl = dist.new_group(backend="gloo") if early else None
+    side = torch.cuda.Stream() if early else None
     scenarios = [S.config2(layers), S.config4(1), S.config3(2)[0], S.config3(2)[1]]
     scenarios += [sc for sc in S.edge_scenarios() if sc.grads == "drop"]  # ragged, identity, join/leave
     for sc in scenarios:
@@ -61,8 +65,8 @@ def main():
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
                         bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
         if dedup:
-            fwd.ex.set_replica_dedup(True)
-            bwd.ex.set_replica_dedup(True)
+            fwd.ex.set_replica_dedup(True, early=early)
+            bwd.ex.set_replica_dedup(True, early=early)
         if vmm:
             fwd.ex.prepare()
             bwd.ex.prepare()
@@ -75,7 +79,15 @@ def main():
             fwd.connect()
             bwd.connect()
             fwd_run, bwd_run = fwd.run, bwd.run
-        if dedup:
+        if early:
+            from paper_2605_18815_b200.runtime import run_dedup_early
+
+            def with_dup(tr):
+                def run():
+                    run_dedup_early(tr.ex, torch.cuda.current_stream(), side, ctrl)
+                return run
+            fwd_run, bwd_run = with_dup(fwd), with_dup(bwd)
+        elif dedup:
             def with_dup(tr):
                 def run():
                     tr.run()
@@ -96,7 +108,7 @@ def main():
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''}{'(early)' if early else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep

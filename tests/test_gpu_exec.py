@@ -334,6 +334,22 @@ def test_multi_gpu_replica_dedup():
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+def test_multi_gpu_replica_dedup_early():
+    """Early replica dedup: the primaries' pushes first, a barrier on them, then the replica
+    copies on a second stream while the other pushes continue; round trips bit-exact."""
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29543",
+                        os.path.join(root, "tests", "mgpu_check.py"), "2", "--dedup-early"],
+                       capture_output=True, text=True, timeout=600)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_cuda_graph_replay_small_transition():
     """The tiny-GPT transition (launch-bound) replayed from a CUDA graph: bit-exact, and
     re-captured after a re-prepare."""

@@ -25,12 +25,17 @@ from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.runtime import (Transition, dist_env, exchange_arena, global_stage_cuts,  # noqa: E402
-                                           setup_multicast)
+                                           run_dedup_early, setup_multicast)
 
 
-def run_once(ex, stream, world, dedup):
+def run_once(ex, stream, world, dedup, early=None):
     """One transition: fused/multicast pushes, then (replica dedup, on EVERY rank so the
-    collectives stay matched) a barrier and the copies on each destination GPU."""
+    collectives stay matched) a barrier and the copies on each destination GPU. early =
+    (side stream, gloo group): the copies start after the primaries' pushes and overlap
+    the rest (runtime.run_dedup_early)."""
+    if early is not None:
+        run_dedup_early(ex, stream, early[0], early[1])
+        return
     ex.run(stream.cuda_stream)
     if dedup:
         torch.cuda.synchronize()
@@ -38,14 +43,14 @@ def run_once(ex, stream, world, dedup):
         ex.run_dup(stream.cuda_stream)
 
 
-def timed(ex, stream, reps, world, dedup):
+def timed(ex, stream, reps, world, dedup, early=None):
     ts = []
     for _ in range(reps):
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        run_once(ex, stream, world, dedup)
+        run_once(ex, stream, world, dedup, early)
         e1.record(stream)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -63,6 +68,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--chunk-mb", type=int, default=512,
                     help="arena chunk (multicast binds chunk by chunk; 512 MiB = the recommended granularity)")
+    ap.add_argument("--variants", default="push,multicast,dedup,dedup_multicast,dedup_early",
+                    help="comma-separated subset to run")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -80,8 +87,12 @@ def main():
            "chunk_mb": args.chunk_mb,
            "plan_bytes": plan.bytes_moved()}
 
-    def variant(name, dedup, multicast):
-        ex.set_replica_dedup(dedup)
+    ctrl = dist.new_group(backend="gloo")
+    side = torch.cuda.Stream()
+
+    def variant(name, dedup, multicast, early=False):
+        ex.set_replica_dedup(dedup, early=early)
+        ear = (side, ctrl) if early else None
         mcs = []
         groups = ex.bcast_groups()
         if multicast and groups:
@@ -92,11 +103,11 @@ def main():
         ex.fill(A.SIDE_SRC, seed)
         torch.cuda.synchronize()
         dist.barrier()
-        run_once(ex, stream, world, dedup)
+        run_once(ex, stream, world, dedup, ear)
         torch.cuda.synchronize()
         dist.barrier()
         bad = ex.verify(A.SIDE_DST, seed)[0] + ex.verify(A.SIDE_SRC, seed)[0]
-        ms_min, ms_avg, per = timed(ex, stream, args.reps, world, dedup)
+        ms_min, ms_avg, per = timed(ex, stream, args.reps, world, dedup, ear)
         st = ex.stats()
         t = torch.tensor([bad], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
@@ -115,12 +126,15 @@ def main():
             if g.root_gpu == rank and mcs:
                 ex.set_multicast(g.id, 0)
 
-    variant("push", False, False)
-    variant("multicast", False, True)
-    variant("dedup", True, False)
-    variant("dedup_multicast", True, True)
-    out["speedup_vs_push"] = {k: round(out["push"]["ms_min"] / out[k]["ms_min"], 3)
-                              for k in ("multicast", "dedup", "dedup_multicast")}
+    todo = args.variants.split(",")
+    for name, dedup, multicast, early in (("push", False, False, False), ("multicast", False, True, False),
+                                          ("dedup", True, False, False), ("dedup_multicast", True, True, False),
+                                          ("dedup_early", True, False, True)):
+        if name in todo:
+            variant(name, dedup, multicast, early)
+    if "push" in out:
+        out["speedup_vs_push"] = {k: round(out["push"]["ms_min"] / out[k]["ms_min"], 3)
+                                  for k in ("multicast", "dedup", "dedup_multicast", "dedup_early") if k in out}
     del ex, tr, arena
     torch.cuda.synchronize()
     dist.barrier()

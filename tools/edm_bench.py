@@ -24,7 +24,8 @@ from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.edm import ElasticDeviceManager, overlap_accounting  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env, setup_multicast, share_buffers  # noqa: E402
+from paper_2605_18815_b200.runtime import (Transition, dist_env, run_dedup_early, setup_multicast,  # noqa: E402
+                                           share_buffers)
 
 
 def main():
@@ -35,12 +36,16 @@ def main():
                     help="grow with balance_fanout (reference PlanOptions): joiners spread over the replicas")
     ap.add_argument("--dedup", action="store_true",
                     help="replica dedup: the grow's parameters cross NVLink once per destination GPU")
+    ap.add_argument("--dedup-early", action="store_true",
+                    help="--dedup with the replica copies overlapping the tail of the pushes")
     ap.add_argument("--multicast", action="store_true",
                     help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
     args = ap.parse_args()
+    args.dedup = args.dedup or args.dedup_early
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    early = (torch.cuda.Stream(), dist.new_group(backend="gloo")) if args.dedup_early else None
     shrink, grow = S.config3(args.layers)
     grow.balance = args.balance
     edm = ElasticDeviceManager()
@@ -73,7 +78,7 @@ def main():
             plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
             t["plan_s"] = time.perf_counter() - t0
             tr = Transition(plan, world, rank, local, alloc=False)
-            tr.ex.set_replica_dedup(args.dedup)
+            tr.ex.set_replica_dedup(args.dedup, early=args.dedup_early)
             keep = []
             if args.multicast:
                 # VMM state buffers shared by descriptor; the current state is the source
@@ -164,10 +169,13 @@ def main():
             dist.all_reduce(flag)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            tr.run()
+            if early is not None:  # replica copies overlap the tail of the pushes
+                run_dedup_early(tr.ex, torch.cuda.current_stream(), early[0], early[1])
+            else:
+                tr.run()
             torch.cuda.synchronize()
             dist.barrier()
-            if args.dedup:  # the replica copies on each destination GPU, after the pushes everywhere
+            if args.dedup and early is None:  # the replica copies on each destination GPU, after the pushes everywhere
                 tr.ex.run_dup()
                 torch.cuda.synchronize()
                 dist.barrier()
@@ -213,7 +221,7 @@ def main():
         torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
-                          "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast, "dedup": args.dedup,
+                          "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast, "dedup": args.dedup, "dedup_early": args.dedup_early,
                           "results": results}), flush=True)
     dist.barrier()
     dist.destroy_process_group()
