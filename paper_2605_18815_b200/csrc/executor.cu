@@ -1182,8 +1182,21 @@ int Executor::run_stage(int stage, cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
     if (split_remote_ || !ce_ops_.empty()) throw ConfigError("run_stage needs the single mixed launch (no CE offload)");
     RS_CUDA(cudaSetDevice(cfg_.device));
-    const int nmc = stage == 0 ? launch_multicast(stream) : 0;
-    return nmc + fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, has_remote_ ? remote_bulk_ : use_bulk_, -1, stage);
+    const bool bulk = has_remote_ ? remote_bulk_ : use_bulk_;
+    if (stage != 0 || !mc_ || mc_->groups.empty())
+        return fused_->launch(stream, 0, 0, sms_, cfg_.ctas_per_sm, bulk, -1, stage);
+    // stage 0 carries the multicast stores: concurrent with the fused pushes, as in run()
+    if (!mc_stream_) {
+        RS_CUDA(cudaStreamCreateWithFlags(&mc_stream_, cudaStreamNonBlocking));
+        for (auto& e : mc_ev_) RS_CUDA(cudaEventCreate(&e));
+    }
+    RS_CUDA(cudaEventRecord(mc_ev_[0], stream));
+    RS_CUDA(cudaStreamWaitEvent(mc_stream_, mc_ev_[0], 0));
+    const int n0 = launch_multicast(mc_stream_);
+    RS_CUDA(cudaEventRecord(mc_ev_[1], mc_stream_));
+    const int n1 = fused_->launch(stream, 0, 0, sms_, 2, bulk, -1, stage);
+    RS_CUDA(cudaStreamWaitEvent(stream, mc_ev_[1], 0));
+    return n0 + n1;
 }
 
 std::int64_t Executor::channel_bytes(int src_phys, int dst_phys) const {

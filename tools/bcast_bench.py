@@ -68,7 +68,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--chunk-mb", type=int, default=512,
                     help="arena chunk (multicast binds chunk by chunk; 512 MiB = the recommended granularity)")
-    ap.add_argument("--variants", default="push,multicast,dedup,dedup_multicast,dedup_early",
+    ap.add_argument("--variants", default="push,multicast,dedup,dedup_multicast,dedup_early,dedup_early_multicast",
                     help="comma-separated subset to run")
     args = ap.parse_args()
     rank, world, local = dist_env()
@@ -129,12 +129,14 @@ def main():
     todo = args.variants.split(",")
     for name, dedup, multicast, early in (("push", False, False, False), ("multicast", False, True, False),
                                           ("dedup", True, False, False), ("dedup_multicast", True, True, False),
-                                          ("dedup_early", True, False, True)):
+                                          ("dedup_early", True, False, True),
+                                          ("dedup_early_multicast", True, True, True)):
         if name in todo:
             variant(name, dedup, multicast, early)
     if "push" in out:
         out["speedup_vs_push"] = {k: round(out["push"]["ms_min"] / out[k]["ms_min"], 3)
-                                  for k in ("multicast", "dedup", "dedup_multicast", "dedup_early") if k in out}
+                                  for k in ("multicast", "dedup", "dedup_multicast", "dedup_early", "dedup_early_multicast")
+                                  if k in out}
     del ex, tr, arena
     torch.cuda.synchronize()
     dist.barrier()
