@@ -433,16 +433,18 @@ def run_ours(args):
                     "per_gpu_out_in_gb": [[round(p.out_bytes / 1e9, 2), round(p.in_bytes / 1e9, 2)] for p in pl],
                     **nvlink_wire(nv),
                     "hbm_achieved_gbs_rank0": round(achieved_hbm, 1)}
-            # DRAM read + write of one GPU's forward launch from the committed ncu capture of
-            # the same transition at N=2 (tools/p2p_profile.py, one process driving both GPUs)
-            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic_n2_L32.json")
-            if n == 2 and args.layers == 32 and os.path.exists(tp):
+            # DRAM read + write of the binding GPU's forward launch (the longest) from the
+            # committed ncu capture of the same transition at this N (tools/p2p_profile.py, one
+            # process driving all GPUs): its HBM side, local copies r+w + peer-bound reads
+            tname = f"r01_traffic_n{n}_L32.json"
+            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", tname)
+            if args.layers == 32 and os.path.exists(tp):
                 with open(tp) as f:
                     cap = json.load(f)
-                roof["traffic"] = max(l["traffic"] for l in cap["launches"])
-                roof["traffic_algorithmic_hbm_bytes"] = local_rw
-                roof["traffic_source"] = ("profiles/r01_traffic_n2_L32.json (ncu dram__bytes_read.sum + write.sum of "
-                                          "one GPU's launch: its HBM side, local copies r+w + peer-bound reads)")
+                bind = max(cap["launches"], key=lambda l: l["gpu__time_duration.sum"])
+                roof["traffic"] = bind["traffic"]
+                roof["traffic_gpu"] = bind["device"]
+                roof["traffic_source"] = f"profiles/{tname} (ncu dram__bytes_read.sum + write.sum)"
         # planner: ZeRO transfer-list expansion (1.84 M reference SliceTransfers at L=32) on the
         # GPU planner vs the host sweep; the reference's own O(n*m) planner needs hours at L=32
         g_ms, g_runs = ab.expand_timed(dev)

@@ -1,6 +1,6 @@
 """The fused push across GPUs driven from ONE process (so ncu can attach): each GPU's
 executor stores its peer-bound tiles straight into the other GPU's memory (peer access,
-no cudaIpc). Both halves of the north star's forward transition on 2 GPUs, bit-exact,
+no cudaIpc). The north star's forward transition split over 2 (--gpus) GPUs, bit-exact,
 with per-GPU NVLink GB/s from CUDA events.
 
     python tools/p2p_profile.py [--layers 4] [--reps 3]
@@ -26,10 +26,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--gpus", type=int, default=2)
     args = ap.parse_args()
-    G = 2
+    G = args.gpus
     if torch.cuda.device_count() < G:
-        print(json.dumps({"skipped": "needs 2 GPUs"}))
+        print(json.dumps({"skipped": f"needs {G} GPUs"}))
         return
     for a in range(G):
         for b in range(G):
@@ -79,7 +80,7 @@ def main():
         best = ts if best is None or max(ts) < max(best) else best
     bad = sum(e.verify(A.SIDE_DST, seed)[0] for e in ex)
     st = [e.stats() for e in ex]
-    out = {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1 forward, 2 GPUs from one process (peer access)",
+    out = {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1 forward, {G} GPUs from one process (peer access)",
            "ms_per_gpu": [round(t, 3) for t in best],
            "remote_gb_per_gpu": [round(s.remote_bytes / 1e9, 3) for s in st],
            "local_gb_per_gpu": [round(s.local_bytes / 1e9, 3) for s in st],
