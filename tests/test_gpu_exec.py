@@ -436,3 +436,29 @@ def test_north_star_full_size_round_trip():
     torch.cuda.synchronize()
     bad, first = e2.verify(1, SEED)
     assert bad == 0, f"way back: {bad} mismatches, first flat index {first}"
+
+
+@pytest.mark.parametrize("flags", [[], ["--dedup-early"]])
+def test_edm_scale_events_bit_exact(flags):
+    """The EDM end to end (BASELINE config 3 at L=2): DP8 -> DP4 -> DP8 on the side thread
+    while GEMM steps run, blocking and overlapped; every switch verified against canon."""
+    import json
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = "29545" if not flags else "29547"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+                        "--master-addr", "127.0.0.1", "--master-port", port,
+                        os.path.join(root, "tools", "edm_bench.py"), "--layers", "2", "--gemm", "2048"] + flags,
+                       capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])["results"]
+    assert len(res) == 2
+    for name, modes in res.items():
+        for mode in ("blocking", "overlapped"):
+            assert modes[mode]["verified_mismatches"] == 0, (name, mode)
+            assert modes[mode]["bytes_moved"] > 0
