@@ -176,9 +176,13 @@ def test_resolve_peers_elementwise_audit(seed):
     world = rng.choice([4, 8])
     src, dst = _random_cfg(rng, world), _random_cfg(rng, world)
     dst.zero = src.zero  # ZeRO toggling is rejected (routing.hpp:290-291)
+    _audit(m, src, dst)
+
+
+def _audit(m, src, dst, world_src=None, world_dst=None):
     # ZeRO src with tp > 1 can over-source the replicated norms (D2): the reference throws
     # there, so the audit runs on the allow_oversourced extension
-    p = _plan(m, src, dst, allow_oversourced=src.zero)
+    p = _plan(m, src, dst, allow_oversourced=src.zero, world_src=world_src, world_dst=world_dst)
     rs, rd = _param_regions(p, 0), _param_regions(p, 1)
     inbound = {}
     for kind, t, box, s, d, _ in _rows(p):
@@ -209,3 +213,25 @@ def test_resolve_peers_elementwise_audit(seed):
             for e in elems:
                 assert (e in os_.get(d, set())) != ((d, e) in inbound), (d, e)
         assert all(e in od[d] for d, e in inbound)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_elementwise_audit_random_moe_models(seed):
+    # SPEC.md:197/206 audits on random toy models (SPEC.md:538 sizes) with expert tensors,
+    # EP, the alternative rank orders and world-size changes (joiners/leavers, WorldMap
+    # identity(n, m) as the reference's worldmap.hpp:30-79 builds it)
+    rng = random.Random(1000 + seed)
+    m = S.toy_model(rng, max_layers=4, max_per_layer=4, experts=4)
+    src = S.random_cfg(rng, m, max_world=8)
+    dst = S.random_cfg(rng, m, max_world=8, zero=src.zero)
+    _audit(m, src, dst, world_src=list(range(src.world())), world_dst=list(range(dst.world())))
+
+
+def test_fig4_rank3_has_all_three_categories():
+    # SPEC.md:185 Fig. 4, (TP,PP) (2,2) -> (4,1) on 4 ranks: rank 3 sends, retains and receives
+    m = S.Model("fig4", [S.Tensor("w0", (8, 4), layer=0, tp=0), S.Tensor("w1", (8, 4), layer=1, tp=0)],
+                layers=2)
+    p = _plan(m, S.Cfg(tp=2, pp=2), S.Cfg(tp=4))
+    params = [r for r in _rows(p) if r[0] == "param"]
+    assert [r for r in params if r[3] == 3] and [r for r in params if r[4] == 3]
+    assert _param_regions(p, 0)[3]["w1"] & _param_regions(p, 1)[3]["w1"]
