@@ -24,6 +24,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's banner ("NCCL version ...", printed when NCCL_DEBUG is set) goes to stdout by
+# default; keep stdout to the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "reconfig time (s) & effective GB/s per GPU, Llama-3-8B TP8→DP2×TP4+ZeRO-1"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}

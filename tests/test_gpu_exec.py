@@ -34,7 +34,8 @@ def _run_single_gpu(sc, with_grads=False, allow=False, bind_torch=False):
                 for b in range(6):
                     _, nbytes, _ = ex.buffer(side, r, b)
                     if nbytes:
-                        t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                        # zeroed like the oracle's buffers: the 16-B segment padding stays 0
+                        t = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
                         tensors[(side, r, b)] = t
                         ex.bind(side, r, b, t.data_ptr(), nbytes)
     ex.alloc()
@@ -462,3 +463,25 @@ def test_edm_scale_events_bit_exact(flags):
         for mode in ("blocking", "overlapped"):
             assert modes[mode]["verified_mismatches"] == 0, (name, mode)
             assert modes[mode]["bytes_moved"] > 0
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_moe_models_vs_oracle_buffers(seed):
+    """Random toy MoE models (EP, rank orders, world-size changes; the CPU audits in
+    test_spec_kats.py use the same generator) executed on the GPU and compared byte for
+    byte with the oracle's CPU executor on every destination buffer."""
+    import random
+    rng = random.Random(1000 + seed)
+    m = S.toy_model(rng, max_layers=4, max_per_layer=4, experts=4)
+    src = S.random_cfg(rng, m, max_world=8)
+    dst = S.random_cfg(rng, m, max_world=8, zero=src.zero)
+    sc = S.Scenario(m, src, dst, world_src=list(range(src.world())), world_dst=list(range(dst.world())))
+    plan, ex, tensors = _run_single_gpu(sc, allow=src.zero, bind_torch=True)
+    ref = _oracle_dst(sc, allow=src.zero)
+    n = 0
+    for r in range(plan.summary.dst_world):
+        for b in range(6):
+            if (1, r, b) in tensors:
+                assert tensors[(1, r, b)].cpu().numpy().tobytes() == ref.buffer(r, b), (r, b)
+                n += 1
+    assert n > 0
