@@ -24,9 +24,22 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# NCCL's banner ("NCCL version ...", printed when NCCL_DEBUG is set) goes to stdout by
-# default; keep stdout to the one JSON line
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_OUT = sys.stdout
+
+
+def _claim_stdout():
+    """Keep stdout to the one JSON line: anything else written to fd 1 (the "NCCL version"
+    banner NCCL prints from C under torchrun, library chatter) goes to stderr."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def _emit(out):
+    _JSON_OUT.write(json.dumps(out) + "\n")
+    _JSON_OUT.flush()
+
 
 METRIC = "reconfig time (s) & effective GB/s per GPU, Llama-3-8B TP8→DP2×TP4+ZeRO-1"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
@@ -208,7 +221,7 @@ def run_reference(args):
                       "model": "Llama-3-8B", "parallelism": "tp8 -> dp2xtp4 + zero1"},
            "cpu_baseline": cb.describe(v),
            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    _emit(out)
 
 
 def run_ours(args):
@@ -503,7 +516,7 @@ def run_ours(args):
                              "new_layout_gb": round(a.b_bytes / 1e9, 2), "aliased_gb": round(a.aliased_bytes / 1e9, 2),
                              "stages_fwd": arena.stage_order(0), "stages_bwd": arena.stage_order(1),
                              "stage_groups": [fwd.ex.num_stages(), bwd.ex.num_stages()]}
-        print(json.dumps(out), flush=True)
+        _emit(out)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -525,6 +538,7 @@ def main():
     ap.add_argument("--transport", default="fused", choices=["fused", "nccl"],
                     help="fused: one-sided NVLink stores (product); nccl: pack -> NCCL send/recv -> unpack (comparison)")
     args = ap.parse_args()
+    _claim_stdout()
     if args.impl == "reference":
         run_reference(args)
     else:
