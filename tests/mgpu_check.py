@@ -24,6 +24,8 @@ def main():
     vmm = "--vmm" in sys.argv  # shareable VMM buffers mapped by descriptor instead of cudaIpc
     dedup = "--dedup" in sys.argv  # replica dedup: one NVLink crossing per destination GPU
     early = "--dedup-early" in sys.argv  # ... with the copies overlapping the non-replica pushes
+    # --random K: only K random toy MoE models (the generator of tests/test_spec_kats.py)
+    n_random = int(sys.argv[sys.argv.index("--random") + 1]) if "--random" in sys.argv else 0
     dedup = dedup or early
     rank, world, local = dist_env()
     # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box) exercise the N=8 placement: ranks
@@ -41,6 +43,16 @@ def main():
     side = torch.cuda.Stream() if early else None
     scenarios = [S.config2(layers), S.config4(1), S.config3(2)[0], S.config3(2)[1]]
     scenarios += [sc for sc in S.edge_scenarios() if sc.grads == "drop"]  # ragged, identity, join/leave
+    if n_random:
+        import random
+        scenarios = []
+        for k in range(n_random):
+            rng = random.Random(1000 + k)
+            m = S.toy_model(rng, max_layers=4, max_per_layer=4, experts=4)
+            src = S.random_cfg(rng, m, max_world=8)
+            dst = S.random_cfg(rng, m, max_world=8, zero=src.zero)
+            scenarios.append(S.Scenario(m, src, dst, world_src=list(range(src.world())),
+                                        world_dst=list(range(dst.world())), name=f"random-moe-{k}"))
     for sc in scenarios:
         ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)

@@ -205,6 +205,23 @@ def test_multi_gpu_push_over_nvlink():
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("dedup", [[], ["--dedup"]])
+def test_multi_gpu_random_moe_models(dedup):
+    """The random toy MoE models of test_random_moe_models_vs_oracle_buffers pushed across
+    GPUs (one process per GPU, cudaIpc peer stores), forward and back, bit-exact."""
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29537",
+                        os.path.join(root, "tests", "mgpu_check.py"), "1", "--random", "16"] + dedup,
+                       capture_output=True, text=True, timeout=900)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_multi_gpu_arena_stages():
     """N>1 memory-aware arena: VMM buffers shared across processes by POSIX descriptors,
     eager-free aliasing, one global barrier per stage; skipped on a 1-GPU box."""
