@@ -170,6 +170,9 @@ int rs_plan_tensor(const rs_plan_t* p, int index, char* id_buf, int cap, int64_t
 int rs_plan_num_tensors(const rs_plan_t* p, int* n);
 
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
+/* participating physical devices, ascending (WorldMap::participants, worldmap.hpp:60-68);
+ * *n = count (fills at most cap) */
+int rs_plan_participants(const rs_plan_t* p, int* phys, int cap, int* n);
 /* validate_plan: invariants + destination coverage; violations are
  * returned (one per line), not raised. drop >= 0 removes one fragment first (fault
  * injection: box transfers are indexed first, then ZeRO runs). */
@@ -432,6 +435,8 @@ int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t*
  * readback; synchronous on `stream`) */
 int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream);
 int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out);
+/* GPU index (in [0, n_gpus)) the executor places physical device `phys` on */
+int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,14 @@ class RoutingPlan:
         A.check(A.lib().rs_plan_placement(self.h, n_gpus, gpu, C.byref(s)))
         return s
 
+    def participants(self) -> List[int]:
+        """Participating physical devices, ascending (WorldMap::participants)."""
+        n = C.c_int()
+        A.check(A.lib().rs_plan_participants(self.h, None, 0, C.byref(n)))
+        arr = (C.c_int * max(1, n.value))()
+        A.check(A.lib().rs_plan_participants(self.h, arr, n.value, C.byref(n)))
+        return list(arr[: n.value])
+
     def transfers(self, device: int = -1) -> List[A.Transfer_t]:
         p, n = C.c_void_p(), C.c_int64()
         A.check(A.lib().rs_plan_transfers(self.h, device, C.byref(p), C.byref(n)))
@@ -179,6 +187,12 @@ class Executor:
         p, n, g = C.c_void_p(), C.c_int64(), C.c_int()
         A.check(A.lib().rs_exec_buffer(self.h, side, rank, buf, C.byref(p), C.byref(n), C.byref(g)))
         return p.value or 0, n.value, g.value
+
+    def gpu_of_phys(self, phys: int) -> int:
+        """GPU index this executor places physical device `phys` on."""
+        g = C.c_int()
+        A.check(A.lib().rs_exec_gpu_of_phys(self.h, phys, C.byref(g)))
+        return g.value
 
     def ipc_export(self) -> bytes:
         n = C.c_size_t()

@@ -113,6 +113,11 @@ Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConf
         bands = L.bands;
     }
     const MemoryPlan mp = plan_memory(ab, ba, C, with_grads, n_gpus, gpu, groups, bands);
+    // replay the plan chunk by chunk before mapping anything (host-only): a planner
+    // regression must fail here, not corrupt state silently
+    if (const std::int64_t v = simulate_memory_plan(mp, ab, ba); v != 0)
+        throw std::logic_error(strfmt("memory plan: %lld simulated read/write violations on GPU %d",
+                                      static_cast<long long>(v), gpu));
     bands_ = mp.bands;
     const bool shareable = n_gpus > 1;
     order_[0] = mp.order[0];

@@ -747,6 +747,22 @@ int rs_exec_prepare_staged(rs_exec_t* e) {
     });
 }
 
+int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu) {
+    return guarded([&] {
+        *gpu = e->ex->gpu_of_phys(phys);
+        return RS_OK;
+    });
+}
+
+int rs_plan_participants(const rs_plan_t* p, int* phys, int cap, int* n) {
+    return guarded([&] {
+        const auto& r = p->core.routes;
+        *n = static_cast<int>(r.size());
+        for (int i = 0; i < *n && i < cap; ++i) phys[i] = r[static_cast<size_t>(i)].phys;
+        return RS_OK;
+    });
+}
+
 int rs_exec_channel_bytes(const rs_exec_t* e, int src_phys, int dst_phys, int64_t* bytes) {
     return guarded([&] {
         *bytes = e->ex->channel_bytes(src_phys, dst_phys);

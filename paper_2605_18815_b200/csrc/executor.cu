@@ -629,6 +629,12 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         // flight. Both are kept across re-prepares: with peer access enabled every
         // cudaMalloc/cudaFree also edits the peers' mappings (measured: 0.6 s stalls)
         cur ^= 1;
+        // the upload into dev_buf[cur] waits for every launch that read it
+        for (cudaEvent_t e : fences[cur]) {
+            RS_CUDA(cudaStreamWaitEvent(upload, e, 0));
+            fence_pool.push_back(e);
+        }
+        fences[cur].clear();
         if (host.size() * sizeof(Tile) > dev_bytes[cur]) {
             if (dev_buf[cur]) cudaFree(dev_buf[cur]);
             dev_buf[cur] = nullptr;
@@ -657,6 +663,34 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
 TileSet::~TileSet() {
     for (void* p : dev_buf)
         if (p) cudaFree(p);
+    for (auto& v : fences)
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+    for (cudaEvent_t e : fence_pool) cudaEventDestroy(e);
+}
+
+void TileSet::fence(cudaStream_t stream) const {
+    if (!dev) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    RS_CUDA(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return;
+    cudaEvent_t e = nullptr;
+    if (!fence_pool.empty()) {
+        e = fence_pool.back();
+        fence_pool.pop_back();
+    } else {
+        RS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    RS_CUDA(cudaEventRecord(e, stream));
+    fences[cur].push_back(e);
+    // bound the list: one event per stream suffices once a later record on the same
+    // stream exists, but streams are opaque here, so collapse long lists by waiting
+    if (fences[cur].size() > 64) {
+        for (size_t i = 0; i + 1 < fences[cur].size(); ++i) {
+            RS_CUDA(cudaEventSynchronize(fences[cur][i]));
+            fence_pool.push_back(fences[cur][i]);
+        }
+        fences[cur].erase(fences[cur].begin(), fences[cur].end() - 1);
+    }
 }
 
 int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm,
@@ -687,6 +721,7 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
         ++launches;
     }
     RS_CUDA(cudaGetLastError());
+    if (launches) fence(stream);
     return launches;
 }
 
@@ -1027,6 +1062,7 @@ int Executor::launch_multicast(cudaStream_t stream) const {
         ++n;
     }
     RS_CUDA(cudaGetLastError());
+    if (n) mc_->fence(stream);
     return n;
 }
 
@@ -1054,6 +1090,9 @@ int Executor::run_graph(cudaStream_t stream) {
         graph_stream_ = stream;
     }
     RS_CUDA(cudaGraphLaunch(graph_exec_, stream));
+    // descriptor fences for the graph's launches (skipped during capture)
+    if (fused_) fused_->fence(stream);
+    if (mc_) mc_->fence(stream);
     return graph_launches_;
 }
 
@@ -1282,18 +1321,29 @@ std::vector<FillTask> Executor::fill_tasks(int side) const {
     return tasks;
 }
 
-void Executor::upload_tasks(const std::vector<FillTask>& tasks) {
-    if (d_fill_) cudaFree(d_fill_);
-    d_fill_ = nullptr;
+void Executor::upload_tasks(const std::vector<FillTask>& tasks, cudaStream_t stream) {
+    // stream-ordered upload through pinned staging on the stream the fill/verify kernel
+    // runs on (a pageable cudaMemcpy on the legacy stream is not ordered with a
+    // non-blocking caller stream)
     if (tasks.empty()) return;
-    RS_CUDA(cudaMalloc(&d_fill_, tasks.size() * sizeof(FillTask)));
-    RS_CUDA(cudaMemcpy(d_fill_, tasks.data(), tasks.size() * sizeof(FillTask), cudaMemcpyHostToDevice));
+    const size_t bytes = tasks.size() * sizeof(FillTask);
+    RS_CUDA(cudaStreamSynchronize(stream));  // earlier fill/verify kernels may still read d_fill_
+    if (bytes > fill_bytes_) {
+        if (d_fill_) cudaFree(d_fill_);
+        d_fill_ = nullptr;
+        fill_bytes_ = 0;
+        RS_CUDA(cudaMalloc(&d_fill_, bytes));
+        fill_bytes_ = bytes;
+    }
+    if (fill_staging_.size() < bytes) fill_staging_.grow(bytes);
+    std::memcpy(fill_staging_.ptr, tasks.data(), bytes);
+    RS_CUDA(cudaMemcpyAsync(d_fill_, fill_staging_.ptr, bytes, cudaMemcpyHostToDevice, stream));
 }
 
 void Executor::fill(int side, std::uint64_t seed, cudaStream_t stream) {
     RS_CUDA(cudaSetDevice(cfg_.device));
     const std::vector<FillTask> tasks = fill_tasks(side);
-    upload_tasks(tasks);
+    upload_tasks(tasks, stream);
     if (!tasks.empty()) {
         dim3 grid(static_cast<unsigned>(sms_ * 2), static_cast<unsigned>(std::min<size_t>(tasks.size(), 65535)));
         fill_kernel<<<grid, 256, 0, stream>>>(static_cast<const FillTask*>(d_fill_), static_cast<int>(tasks.size()), seed);
@@ -1311,7 +1361,7 @@ void Executor::fill(int side, std::uint64_t seed, cudaStream_t stream) {
 std::int64_t Executor::verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad) {
     RS_CUDA(cudaSetDevice(cfg_.device));
     const std::vector<FillTask> tasks = fill_tasks(side);
-    upload_tasks(tasks);
+    upload_tasks(tasks, stream);
     if (!d_counters_) RS_CUDA(cudaMalloc(&d_counters_, 64));
     unsigned long long* bad = static_cast<unsigned long long*>(d_counters_);
     long long* first = reinterpret_cast<long long*>(static_cast<char*>(d_counters_) + 8);

@@ -491,6 +491,13 @@ void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanC
                 for (int p : touched) read_in_group[static_cast<size_t>(p)] = 0;
                 touched.clear();
                 for (int q = b; q < static_cast<int>(s); ++q) add_reads(static_cast<size_t>(q));
+                // the moved cut relies on aliasing never occurring inside a concurrency
+                // group: stage s must not write what the rebuilt group (b..s-1) reads
+                for (const auto& w : io[s].writes)
+                    if (read_in_group[static_cast<size_t>(w.first)])
+                        throw std::logic_error(strfmt("memory plan: stage %zu writes chunk %d that stage group "
+                                                      "starting at %d still reads (aliasing inside a group)",
+                                                      s, w.first, b));
             }
             add_reads(s);
         }

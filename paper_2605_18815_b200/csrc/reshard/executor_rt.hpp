@@ -78,6 +78,15 @@ struct TileSet {
     void* dev_buf[2] = {nullptr, nullptr};  // used in turn by successive finalizes
     size_t dev_bytes[2] = {0, 0};
     int cur = 1;
+    // descriptor fences: events recorded after every launch that reads dev_buf[i]; the
+    // next finalize into dev_buf[i] makes its upload wait for all of them, so a re-prepare
+    // never overwrites descriptors a kernel still in flight reads (any number of runs may
+    // be outstanding)
+    mutable std::vector<cudaEvent_t> fences[2];
+    mutable std::vector<cudaEvent_t> fence_pool;
+    /// record a fence for the current descriptors on `stream` (skipped while capturing:
+    /// run_graph fences after the graph launch)
+    void fence(cudaStream_t stream) const;
     TileSet() = default;
     TileSet(const TileSet&) = delete;
     TileSet& operator=(const TileSet&) = delete;
@@ -170,7 +179,7 @@ private:
     void compute_dups(const std::vector<CopyOp>& ops);
     int launch_multicast(cudaStream_t stream) const;
     int run_fused(cudaStream_t stream);
-    void upload_tasks(const std::vector<FillTask>& tasks);
+    void upload_tasks(const std::vector<FillTask>& tasks, cudaStream_t stream);
 
     const core::PlanCore& P_;
     ExecConfig cfg_;
@@ -233,6 +242,8 @@ private:
     int stage_bands_ = 1;
     int stage_of(const CopyOp& op) const;
     void* d_fill_ = nullptr;
+    size_t fill_bytes_ = 0;
+    PinnedBuf fill_staging_;
     void* d_counters_ = nullptr;
     bool prepared_ = false;
     bool use_bulk_ = true;  // TMA bulk pipeline for 16-byte-class tiles (RS_COPY_KERNEL=vector to disable)

@@ -73,9 +73,11 @@ class StagedTransition:
         n = plan.summary.num_participants
         self.sched = Schedule(plan, mem_avail or [1 << 62] * n, promote=False)
         ex.prepare_staged()
-        self.phys = list(range(n))  # device index -> phys (identity world maps in the benches)
-        span = (max(self.phys) + 1 + n_gpus - 1) // n_gpus
-        self.gpu_of = [p // span for p in self.phys]
+        # device index -> phys from the plan's WorldMap (join/leave maps need not be
+        # contiguous), GPU placement from the executor
+        self.phys = plan.participants()
+        assert len(self.phys) == n
+        self.gpu_of = [ex.gpu_of_phys(p) for p in self.phys]
 
         def chan(i, p, s):
             nbytes = ex.channel_bytes(self.phys[i], self.phys[p])
@@ -95,6 +97,11 @@ class StagedTransition:
                 if xor_peer(i, s, n) >= 0 for c in [chan(i, xor_peer(i, s, n), s)] if c and (c[0], c[1]) not in done]
         if rest:
             self.plan_stages.append(rest)
+        # every cross-GPU byte this GPU pushes must be on some enumerated channel
+        mine = sum(c[4] for st in self.plan_stages for c in st if c[2] == gpu)
+        if mine != ex.stats().remote_bytes:
+            raise A.ReshardError(A.RS_ERR_INTERNAL, f"staged channels carry {mine} B, executor pushes "
+                                                     f"{ex.stats().remote_bytes} B")
 
     def _ops(self, src, dst):
         n = A.C.c_int64()
@@ -149,6 +156,27 @@ class StagedTransition:
                 self._exchange(chans, stream, per_op=True)
 
 
+def job_token(tag: str = "0", group=None) -> str:
+    """A per-job token for the abstract-namespace socket names and payloads: rank 0 draws a
+    random nonce and broadcasts it (collective over `group`), so two jobs of the same user
+    on one node never connect to each other's listeners, and a payload carrying another
+    token is rejected."""
+    import secrets
+
+    import torch.distributed as dist
+    obj = [secrets.token_hex(8) if dist.get_rank(group) == 0 else None]
+    src = 0 if group is None else dist.get_global_rank(group, 0)
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return f"{tag}-{obj[0]}"
+
+
+def _split_token(payload: bytes, token: str) -> bytes:
+    head, sep, rest = payload.partition(b"\0")
+    if not sep or head.decode(errors="replace") != token:
+        raise A.ReshardError(A.RS_ERR_INTERNAL, "fdx payload from a different job (token mismatch)")
+    return rest
+
+
 def global_stage_cuts(arena, world: int):
     """A barrier is needed before a stage if ANY GPU's aliasing needs it (each GPU plans
     only the chunks it hosts): element-wise max of the cuts over all ranks."""
@@ -175,7 +203,8 @@ def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
     from .api import fdx_close, fdx_listen, fdx_recv, fdx_send
     if world < 2:
         return
-    sock = fdx_listen(f"reshard-{tag}-{rank}")
+    tok = job_token(tag)
+    sock = fdx_listen(f"reshard-{tok}-{rank}")
     dist.barrier()
     errors = []
 
@@ -183,6 +212,12 @@ def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
         try:
             for _ in range(world - 1):
                 fds, table = fdx_recv(sock)
+                try:
+                    table = _split_token(table, tok)
+                except BaseException:
+                    for fd in fds:
+                        os.close(fd)
+                    raise
                 arena.import_peer(fds, table)
         except BaseException as e:  # surfaced below
             errors.append(e)
@@ -194,7 +229,7 @@ def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
             continue
         fds, table = arena.export()
         try:
-            fdx_send(f"reshard-{tag}-{peer}", fds, table)
+            fdx_send(f"reshard-{tok}-{peer}", fds, tok.encode() + b"\0" + table)
         finally:
             for fd in fds:
                 os.close(fd)
@@ -268,7 +303,8 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
                     table.append((r, b, n))
     if world < 2:
         return out
-    sock = fdx_listen(f"reshard-vmm-{tag}-{rank}")
+    tok = job_token(tag, group)
+    sock = fdx_listen(f"reshard-vmm-{tok}-{rank}")
     dist.barrier(group=group)
     errors = []
     received = []
@@ -277,6 +313,12 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
         try:
             for _ in range(world - 1):
                 fds, payload = fdx_recv(sock)
+                try:
+                    payload = _split_token(payload, tok)
+                except BaseException:
+                    for fd in fds:
+                        os.close(fd)
+                    raise
                 rows = json.loads(payload.decode())  # plain data: no code runs on receipt
                 for fd, (r, b, n) in zip(fds, rows):
                     received.append((r, b, n, VmmBuffer.import_fd(fd, n, device)))
@@ -290,7 +332,7 @@ def share_buffers(tr: "Transition", rank: int, world: int, device: int, tag: str
             continue
         fds = [out[(A.SIDE_DST, r, b)].export_fd() for r, b, _ in table]
         try:
-            fdx_send(f"reshard-vmm-{tag}-{peer}", fds, json.dumps(table).encode())
+            fdx_send(f"reshard-vmm-{tok}-{peer}", fds, tok.encode() + b"\0" + json.dumps(table).encode())
         finally:
             for fd in fds:
                 os.close(fd)
@@ -336,7 +378,8 @@ def setup_multicast(source, ex: Executor, rank: int, world: int, device: int, ta
             mc.bind_vmm(source[(side, r, b)])
 
     expect = sum(1 for g in groups if rank in list(g.member_gpu[: g.n_members]) and g.root_gpu != rank)
-    sock = fdx_listen(f"reshard-mc-{tag}-{rank}")
+    tok = job_token(tag, group)
+    sock = fdx_listen(f"reshard-mc-{tok}-{rank}")
     dist.barrier(group=group)
     errors = []
 
@@ -344,6 +387,12 @@ def setup_multicast(source, ex: Executor, rank: int, world: int, device: int, ta
         try:
             for _ in range(expect):
                 fds, payload = fdx_recv(sock)
+                try:
+                    payload = _split_token(payload, tok)
+                except BaseException:
+                    for fd in fds:
+                        os.close(fd)
+                    raise
                 gid = int(payload.decode())
                 mcs[gid] = Multicast.import_fd(fds[0], size[gid])
         except BaseException as e:  # surfaced below
@@ -360,7 +409,7 @@ def setup_multicast(source, ex: Executor, rank: int, world: int, device: int, ta
         for peer in members:
             fd = mc.export_fd()
             try:
-                fdx_send(f"reshard-mc-{tag}-{peer}", [fd], str(g.id).encode())
+                fdx_send(f"reshard-mc-{tok}-{peer}", [fd], tok.encode() + b"\0" + str(g.id).encode())
             finally:
                 os.close(fd)
     t.join()
