@@ -281,11 +281,7 @@ std::vector<core::BoxXfer> box_routes_gpu(const core::PlanCore& P, int device, d
 /// Expand on `device`. Runs of D2-overridden destinations come from the host plan.
 std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device, double* kernel_ms) {
     RS_CUDA_P(cudaSetDevice(device));
-    std::vector<stair::Triple> trip;
-    std::vector<char> d2(static_cast<size_t>(P.dst_cfg.world_size()), 0);
-    for (const core::FlatXfer& f : P.d2_runs) d2[static_cast<size_t>(f.dst)] = 1;
-    for (const stair::Triple& T : P.triples)
-        if (!d2[static_cast<size_t>(T.dst)]) trip.push_back(T);
+    const std::vector<stair::Triple>& trip = P.triples;
     std::vector<core::FlatXfer> out;
     if (!trip.empty()) {
         std::vector<long long> off(trip.size());
@@ -347,16 +343,9 @@ std::vector<core::FlatXfer> expand_flat_gpu(const core::PlanCore& P, int device,
         cudaEventDestroy(e0), cudaEventDestroy(e1), cudaEventDestroy(ea), cudaEventDestroy(eb);
         cudaStreamDestroy(s);
     }
-    if (P.d2_runs.empty()) return out;
-    std::vector<core::FlatXfer> merged;
-    merged.reserve(out.size() + P.d2_runs.size());
-    auto less = [](const core::FlatXfer& a, const core::FlatXfer& b) {
-        if (a.src != b.src) return a.src < b.src;
-        if (a.dst != b.dst) return a.dst < b.dst;
-        return a.lo < b.lo;
-    };
-    std::merge(out.begin(), out.end(), P.d2_runs.begin(), P.d2_runs.end(), std::back_inserter(merged), less);
-    return merged;
+    // D2 extension: the runs inside over-sourced intervals are replaced (host, a few
+    // hundred intervals)
+    return core::apply_d2(P, std::move(out));
 }
 
 }  // namespace gpuplan

@@ -143,28 +143,27 @@ std::vector<CopyOp> build_ops(const PlanCore& P) {
     for (const stair::Triple& T : P.triples)
         if (!overridden(T.dst, T.tensor)) E.triple(T);
     for (const stair::Triple& T : P.retain_triples) E.triple(T);
-    // only the overridden tensors of a D2 route come from runs. Runs are sorted by
-    // (src, dst, lo) and disjoint within a (src, dst) group, so each overridden tensor's
-    // runs are found by binary search (the D2 list holds every run of the route: ~1.8 M
-    // for the north star's way back, of which a few hundred belong to flagged tensors)
-    const std::vector<core::FlatXfer>& R = P.d2_runs;
-    const auto& ents = P.space->entries();
-    for (size_t i = 0; i < R.size();) {
-        const int src = R[i].src, dst = R[i].dst;
-        const size_t e = static_cast<size_t>(
-            std::partition_point(R.begin() + static_cast<std::ptrdiff_t>(i), R.end(),
-                                 [&](const core::FlatXfer& f) { return f.src == src && f.dst == dst; }) -
-            R.begin());
-        for (int t = 0; t < nt; ++t) {
-            if (!overridden(dst, t)) continue;
-            const std::int64_t tlo = ents[static_cast<size_t>(t)].offset;
-            const std::int64_t thi = tlo + ents[static_cast<size_t>(t)].spec.numel();
-            auto it = std::partition_point(R.begin() + static_cast<std::ptrdiff_t>(i), R.begin() + static_cast<std::ptrdiff_t>(e),
-                                           [&](const core::FlatXfer& f) { return f.hi <= tlo; });
-            for (; it != R.begin() + static_cast<std::ptrdiff_t>(e) && it->lo < thi; ++it)
-                E.flat_run(core::FlatXfer{std::max(it->lo, tlo), std::min(it->hi, thi), src, dst});
+    // D2 extension: a tensor of a destination rank holding multi-candidate elements is
+    // re-derived from its triples' runs minus the segments another source was chosen for
+    // (d2_multi, (dst, lo) order); every other element has exactly one source
+    if (!P.d2_tensor_dst.empty()) {
+        std::vector<core::FlatXfer> v;
+        for (const stair::Triple& T : P.triples) {
+            if (!overridden(T.dst, T.tensor)) continue;
+            v.clear();
+            core::append_runs(T, v);
+            auto m0 = std::partition_point(P.d2_multi.begin(), P.d2_multi.end(),
+                                           [&](const core::PlanCore::D2Multi& m) { return m.dst < T.dst; });
+            for (const core::FlatXfer& f : v) {
+                std::int64_t at = f.lo;
+                for (auto m = m0; m != P.d2_multi.end() && m->dst == T.dst && m->lo < f.hi; ++m) {
+                    if (m->hi <= at || m->chosen == T.src) continue;
+                    if (m->lo > at) E.flat_run(core::FlatXfer{at, m->lo, T.src, T.dst});
+                    at = std::max(at, m->hi);
+                }
+                if (at < f.hi) E.flat_run(core::FlatXfer{at, f.hi, T.src, T.dst});
+            }
         }
-        i = e;
     }
     if (P.has_scalars)
         for (int j = 0; j < P.dst_cfg.world_size(); ++j)

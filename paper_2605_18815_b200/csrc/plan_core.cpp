@@ -112,7 +112,8 @@ bool make_triple(const ModelSpace& space, int t, const RankGeom& k, const RankGe
     return true;
 }
 
-/// Append runs of a triple (band sweep) with normalize_intervals-style merging.
+}  // namespace
+
 void append_runs(const stair::Triple& T, std::vector<FlatXfer>& out) {
     for_each_band(T, [&](const std::int64_t* p, std::int64_t u, std::int64_t v, const stair::Iv* cols, int n) {
         const bool full = n == 1 && cols[0].lo == 0 && cols[0].hi == T.t.cols;
@@ -130,6 +131,8 @@ void append_runs(const stair::Triple& T, std::vector<FlatXfer>& out) {
             for (int i = 0; i < n; ++i) push(stair::flat_of(T.t, p, r, cols[i].lo), stair::flat_of(T.t, p, r, cols[i].hi));
     });
 }
+
+namespace {
 
 std::int64_t triple_count(const stair::Triple& T) {
     std::int64_t n = 0;
@@ -236,71 +239,147 @@ Side build_side(const ModelSpace& space, const ParallelConfig& cfg) {
 
 namespace {
 
-/// D2 handling for one destination rank: full runs from every source, merged to
-/// the reference's recv intervals (maximal runs of D_j \ S_own), over-coverage
-/// detection, and (allow mode) uniform-candidate re-splitting of over-sourced ivs.
-struct D2Result {
-    bool over = false;
-    Interval first_bad_iv{0, 0};
-    std::vector<FlatXfer> final_runs;  // allow mode: the route's final runs, (src, lo) order
+/// D2 handling for one destination rank. Only tensors replicated across source TP ranks
+/// can be covered by two source shards, so over-sourced recv intervals are found from
+/// the overlaps of their runs and grown to the reference's maximal recv intervals
+/// (normalize_intervals: connected under lo <= hi) through the runs of every source.
+/// Inside them (allow mode) the elements are re-split into maximal runs with a uniform
+/// candidate set and one source is chosen per run (proximity rule or balance cursor).
+struct D2Route {
+    std::vector<Interval> bad;       // over-sourced recv intervals, ascending
+    std::vector<FlatXfer> patch;     // allow mode: the runs inside them, lo order
+    std::vector<PlanCore::D2Multi> multi;
+    std::int64_t regular_runs = 0, regular_elems = 0;  // the triples' runs inside `bad`
+    std::int64_t patch_elems = 0;
     std::vector<int> flagged_tensors;
 };
 
-D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Triple*>& trip, bool build_final,
-                  std::int64_t* cursor) {
-    D2Result R;
-    struct Piece {
-        std::int64_t lo, hi;
-        int src;
+D2Route d2_route(const PlanCore& P, int j, const std::vector<const stair::Triple*>& trip, bool resolve,
+                 std::int64_t* cursor) {
+    D2Route R;
+    const auto& ents = P.space->entries();
+    const int nt = static_cast<int>(ents.size());
+    // runs of a triple, expanded on first use: only the triples around over-sourced
+    // intervals are ever expanded (a handful of the route's ~2,000)
+    std::vector<std::vector<FlatXfer>> cache(trip.size());
+    std::vector<char> done(trip.size(), 0);
+    auto runs = [&](int ti) -> const std::vector<FlatXfer>& {
+        if (!done[static_cast<size_t>(ti)]) {
+            append_runs(*trip[static_cast<size_t>(ti)], cache[static_cast<size_t>(ti)]);
+            done[static_cast<size_t>(ti)] = 1;
+        }
+        return cache[static_cast<size_t>(ti)];
     };
-    std::vector<Piece> pieces;
-    for (const stair::Triple* T : trip) {
-        std::vector<FlatXfer> v;
-        append_runs(*T, v);
-        for (const FlatXfer& f : v) pieces.push_back({f.lo, f.hi, f.src});
-    }
-    (void)j;
-    std::sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) {
-        return a.lo != b.lo ? a.lo < b.lo : (a.hi != b.hi ? a.hi < b.hi : a.src < b.src);
-    });
-    // recv ivs = union of pieces (every recv element is covered by >= 1 source)
-    std::vector<Interval> ivs, multi;
-    for (const Piece& p : pieces) {
-        if (!ivs.empty() && p.lo <= ivs.back().hi) ivs.back().hi = std::max(ivs.back().hi, p.hi);
-        else ivs.push_back({p.lo, p.hi});
-    }
-    // over-coverage per iv: total piece length vs iv length
-    size_t pi = 0;
-    std::vector<std::int64_t> bounds;
-    for (const Interval& iv : ivs) {
-        size_t first = pi;
-        std::int64_t total = 0;
-        while (pi < pieces.size() && pieces[pi].lo < iv.hi) total += pieces[pi].hi - pieces[pi].lo, ++pi;
-        const bool bad = total != iv.length();
-        if (bad && !R.over) {
-            R.over = true;
-            R.first_bad_iv = iv;
+    // overlapping runs of the replicated tensors seed the over-sourced intervals
+    std::vector<FlatXfer> rep;
+    std::vector<int> slot;                      // src rank -> slot
+    std::vector<int> slot_src;                  // slot -> src rank
+    std::vector<std::vector<int>> tri;          // [slot][tensor] -> index in trip or -1
+    for (size_t ti = 0; ti < trip.size(); ++ti) {
+        const stair::Triple* T = trip[ti];
+        if (T->src >= static_cast<int>(slot.size())) slot.resize(static_cast<size_t>(T->src) + 1, -1);
+        int& k = slot[static_cast<size_t>(T->src)];
+        if (k < 0) {
+            k = static_cast<int>(tri.size());
+            tri.emplace_back(static_cast<size_t>(nt), -1);
+            slot_src.push_back(T->src);
         }
-        if (!build_final) continue;
-        if (!bad) {
-            // pieces partition the iv; consecutive pieces of one source abut -> one run
-            for (size_t q = first; q < pi; ++q) {
-                if (q > first && R.final_runs.back().src == pieces[q].src && R.final_runs.back().hi == pieces[q].lo)
-                    R.final_runs.back().hi = pieces[q].hi;
-                else
-                    R.final_runs.push_back({pieces[q].lo, pieces[q].hi, pieces[q].src, -1});
+        tri[static_cast<size_t>(k)][static_cast<size_t>(T->tensor)] = static_cast<int>(ti);
+        if (!ents[static_cast<size_t>(T->tensor)].spec.tp_shard_axis) {
+            const auto& v = runs(static_cast<int>(ti));
+            rep.insert(rep.end(), v.begin(), v.end());
+        }
+    }
+    std::sort(rep.begin(), rep.end(), [](const FlatXfer& a, const FlatXfer& b) { return a.lo < b.lo; });
+    std::vector<Interval> seeds;
+    for (size_t i = 0; i < rep.size();) {
+        std::int64_t reach = rep[i].hi;
+        bool over = false;
+        size_t e = i + 1;
+        for (; e < rep.size() && rep[e].lo <= reach; ++e) {
+            over = over || rep[e].lo < reach;
+            reach = std::max(reach, rep[e].hi);
+        }
+        if (over) seeds.push_back({rep[i].lo, reach});
+        i = e;
+    }
+    if (seeds.empty()) return R;
+    const std::int64_t space_end = ents.back().offset + ents.back().spec.numel();
+    auto tensor_at = [&](std::int64_t x) {
+        auto it = std::upper_bound(ents.begin(), ents.end(), x, [](std::int64_t v, const ModelSpace::Entry& e) { return v < e.offset; });
+        return static_cast<int>(it - ents.begin()) - 1;
+    };
+    // grow each seed to its recv interval (normalize_intervals: connected under lo <= hi)
+    for (const Interval& sd : seeds) {
+        if (!R.bad.empty() && sd.lo <= R.bad.back().hi) continue;  // already inside
+        Interval iv = sd;
+        for (bool changed = true; changed;) {
+            changed = false;
+            for (size_t k = 0; k < tri.size(); ++k) {
+                for (std::int64_t x : {iv.hi - 1, iv.hi}) {  // a run with lo <= hi < its hi
+                    if (x < 0 || x >= space_end) continue;
+                    const int ti = tri[k][static_cast<size_t>(tensor_at(x))];
+                    if (ti < 0) continue;
+                    const auto& l = runs(ti);
+                    auto it = std::upper_bound(l.begin(), l.end(), iv.hi, [](std::int64_t y, const FlatXfer& f) { return y < f.lo; });
+                    if (it != l.begin() && std::prev(it)->hi > iv.hi) iv.hi = std::prev(it)->hi, changed = true;
+                }
+                if (iv.lo > 0) {  // a run with lo < lo_iv <= its hi
+                    const int ti = tri[k][static_cast<size_t>(tensor_at(iv.lo - 1))];
+                    if (ti < 0) continue;
+                    const auto& l = runs(ti);
+                    auto jt = std::lower_bound(l.begin(), l.end(), iv.lo, [](const FlatXfer& f, std::int64_t y) { return f.hi < y; });
+                    if (jt != l.end() && jt->lo < iv.lo) iv.lo = jt->lo, changed = true;
+                }
             }
-            continue;
         }
-        // uniform-candidate runs (oracle.c plan_optimizer D2 extension)
+        if (!R.bad.empty() && iv.lo <= R.bad.back().hi) R.bad.back().hi = std::max(R.bad.back().hi, iv.hi);
+        else R.bad.push_back(iv);
+    }
+    // every triple run inside an interval (per source, ascending)
+    auto for_runs_in = [&](const Interval& iv, auto&& fn) {
+        const int t0 = tensor_at(iv.lo), t1 = tensor_at(iv.hi - 1);
+        for (size_t k = 0; k < tri.size(); ++k)
+            for (int t = t0; t <= t1; ++t) {
+                const int ti = tri[k][static_cast<size_t>(t)];
+                if (ti < 0) continue;
+                const auto& l = runs(ti);
+                auto it = std::lower_bound(l.begin(), l.end(), iv.lo, [](const FlatXfer& f, std::int64_t y) { return f.hi <= y; });
+                for (; it != l.end() && it->lo < iv.hi; ++it) fn(static_cast<int>(k), *it);
+            }
+    };
+    struct Ev {
+        std::int64_t pos;
+        int src, d;
+    };
+    std::vector<Ev> events;
+    std::vector<std::int64_t> bounds;
+    std::vector<int> cover(slot.size(), 0), cs, run_c;
+    std::vector<Interval> multi;
+    std::vector<std::int64_t> prev_hi(tri.size());
+    for (const Interval& iv : R.bad) {
+        events.clear();
         bounds.clear();
         bounds.push_back(iv.lo);
         bounds.push_back(iv.hi);
-        for (size_t q = first; q < pi; ++q) bounds.push_back(pieces[q].lo), bounds.push_back(pieces[q].hi);
+        std::fill(prev_hi.begin(), prev_hi.end(), -1);
+        for_runs_in(iv, [&](int k, const FlatXfer& f) {
+            // the plan's runs merge abutting runs of one source across tensors
+            if (f.lo != prev_hi[static_cast<size_t>(k)]) ++R.regular_runs;
+            prev_hi[static_cast<size_t>(k)] = f.hi;
+            R.regular_elems += f.hi - f.lo;
+            events.push_back({f.lo, f.src, +1});
+            events.push_back({f.hi, f.src, -1});
+            bounds.push_back(f.lo);
+            bounds.push_back(f.hi);
+        });
+        if (!resolve) continue;
         std::sort(bounds.begin(), bounds.end());
         bounds.erase(std::unique(bounds.begin(), bounds.end()), bounds.end());
+        std::sort(events.begin(), events.end(), [](const Ev& a, const Ev& b) { return a.pos < b.pos; });
+        std::fill(cover.begin(), cover.end(), 0);
         std::int64_t run_lo = -1, run_hi = -1;
-        std::vector<int> run_c, cs;
+        run_c.clear();
         auto flush = [&]() {
             if (run_c.empty()) return;
             int chosen;
@@ -316,16 +395,20 @@ D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Tripl
                     }
                 if (chosen < 0) chosen = run_c.front();
             }
-            R.final_runs.push_back({run_lo, run_hi, chosen, -1});
-            if (run_c.size() > 1) multi.push_back({run_lo, run_hi});
+            R.patch.push_back({run_lo, run_hi, chosen, j});
+            R.patch_elems += run_hi - run_lo;
+            if (run_c.size() > 1) {
+                multi.push_back({run_lo, run_hi});
+                R.multi.push_back({run_lo, run_hi, j, chosen});
+            }
         };
+        size_t ei = 0;
         for (size_t b = 0; b + 1 < bounds.size(); ++b) {
             const std::int64_t lo = bounds[b], hi = bounds[b + 1];
+            for (; ei < events.size() && events[ei].pos <= lo; ++ei) cover[static_cast<size_t>(events[ei].src)] += events[ei].d;
             cs.clear();
-            for (size_t q = first; q < pi; ++q)
-                if (pieces[q].lo <= lo && hi <= pieces[q].hi) cs.push_back(pieces[q].src);
-            std::sort(cs.begin(), cs.end());
-            cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+            for (size_t c = 0; c < cover.size(); ++c)
+                if (cover[c] > 0) cs.push_back(static_cast<int>(c));
             if (!run_c.empty() && run_hi == lo && cs == run_c) {
                 run_hi = hi;
             } else {
@@ -337,12 +420,10 @@ D2Result d2_route(const PlanCore& P, int j, const std::vector<const stair::Tripl
         }
         flush();
     }
-    // tensors holding over-sourced elements: the executor takes their optimizer moves from
-    // the resolved runs (a choice among replicas); elsewhere every element has a single
-    // source, exactly as in the triples
+    // tensors holding multi-candidate elements: the executor re-derives their moves
     for (const stair::Triple* T : trip) {
         const std::int64_t tlo = T->t.off;
-        const std::int64_t thi = tlo + P.space->entries()[static_cast<size_t>(T->tensor)].spec.numel();
+        const std::int64_t thi = tlo + ents[static_cast<size_t>(T->tensor)].spec.numel();
         for (const Interval& m : multi)
             if (m.lo < thi && tlo < m.hi) {
                 R.flagged_tensors.push_back(T->tensor);
@@ -544,79 +625,63 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         bool d2_possible = false;
         if (srcc.tp > 1)
             for (const auto& e : space.entries()) d2_possible |= !e.spec.tp_shard_axis.has_value();
-        std::vector<char> d2_dst(static_cast<size_t>(ndst), 0);
+        std::int64_t d2_regular_runs = 0, d2_regular_elems = 0, d2_patch_elems = 0;
         if (d2_possible) {
             // cursor position after box pendings (params, grads) for the extension
             std::int64_t cur = cursor;
             for (const RouteInfo& r : P.routes) {
                 if (r.dst_rank < 0) continue;
                 const int j = r.dst_rank;
-                std::vector<const stair::Triple*> rep;
-                for (const stair::Triple* T : by_dst[static_cast<size_t>(j)])
-                    if (!space.entries()[static_cast<size_t>(T->tensor)].spec.tp_shard_axis) rep.push_back(T);
-                if (rep.empty()) continue;
-                // quick over-coverage test on replicated tensors only
-                std::vector<FlatXfer> v;
-                for (const stair::Triple* T : rep) append_runs(*T, v);
-                std::sort(v.begin(), v.end(), [](const FlatXfer& a, const FlatXfer& b) { return a.lo < b.lo; });
-                bool over = false;
-                std::int64_t reach = v.empty() ? 0 : v[0].hi;
-                for (size_t i = 1; i < v.size() && !over; ++i) {
-                    over = v[i].lo < reach;
-                    reach = std::max(reach, v[i].hi);
-                }
-                if (!over) continue;
-                D2Result R = d2_route(P, j, by_dst[static_cast<size_t>(j)], allow_oversourced, &cur);
-                if (!R.over) continue;
+                D2Route R = d2_route(P, j, by_dst[static_cast<size_t>(j)], allow_oversourced, &cur);
+                if (R.bad.empty()) continue;
                 if (!allow_oversourced)
                     throw ConfigError(strfmt("unreachable state: optimizer interval [%lld:%lld] for device %d not fully sourced",
-                                             static_cast<long long>(R.first_bad_iv.lo),
-                                             static_cast<long long>(R.first_bad_iv.hi), r.phys));
-                d2_dst[static_cast<size_t>(j)] = 1;
+                                             static_cast<long long>(R.bad.front().lo),
+                                             static_cast<long long>(R.bad.front().hi), r.phys));
+                if (P.d2_bad.empty()) P.d2_bad.resize(static_cast<size_t>(ndst));
+                P.d2_bad[static_cast<size_t>(j)] = std::move(R.bad);
                 if (P.d2_tensor_dst.empty()) P.d2_tensor_dst.assign(static_cast<size_t>(ndst) * nt, 0);
                 for (int t : R.flagged_tensors) P.d2_tensor_dst[static_cast<size_t>(j) * nt + t] = 1;
-                for (FlatXfer& f : R.final_runs) {
-                    f.dst = j;
-                    P.d2_runs.push_back(f);
-                }
+                P.d2_runs.insert(P.d2_runs.end(), R.patch.begin(), R.patch.end());
+                P.d2_multi.insert(P.d2_multi.end(), R.multi.begin(), R.multi.end());
+                d2_regular_runs += R.regular_runs;
+                d2_regular_elems += R.regular_elems;
+                d2_patch_elems += R.patch_elems;
             }
+            std::sort(P.d2_multi.begin(), P.d2_multi.end(), [](const PlanCore::D2Multi& a, const PlanCore::D2Multi& b) {
+                return a.dst != b.dst ? a.dst < b.dst : a.lo < b.lo;
+            });
+            // uniform pieces are separate pendings: D2 runs are kept as produced
             std::stable_sort(P.d2_runs.begin(), P.d2_runs.end(), [](const FlatXfer& a, const FlatXfer& b) {
                 if (a.src != b.src) return a.src < b.src;
                 if (a.dst != b.dst) return a.dst < b.dst;
                 return a.lo < b.lo;
             });
-            // merge abutting runs of the same (src,dst) only where the reference would:
-            // D2 runs are kept as produced (uniform pieces are separate pendings).
         }
-        // transfer count + bytes: non-D2 routes from triples, D2 routes from final runs
-        std::vector<FlatXfer> tmp;
-        for (const stair::Triple& T : P.triples) {
-            if (d2_dst[static_cast<size_t>(T.dst)]) continue;
-            flat_elems += triple_count(T);
-        }
-        for (const FlatXfer& f : P.d2_runs) flat_elems += f.hi - f.lo;
-        P.n_flat = -1;  // resolved lazily by expand_* (count needs merging)
+        // transfer count + bytes: the triples' runs, minus those inside over-sourced
+        // intervals, plus the D2 runs that replace them
+        for (const stair::Triple& T : P.triples) flat_elems += triple_count(T);
+        flat_elems += d2_patch_elems - d2_regular_elems;
         {
             // count transfers exactly: merged runs per (src,dst) group
+            // per band in O(1): rows x pieces, minus row-to-row merges when the pattern
+            // wraps (first piece at column 0, last at the row end), minus a merge with the
+            // previous band / triple of the same (src, dst) when they abut
             std::int64_t cnt = 0;
             int cs = -1, cd = -1;
             std::int64_t last_hi = -1;
-            for (const stair::Triple& T : P.triples) {
-                if (d2_dst[static_cast<size_t>(T.dst)]) continue;
-                tmp.clear();
-                append_runs(T, tmp);
-                for (const FlatXfer& f : tmp) {
-                    if (f.src == cs && f.dst == cd && f.lo == last_hi) {
-                        last_hi = f.hi;
-                        continue;
-                    }
-                    ++cnt;
-                    cs = f.src;
-                    cd = f.dst;
-                    last_hi = f.hi;
-                }
-            }
-            P.n_flat = cnt + static_cast<std::int64_t>(P.d2_runs.size());
+            for (const stair::Triple& T : P.triples)
+                for_each_band(T, [&](const std::int64_t* p, std::int64_t u, std::int64_t v, const stair::Iv* cols, int n) {
+                    const std::int64_t first_lo = stair::flat_of(T.t, p, u, cols[0].lo);
+                    const bool wrap = cols[0].lo == 0 && cols[n - 1].hi == T.t.cols;
+                    std::int64_t c = (v - u) * n - (wrap ? v - u - 1 : 0);
+                    if (T.src == cs && T.dst == cd && first_lo == last_hi) --c;
+                    cnt += c;
+                    cs = T.src;
+                    cd = T.dst;
+                    last_hi = stair::flat_of(T.t, p, v - 1, cols[n - 1].hi);
+                });
+            P.n_flat = cnt - d2_regular_runs + static_cast<std::int64_t>(P.d2_runs.size());
         }
     }
 
@@ -639,42 +704,47 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     return P;
 }
 
-namespace {
-bool is_d2(const PlanCore& P, int dst) {
-    for (const FlatXfer& f : P.d2_runs)
-        if (f.dst == dst) return true;
-    return false;
-}
-
-std::vector<FlatXfer> merge_with_d2(const PlanCore& P, std::vector<FlatXfer> base) {
-    if (P.d2_runs.empty()) return base;
+std::vector<FlatXfer> apply_d2(const PlanCore& P, std::vector<FlatXfer> base) {
+    if (P.d2_bad.empty()) return base;
+    auto less = [](const FlatXfer& a, const FlatXfer& b) {
+        if (a.src != b.src) return a.src < b.src;
+        if (a.dst != b.dst) return a.dst < b.dst;
+        return a.lo < b.lo;
+    };
+    // a triple run lies inside or outside each recv interval (intervals are maximal under
+    // abutting), so testing its start suffices; base is (src, dst, lo)-sorted: one pointer
+    // into the destination's sorted bad list per (src, dst) group
+    std::vector<FlatXfer> kept;
+    kept.reserve(base.size());
+    int gs = -1, gd = -1;
+    size_t q = 0;
+    const std::vector<Interval>* bad = nullptr;
+    for (const FlatXfer& f : base) {
+        if (f.src != gs || f.dst != gd) {
+            gs = f.src, gd = f.dst, q = 0;
+            bad = static_cast<size_t>(f.dst) < P.d2_bad.size() ? &P.d2_bad[static_cast<size_t>(f.dst)] : nullptr;
+        }
+        if (bad && !bad->empty()) {
+            while (q < bad->size() && (*bad)[q].hi <= f.lo) ++q;
+            if (q < bad->size() && (*bad)[q].lo <= f.lo) continue;
+        }
+        kept.push_back(f);
+    }
     std::vector<FlatXfer> out;
-    out.reserve(base.size() + P.d2_runs.size());
-    std::merge(base.begin(), base.end(), P.d2_runs.begin(), P.d2_runs.end(), std::back_inserter(out),
-               [](const FlatXfer& a, const FlatXfer& b) {
-                   if (a.src != b.src) return a.src < b.src;
-                   if (a.dst != b.dst) return a.dst < b.dst;
-                   return a.lo < b.lo;
-               });
+    out.reserve(kept.size() + P.d2_runs.size());
+    std::merge(kept.begin(), kept.end(), P.d2_runs.begin(), P.d2_runs.end(), std::back_inserter(out), less);
     return out;
 }
-}  // namespace
 
 std::vector<FlatXfer> expand_flat_host(const PlanCore& P) {
     std::vector<FlatXfer> out;
-    std::vector<char> skip(static_cast<size_t>(P.dst_cfg.world_size()), 0);
-    for (int j = 0; j < P.dst_cfg.world_size(); ++j) skip[static_cast<size_t>(j)] = is_d2(P, j);
-    for (const stair::Triple& T : P.triples)
-        if (!skip[static_cast<size_t>(T.dst)]) append_runs(T, out);
-    return merge_with_d2(P, std::move(out));
+    for (const stair::Triple& T : P.triples) append_runs(T, out);
+    return apply_d2(P, std::move(out));
 }
 
 std::vector<FlatXfer> expand_flat_rows_host(const PlanCore& P) {
     std::vector<FlatXfer> out;
-    std::vector<char> skip(static_cast<size_t>(P.dst_cfg.world_size()), 0);
-    for (int j = 0; j < P.dst_cfg.world_size(); ++j) skip[static_cast<size_t>(j)] = is_d2(P, j);
     for (const stair::Triple& T : P.triples) {
-        if (skip[static_cast<size_t>(T.dst)]) continue;
         for (std::int64_t q = 0; q < T.nrows; ++q) {
             stair::Iv r[2];
             const int n = stair::triple_row_runs(T, q, r);
@@ -686,7 +756,7 @@ std::vector<FlatXfer> expand_flat_rows_host(const PlanCore& P) {
             }
         }
     }
-    return merge_with_d2(P, std::move(out));
+    return apply_d2(P, std::move(out));
 }
 
 std::string dump(const PlanCore& P, const std::vector<FlatXfer>& flat) { return dump(P, P.box, flat); }

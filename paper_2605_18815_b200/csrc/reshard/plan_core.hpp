@@ -112,11 +112,20 @@ struct PlanCore {
     std::vector<BoxXfer> box_retain;  // same-device copies (executor only)
     std::vector<stair::Triple> triples;         // ZeRO moves, (src, dst, tensor) order
     std::vector<stair::Triple> retain_triples;  // ZeRO same-device copies
-    // D2 extension (allow_oversourced): routes whose recv intervals are over-sourced
-    // get their optimizer runs from `d2_runs` instead of `triples` for the listed
-    // tensors (parity unpinned).
-    std::vector<FlatXfer> d2_runs;          // canonical order
-    std::vector<std::uint8_t> d2_tensor_dst; // [dst_rank * ntensors + t] -> 1 if overridden
+    // D2 extension (allow_oversourced, parity unpinned). Over-sourced
+    // recv intervals (`d2_bad`, per destination rank, ascending) replace the triples' runs
+    // inside them by `d2_runs`: maximal runs with a uniform candidate set, one source
+    // chosen per run. Outside them the triples' runs are the plan's runs unchanged. The
+    // executor re-derives only tensors holding multi-candidate elements (`d2_tensor_dst`)
+    // from their triples minus the segments another source was chosen for (`d2_multi`).
+    struct D2Multi {
+        std::int64_t lo = 0, hi = 0;
+        int dst = -1, chosen = -1;
+    };
+    std::vector<FlatXfer> d2_runs;                  // canonical (src, dst, lo) order
+    std::vector<std::vector<Interval>> d2_bad;      // [dst rank] over-sourced recv ivs
+    std::vector<D2Multi> d2_multi;                  // (dst, lo) order
+    std::vector<std::uint8_t> d2_tensor_dst;        // [dst_rank * ntensors + t] -> 1 if overridden
 
     bool has_scalars = false;
     int scalar_root_phys = -1;
@@ -143,6 +152,14 @@ Side build_side(const ModelSpace& space, const ParallelConfig& cfg);
 /// merged exactly like normalize_intervals, in canonical (src, dst, lo) order.
 /// Applies the D2 override.
 std::vector<FlatXfer> expand_flat_host(const PlanCore& P);
+
+/// Runs of the triples (canonical order) -> the plan's runs: drop those inside the D2
+/// over-sourced intervals and merge in `d2_runs` (identity without the extension).
+std::vector<FlatXfer> apply_d2(const PlanCore& P, std::vector<FlatXfer> base);
+
+/// Append the runs of a triple (band sweep), merging abutting runs of the same
+/// (src, dst) with the last element of `out` like normalize_intervals.
+void append_runs(const stair::Triple& T, std::vector<FlatXfer>& out);
 
 /// The same expansion evaluated row by row (the GPU planner's algorithm), host side.
 std::vector<FlatXfer> expand_flat_rows_host(const PlanCore& P);

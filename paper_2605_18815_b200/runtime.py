@@ -22,6 +22,26 @@ def dist_env():
     return rank, world, local
 
 
+def init_dist():
+    """One process per rank: set the device and create the default process group. More
+    ranks than GPUs (a 1-GPU box running a 2/4/8-rank placement) share devices round
+    robin; NCCL refuses two ranks on one device, so those runs use gloo plumbing (the data
+    path needs no collective: pushes go through cudaIpc / VMM mappings either way).
+    Returns (rank, world, local device, shared)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    n = torch.cuda.device_count()
+    shared = world > n
+    local %= n
+    torch.cuda.set_device(local)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local, shared
+
+
 class Transition:
     """One direction of a reshard on this GPU (push model)."""
 

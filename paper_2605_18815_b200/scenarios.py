@@ -127,9 +127,10 @@ def llama3_8b(layers: int = 32) -> Model:
     return Model(f"llama3-8b-L{layers}", ts, layers=layers)
 
 
-def llama3_70b(layers: int = 80) -> Model:
-    """Llama-3-70B (config 5): 723 tensors at L=80."""
-    h, kv, ffn, vocab = 8192, 1024, 28672, 128256
+def llama3_70b(layers: int = 80, hidden: int = 8192, kv: int = 1024, ffn: int = 28672, vocab: int = 128256) -> Model:
+    """Llama-3-70B (config 5): 723 tensors at L=80. Smaller widths give the same tensor
+    list and TP axes at toy size (parity tests against the oracle's buffers)."""
+    h = hidden
     ts = [Tensor("embed", (vocab, h), 0, tp=0)]
     for l in range(layers):
         p = f"l{l}."
@@ -145,7 +146,8 @@ def llama3_70b(layers: int = 80) -> Model:
             Tensor(p + "down", (h, ffn), l, tp=1),
         ]
     ts += [Tensor("final_norm", (h,), layers - 1), Tensor("lm_head", (vocab, h), layers - 1, tp=0)]
-    return Model(f"llama3-70b-L{layers}", ts, layers=layers)
+    name = f"llama3-70b-L{layers}" if h == 8192 else f"llama3-70b-shape-L{layers}-h{h}"
+    return Model(name, ts, layers=layers)
 
 
 def llama2_13b(layers: int = 40) -> Model:

@@ -17,26 +17,26 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import (Transition, dist_env, exchange_arena, global_stage_cuts, run_stages,  # noqa: E402
+from paper_2605_18815_b200.runtime import (Transition, exchange_arena, global_stage_cuts, init_dist, run_stages,  # noqa: E402
                                            shared_arena)
 
 
 def main():
     layers = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local, shared = init_dist()
     seed = 0xA7E4
     fails = 0
     # groups 0: one group per stage (most aliasing); 2: the stage order in two halves
     # groups < 0: the schedule ladder under a per-GPU cap (config 5 depth-scaled: old + new
     # state does not fit, the arena has to rebuild it in layer bands; the analogue of the
     # full 70B model on 8 GPUs under 180 GB)
-    c5cap = {2: 86e9, 4: 45e9}.get(world)
+    # ranks sharing one device (a 1-GPU box): config 5 at L=4, caps summing to < 150 GB
+    c5cap = ({2: 62e9, 4: 36e9} if shared else {2: 86e9, 4: 45e9}).get(world)
+    c5layers = 4 if shared else 8
     cases = [(S.config2(layers), 0), (S.config2(layers), 2), (S.config3(2)[0], 0)]
     if c5cap:
-        cases.append((S.config5(8), "cap"))
-        cases.append((S.config5(8), "rounds"))
+        cases.append((S.config5(c5layers), "cap"))
+        cases.append((S.config5(c5layers), "rounds"))
     for sc, groups in cases:
         ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
@@ -80,7 +80,7 @@ def main():
         del fwd, bwd, arena
         torch.cuda.synchronize()
         dist.barrier()
-    t = torch.tensor([fails], device="cuda")
+    t = torch.tensor([fails], device="cpu" if shared else "cuda")
     dist.all_reduce(t)
     dist.destroy_process_group()
     if rank == 0:

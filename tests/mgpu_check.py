@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, init_dist  # noqa: E402
 
 
 def main():
@@ -27,16 +27,10 @@ def main():
     # --random K: only K random toy MoE models (the generator of tests/test_spec_kats.py)
     n_random = int(sys.argv[sys.argv.index("--random") + 1]) if "--random" in sys.argv else 0
     dedup = dedup or early
-    rank, world, local = dist_env()
-    # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box) exercise the N=8 placement: ranks
-    # sharing a device still exchange cudaIpc handles and push through them
-    shared = world > torch.cuda.device_count()
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if shared:  # NCCL refuses two ranks on one device; the push needs no collective anyway
-        dist.init_process_group("gloo")
-    else:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box, or 2/4 on a 1-GPU box) exercise
+    # the N>1 placement: ranks sharing a device still exchange cudaIpc handles / VMM
+    # descriptors and push through them (gloo plumbing, runtime.init_dist)
+    rank, world, local, shared = init_dist()
     seed = 0xBEEF
     failures = 0
     ctrl = dist.new_group(backend="gloo") if early else None

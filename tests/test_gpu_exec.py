@@ -50,6 +50,14 @@ def _run_single_gpu(sc, with_grads=False, allow=False, bind_torch=False):
     return plan, ex, tensors
 
 
+def _ranks():
+    """Rank processes for the N>1 checks: one per GPU (up to 4); on a 1-GPU box 4 rank
+    processes share the device (gloo plumbing, cudaIpc / VMM pushes between processes),
+    so the N>1 code paths run on every box the driver leases."""
+    n = torch.cuda.device_count()
+    return min(n, 4) if n >= 2 else 4
+
+
 def _oracle_dst(sc, with_grads=False, allow=False):
     s = O.OScenario(sc.text())
     p = O.OPlan(s, allow)
@@ -194,11 +202,8 @@ def test_multi_gpu_push_over_nvlink():
     """N>1: torchrun one process per GPU; skipped on a 1-GPU box."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29531",
                         os.path.join(root, "tests", "mgpu_check.py"), "2"],
                        capture_output=True, text=True, timeout=900)
@@ -211,11 +216,8 @@ def test_multi_gpu_random_moe_models(dedup):
     GPUs (one process per GPU, cudaIpc peer stores), forward and back, bit-exact."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29537",
                         os.path.join(root, "tests", "mgpu_check.py"), "1", "--random", "16"] + dedup,
                        capture_output=True, text=True, timeout=900)
@@ -227,11 +229,8 @@ def test_multi_gpu_arena_stages():
     eager-free aliasing, one global barrier per stage; skipped on a 1-GPU box."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29533",
                         os.path.join(root, "tests", "mgpu_arena_check.py"), "2"],
                        capture_output=True, text=True, timeout=900)
@@ -285,11 +284,8 @@ def test_multi_gpu_vmm_shared_buffers():
     instead of cudaIpc; the way back adopts the forward's buffers. Skipped on one GPU."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29537",
                         os.path.join(root, "tests", "mgpu_check.py"), "2", "--vmm"],
                        capture_output=True, text=True, timeout=900)
@@ -341,11 +337,8 @@ def test_multi_gpu_replica_dedup():
     barrier): every scenario's round trip bit-exact. Skipped on one GPU."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29539",
                         os.path.join(root, "tests", "mgpu_check.py"), "2", "--dedup"],
                        capture_output=True, text=True, timeout=600)
@@ -357,11 +350,8 @@ def test_multi_gpu_replica_dedup_early():
     copies on a second stream while the other pushes continue; round trips bit-exact."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", "29543",
                         os.path.join(root, "tests", "mgpu_check.py"), "2", "--dedup-early"],
                        capture_output=True, text=True, timeout=600)
@@ -413,9 +403,6 @@ def test_eight_rank_placement_oversubscribed():
     this box has (ranks share devices; gloo plumbing): every scenario bit-exact."""
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
                         "--master-addr", "127.0.0.1", "--master-port", "29541",
@@ -463,12 +450,9 @@ def test_edm_scale_events_bit_exact(flags):
     import json
     import subprocess
     import sys
-    n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     port = "29545" if not flags else "29547"
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={min(n, 4)}",
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
                         "--master-addr", "127.0.0.1", "--master-port", port,
                         os.path.join(root, "tools", "edm_bench.py"), "--layers", "2", "--gemm", "2048"] + flags,
                        capture_output=True, text=True, timeout=600)

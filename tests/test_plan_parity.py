@@ -106,3 +106,41 @@ def test_config_errors_mirror_reference():
         plan_transition(ModelSpace(m), S.Cfg(tp=3), S.Cfg(tp=2))
     with pytest.raises(ConfigError, match="duplicate tensor_id"):
         ModelSpace(S.Model("m", [S.Tensor("W", (4,)), S.Tensor("W", (4,))]))
+
+
+def test_d2_extension_north_star_way_back_matches_oracle():
+    """The bench's way back (DP2xTP4 -> TP8, over-sourced norms): the whole dump, with the
+    proximity rule and with balance_fanout (the extension's cursor order)."""
+    import dataclasses
+    for sc in (S.config2(2).reversed(), dataclasses.replace(S.config2(2).reversed(), balance=True)):
+        p = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+        o = O.OPlan(O.OScenario(sc.text()), True)
+        assert p.dump() == o.dump()
+        assert p.bytes_moved() == o.bytes_moved() and p.bytes_retained() == o.bytes_retained()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_d2_extension_random_campaign_matches_oracle(seed):
+    """Random toy models with replicated tensors, ZeRO on both sides, src tp > 1 (where the
+    reference throws, D2): the extension's dump equals the oracle's, with and without
+    balance_fanout, identity and shuffled join/leave world maps."""
+    import random
+    rng = random.Random(7000 + seed)
+    for _ in range(50):
+        m = S.toy_model(rng, experts=rng.choice([1, 1, 2, 4]))
+        src = S.random_cfg(rng, m, max_world=8, zero=True)
+        dst = S.random_cfg(rng, m, max_world=8, zero=True)
+        if src.tp > 1:
+            break
+    sc = S.Scenario(m, src, dst, balance=bool(seed % 2), rpn=rng.choice([2, 4, 8]))
+    if seed % 3 == 2:  # joiners / leavers on a shuffled set of physical devices
+        phys = list(range(src.world() + dst.world()))
+        rng.shuffle(phys)
+        sc.world_src = sorted(phys[: src.world()])
+        sc.world_dst = sorted(phys[src.world() - min(src.world(), dst.world()) // 2:][: dst.world()])
+    o = O.OPlan(O.OScenario(sc.text()), True)
+    p = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+    assert p.dump() == o.dump()
+    assert p.dump(device=-1) == p.dump_rows_host()
+    assert p.bytes_moved() == o.bytes_moved()
+    assert p.validate() == []

@@ -24,7 +24,7 @@ from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.edm import ElasticDeviceManager, overlap_accounting  # noqa: E402
-from paper_2605_18815_b200.runtime import (Transition, dist_env, run_dedup_early, setup_multicast,  # noqa: E402
+from paper_2605_18815_b200.runtime import (Transition, init_dist, run_dedup_early, setup_multicast,  # noqa: E402
                                            share_buffers)
 
 
@@ -42,9 +42,7 @@ def main():
                     help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
     args = ap.parse_args()
     args.dedup = args.dedup or args.dedup_early
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local, shared = init_dist()
     early = (torch.cuda.Stream(), dist.new_group(backend="gloo")) if args.dedup_early else None
     shrink, grow = S.config3(args.layers)
     grow.balance = args.balance
