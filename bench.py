@@ -2,10 +2,12 @@
 """Benchmark: Llama-3-8B full training state resharded TP8 -> DP2xTP4 + ZeRO-1
 (BASELINE.json metric / configs[1]) on N B200s, 8 virtual ranks in contiguous blocks.
 
-A step is a ROUND TRIP: TP8 -> DP2xTP4 (the metric's transition) and back, so the
-state is identical at every step start (two full transitions per step; the reported
-value is per transition). Inputs (the 112 GB source state, canon payloads) are resident
-in HBM and far larger than L2 (126 MB), so no L2 flush is needed between steps.
+A step is ONE forward transition TP8 -> DP2xTP4 (the metric's), timed with CUDA events
+on the launching stream; the way back DP2xTP4 -> TP8 runs between steps (untimed for
+`value`, reported as `way_back`) so every step starts from the same state. `e2e` repeats
+the step through the public API with the plan rebuilt every step. Inputs (the 112 GB
+source state, canon payloads) are resident in HBM and far larger than L2 (126 MB), so no
+L2 flush is needed between steps.
 
   python bench.py [--gpus N --steps K --warmup W --layers 32]
   torchrun --nproc-per-node N bench.py --gpus N ...          (driver launch for N>1)
@@ -142,7 +144,7 @@ class CpuBaseline:
     the Llama-3-8B shape with `layers` layers (embed + L layers + lm_head). The plan
     (oracle planner) is rebuilt inside every timed step, as the GPU arm's e2e does."""
 
-    def __init__(self, layers: int = 1, threads: int = 0):
+    def __init__(self, layers: int = 4, threads: int = 0):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle as O
         from paper_2605_18815_b200 import scenarios as S
@@ -178,7 +180,7 @@ class CpuBaseline:
                           f"bit-exact vs canon"}
 
 
-def cpu_baseline(layers_sample: int = 1, reps: int = 2):
+def cpu_baseline(layers_sample: int = 4, reps: int = 2):
     cb = CpuBaseline(layers_sample)
     ts = [cb.step() for _ in range(reps)]
     assert cb.verify() == 0
@@ -245,10 +247,12 @@ def run_ours(args):
     sc = S.config2(args.layers)
     t0 = time.perf_counter()
     ab = RoutingPlan.from_scenario(sc)
+    plan_s = time.perf_counter() - t0
     # the way back (DP2xTP4 -> TP8) has TP-replicated norms in several ZeRO shards: the
     # reference throws there (defect D2); the documented extension resolves it
+    t0 = time.perf_counter()
     ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
-    plan_s = time.perf_counter() - t0
+    plan_back_s = time.perf_counter() - t0
     # forward and backward transitions share buffers: A (TP8) and B (DP2xTP4)
     fwd = Transition(ab, n, rank, dev, alloc=False)
     bwd = Transition(ba, n, rank, dev, alloc=False)
@@ -305,34 +309,36 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
-    def step():
-        fwd.run(sp)
-        if world > 1:
-            torch.cuda.synchronize()
-            barrier()
-        bwd.run(sp)
+    def settle():
+        # every rank's pushes have landed before anyone reads or overwrites them
         if world > 1:
             torch.cuda.synchronize()
             barrier()
 
     for _ in range(args.warmup):
-        step()
+        fwd.run(sp)
+        settle()
+        bwd.run(sp)
+        settle()
     torch.cuda.synchronize()
     barrier()
     # correctness of the measured configuration (outside the timed region): B right
     # after A->B, A right after B->A (with the arena, B is dead once A is rebuilt)
     fwd.run(sp)
+    settle()
     torch.cuda.synchronize()
-    barrier()
     bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
     bwd.run(sp)
+    settle()
     torch.cuda.synchronize()
-    barrier()
     bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     barrier()
+    # timed: K steps = K forward transitions TP8 -> DP2xTP4 (the metric's), each between
+    # CUDA events on the launching stream; the way back DP2xTP4 -> TP8 restores the TP8
+    # state between steps and is reported on its own (its plan is the D2 extension)
     with ClockSampler(dev) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
@@ -342,14 +348,10 @@ def run_ours(args):
             e0.record(stream)
             fwd.run(sp)
             e1.record(stream)
-            if world > 1:
-                torch.cuda.synchronize()
-                barrier()
+            settle()
             bwd.run(sp)
             e2.record(stream)
-            if world > 1:
-                torch.cuda.synchronize()
-                barrier()
+            settle()
         t_end.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -362,52 +364,49 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms, fwd_avg, bwd_avg, bad = t.tolist()
 
-    # end-to-end through the public API: per step, descriptors rebuilt from the plan
-    # and uploaded (H2D), both transitions run, and a result word read back (D2H)
-    e2e_steps = max(1, min(args.steps, 3))
+    # end to end through the public API, every step: the forward plan rebuilt from the
+    # scenario (host planner), handed to the executor that owns the state buffers, its
+    # descriptors rebuilt and uploaded (H2D), the transition run, and one 8-byte word of the
+    # new layout read back (D2H); host wall clock, max over ranks. The way back (untimed)
+    # restores the TP8 state before the next step.
     from paper_2605_18815_b200.runtime import local_ranks
-    local_rank0 = (local_ranks(ba, bwd.ex, A.SIDE_DST) or [0])[0]
-    h2d = (fwd.ex.stats().tiles + bwd.ex.stats().tiles) * 40
-    # warm-up of the e2e path itself: both alternating descriptor buffers of every
-    # executor exist before timing (their first allocation is a one-time cost)
-    for _ in range(2):
-        reprepare[0]()
-        reprepare[1]()
-    torch.cuda.synchronize()
-    barrier()
-    t0 = time.perf_counter()
-    # descriptors are rebuilt from the plan and uploaded inside every step; the host work
-    # overlaps the device: the way back's while the forward runs, the next forward's while
-    # the way back runs (the executor's descriptor buffers alternate, so an upload never
-    # touches descriptors a running kernel reads)
-    reprepare[0]()
-    for i in range(e2e_steps):
-        ta = time.perf_counter()
-        fwd.run(sp)
-        reprepare[1]()
-        tb = time.perf_counter()
-        if world > 1:
-            torch.cuda.synchronize()
-            barrier()
-        bwd.run(sp)
-        if i + 1 < e2e_steps:
-            reprepare[0]()
-        # the step's result: one 8-byte word of the rebuilt old layout, read back (D2H)
-        bwd.ex.read(A.SIDE_DST, local_rank0, A.BUF_MASTER, 0, 8, sp)
+    local_dst0 = (local_ranks(ab, fwd.ex, A.SIDE_DST) or [0])[0]
+    h2d = fwd.ex.stats().tiles * 40
+    e2e_ts, e2e_plan, e2e_prep = [], [], []
+    keep_plans = []
+    for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
-        if world > 1:
-            barrier()
-        if os.environ.get("RS_TIMING"):
-            print(f"[bench rank {rank}] e2e step: launch+prepare {1e3 * (tb - ta):.1f} ms, rest {1e3 * (time.perf_counter() - tb):.1f} ms",
-                  file=sys.stderr, flush=True)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        barrier()
+        t0 = time.perf_counter()
+        plan_i = RoutingPlan.from_scenario(sc)
+        t1 = time.perf_counter()
+        fwd.ex.set_plan(plan_i)
+        reprepare[0]()
+        t2 = time.perf_counter()
+        fwd.run(sp)
+        settle()
+        fwd.ex.read(A.SIDE_DST, local_dst0, A.BUF_MASTER, 0, 8, sp)
+        torch.cuda.synchronize()
+        t3 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_ts.append(t3 - t0)
+            e2e_plan.append(t1 - t0)
+            e2e_prep.append(t2 - t1)
+        keep_plans = [plan_i]  # the executor drives from it until the next set_plan
+        bwd.run(sp)
+        settle()
+    torch.cuda.synchronize()
+    bad_e2e = bwd.ex.verify(A.SIDE_DST, seed)[0]  # the last way back restored A
+    e2e_t = torch.tensor([statistics.mean(e2e_ts), statistics.mean(e2e_plan), statistics.mean(e2e_prep),
+                          float(bad_e2e)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_s = e2e_t.item()
+    e2e_s, e2e_plan_s, e2e_prep_s, bad_e2e = e2e_t.tolist()
+    bad += bad_e2e
+    del keep_plans
 
-    bytes_step = ab.bytes_moved() + ba.bytes_moved()
-    ms_step = total_ms / args.steps
+    bytes_step = ab.bytes_moved()
+    ms_step = fwd_avg
     value = bytes_step / (ms_step / 1e3) / 1e9  # whole-job GB/s (plan bytes per second)
     st_f = fwd.ex.stats()
     pk = peaks()
@@ -496,17 +495,25 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "u16/u32 payload copy (bf16 params, fp32 master/m/v)",
             "data": "synthetic (canon payloads, bit-exact verified)",
             "transport": args.transport,
-            "config": {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1, round trip per step",
+            "config": {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1: one forward transition per step "
+                                   f"(the way back restores the state between steps, reported as way_back)",
                        "model": "Llama-3-8B", "layers": args.layers, "virtual_ranks": 8,
                        "parallelism": f"tp8 -> dp2xtp4 + zero1 on {n} GPU(s)", "l2": "inputs >> L2 (no flush needed)",
                        "plan_bytes_per_transition": ab.bytes_moved()},
-            "reconfig_s": round(fwd_avg / 1e3, 5), "reconfig_back_s": round(bwd_avg / 1e3, 5),
+            "reconfig_s": round(fwd_avg / 1e3, 5),
             "gbs_per_gpu": round(ab.bytes_moved() / (fwd_avg / 1e3) / 1e9 / n, 2),
             "plan_s": round(plan_s, 4), "verified_mismatches": int(bad),
+            "way_back": {"what": "DP2xTP4 -> TP8 (D2 extension plan: parity unpinned; state verified vs canon)",
+                         "reconfig_s": round(bwd_avg / 1e3, 5), "plan_s": round(plan_back_s, 4),
+                         "bytes_moved": ba.bytes_moved(),
+                         "gbs": round(ba.bytes_moved() / (bwd_avg / 1e3) / 1e9, 2)},
+            "round_trip_ms_per_step": round(total_ms / args.steps, 3),
             "roofline": roof, "cpu_baseline": cpu, "planner": planner,
             "e2e": {"value": round(bytes_step / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": 8, "seconds_per_step": round(e2e_s, 4),
-                    "what": "per step: descriptor rebuild + upload for both transitions (overlapped with the device), both transitions, result readback"},
+                    "d2h_bytes_per_step": 8, "seconds_per_step": round(e2e_s, 5),
+                    "plan_s": round(e2e_plan_s, 5), "prepare_s": round(e2e_prep_s, 5), "steps": args.steps,
+                    "what": "per step, sequential: forward plan from the scenario (host planner) + set_plan + "
+                            "descriptor build and upload + the transition + 8-byte result readback"},
             "clocks": clk.summary(),
         }
         out["gpu_launches"] = (st_f.launches + bwd.ex.stats().launches) * args.steps
@@ -529,7 +536,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--cpu-layers", type=int, default=1)
+    ap.add_argument("--cpu-layers", type=int, default=4,
+                    help="CPU arm sample: the Llama-3-8B shape at this depth (full depth needs > 241 GB of host RAM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-arena", action="store_true", help="N=1: plain allocations (needs old+new to fit)")
     ap.add_argument("--arena-multi", action="store_true",

@@ -435,6 +435,10 @@ int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t*
  * readback; synchronous on `stream`) */
 int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream);
 int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out);
+/* drive the executor's bound buffers with a re-computed plan of the same transition (same
+ * configs, world map, model and buffer geometry: RS_ERR_CONFIG otherwise); the next
+ * rs_exec_prepare builds descriptors from it. The plan must outlive its use. */
+int rs_exec_set_plan(rs_exec_t* e, const rs_plan_t* p);
 /* GPU index (in [0, n_gpus)) the executor places physical device `phys` on */
 int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu);
 

@@ -188,6 +188,12 @@ class Executor:
         A.check(A.lib().rs_exec_buffer(self.h, side, rank, buf, C.byref(p), C.byref(n), C.byref(g)))
         return p.value or 0, n.value, g.value
 
+    def set_plan(self, plan: RoutingPlan) -> None:
+        """Drive the bound buffers with a re-computed plan of the same transition (same
+        configs, world map, model, buffer geometry); the next prepare() builds from it."""
+        A.check(A.lib().rs_exec_set_plan(self.h, plan.h))
+        self.plan = plan
+
     def gpu_of_phys(self, phys: int) -> int:
         """GPU index this executor places physical device `phys` on."""
         g = C.c_int()

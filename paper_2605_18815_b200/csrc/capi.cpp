@@ -747,6 +747,14 @@ int rs_exec_prepare_staged(rs_exec_t* e) {
     });
 }
 
+int rs_exec_set_plan(rs_exec_t* e, const rs_plan_t* p) {
+    return guarded([&] {
+        e->ex->set_plan(p->core);
+        e->plan = p;
+        return RS_OK;
+    });
+}
+
 int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu) {
     return guarded([&] {
         *gpu = e->ex->gpu_of_phys(phys);

@@ -335,18 +335,18 @@ int class_index(int v) { return v == 16 ? 0 : v == 8 ? 1 : v == 4 ? 2 : v == 2 ?
 
 }  // namespace
 
-Executor::Executor(const core::PlanCore& P, const ExecConfig& cfg) : P_(P), cfg_(cfg) {
+Executor::Executor(const core::PlanCore& P, const ExecConfig& cfg) : P_(&P), cfg_(cfg) {
     if (cfg_.n_gpus < 1 || cfg_.gpu < 0 || cfg_.gpu >= cfg_.n_gpus) throw ConfigError("bad executor placement");
     int max_phys = 0;
-    for (const auto& r : P_.routes) max_phys = std::max(max_phys, r.phys);
+    for (const auto& r : P_->routes) max_phys = std::max(max_phys, r.phys);
     per_gpu_ = (max_phys + 1 + cfg_.n_gpus - 1) / cfg_.n_gpus;
     for (int side = 0; side < 2; ++side) {
-        const int n = side == 0 ? P_.src_cfg.world_size() : P_.dst_cfg.world_size();
+        const int n = side == 0 ? P_->src_cfg.world_size() : P_->dst_cfg.world_size();
         bufs_[side].resize(static_cast<size_t>(n));
         for (int r = 0; r < n; ++r) {
             RankBufs& rb = bufs_[side][static_cast<size_t>(r)];
-            buffer_sizes(P_, side, r, cfg_.with_grads, rb.bytes);
-            const int phys = side == 0 ? P_.wm.src_phys[static_cast<size_t>(r)] : P_.wm.dst_phys[static_cast<size_t>(r)];
+            buffer_sizes(*P_, side, r, cfg_.with_grads, rb.bytes);
+            const int phys = side == 0 ? P_->wm.src_phys[static_cast<size_t>(r)] : P_->wm.dst_phys[static_cast<size_t>(r)];
             rb.gpu = gpu_of_phys(phys);
         }
     }
@@ -373,8 +373,33 @@ Executor::~Executor() {
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
 
+void Executor::set_plan(const core::PlanCore& P) {
+    // a re-computed plan of the same transition drives the bound buffers: the layouts
+    // (configs, world map, model, buffer sizes) must be identical
+    const core::PlanCore& O = *P_;
+    auto same_cfg = [](const ParallelConfig& a, const ParallelConfig& b) {
+        return a.dp == b.dp && a.tp == b.tp && a.pp == b.pp && a.ep == b.ep && a.zero_enabled == b.zero_enabled &&
+               a.rank_order == b.rank_order;
+    };
+    if (P.space->fingerprint() != O.space->fingerprint() || !same_cfg(P.src_cfg, O.src_cfg) ||
+        !same_cfg(P.dst_cfg, O.dst_cfg) || P.wm.src_phys != O.wm.src_phys || P.wm.dst_phys != O.wm.dst_phys ||
+        P.opts.scalar_words != O.opts.scalar_words)
+        throw ConfigError("set_plan: the plan describes a different transition than the executor's buffers");
+    for (int side = 0; side < 2; ++side)
+        for (size_t r = 0; r < bufs_[side].size(); ++r) {
+            std::int64_t b[kNumBufs];
+            buffer_sizes(P, side, static_cast<int>(r), cfg_.with_grads, b);
+            for (int k = 0; k < kNumBufs; ++k)
+                if (b[k] != bufs_[side][r].bytes[k]) throw ConfigError("set_plan: buffer geometry differs");
+        }
+    P_ = &P;
+    bcast_.clear();
+    bcast_ready_ = false;
+    prepared_ = false;
+}
+
 void Executor::set_stage_order(const std::vector<int>& order, const std::vector<int>& cuts) {
-    const int nd = P_.dst_cfg.world_size();
+    const int nd = P_->dst_cfg.world_size();
     if (order.empty()) {
         stage_of_dst_.clear();
         stage_bands_ = 1;
@@ -404,9 +429,9 @@ int Executor::stage_of(const CopyOp& op) const {
     if (stage_of_dst_.empty()) return 0;
     int band = 0;
     if (stage_bands_ > 1 && op.tensor >= 0) {
-        const int L = std::max(1, P_.space->num_layers());
+        const int L = std::max(1, P_->space->num_layers());
         const int nb = std::min(stage_bands_, L);
-        band = P_.space->entries()[static_cast<size_t>(op.tensor)].spec.layer * nb / L;
+        band = P_->space->entries()[static_cast<size_t>(op.tensor)].spec.layer * nb / L;
     }
     return stage_of_dst_[static_cast<size_t>(op.dst_rank * stage_bands_ + band)];
 }
@@ -765,7 +790,7 @@ void Executor::set_replica_dedup(bool on, bool early) {
 const std::vector<BcastGroup>& Executor::bcast_groups() {
     if (bcast_ready_) return bcast_;
     bcast_.clear();
-    const std::vector<CopyOp> ops = build_ops(P_);
+    const std::vector<CopyOp> ops = build_ops(*P_);
     compute_dups(ops);
     // candidate ops: cross-GPU, destination at the source's own offset in an equally
     // sized buffer (replica layout), 16-B aligned (multimem.st.v4)
@@ -844,7 +869,7 @@ void Executor::prepare(bool staged) {
     RS_CUDA(cudaSetDevice(cfg_.device));
     const char* sr = std::getenv("RS_SPLIT_REMOTE");
     split_remote_ = sr && std::string(sr) == "1";
-    const std::vector<CopyOp> ops = build_ops(P_);
+    const std::vector<CopyOp> ops = build_ops(*P_);
     const auto t_ops = std::chrono::steady_clock::now();
     stats_ = ExecStats{};
     staged_ = staged;
@@ -935,8 +960,8 @@ void Executor::prepare(bool staged) {
         if (staged && S.gpu != D.gpu) {
             // channel between physical devices: ops packed densely in build_ops order,
             // so sender and receiver derive identical offsets without metadata
-            const int sp = P_.wm.src_phys[static_cast<size_t>(op.src_side_rank)];
-            const int dpp = P_.wm.dst_phys[static_cast<size_t>(op.dst_rank)];
+            const int sp = P_->wm.src_phys[static_cast<size_t>(op.src_side_rank)];
+            const int dpp = P_->wm.dst_phys[static_cast<size_t>(op.dst_rank)];
             const auto key = std::make_pair(sp, dpp);
             std::int64_t& off = chan_off[key];
             Channel& ch = channels_[key];
@@ -1259,13 +1284,13 @@ int Executor::unpack(int src_phys, int dst_phys, const void* buf, cudaStream_t s
 
 std::vector<FillTask> Executor::fill_tasks(int side) const {
     std::vector<FillTask> tasks;
-    const core::Side& S = side == 0 ? P_.src : P_.dst;
+    const core::Side& S = side == 0 ? P_->src : P_->dst;
     for (size_t r = 0; r < S.ranks.size(); ++r) {
         const RankBufs& rb = bufs_[side][r];
         if (rb.gpu != cfg_.gpu) continue;
         const core::RankGeom& g = S.ranks[r];
         for (const core::Seg& s : g.segs) {
-            const auto& e = P_.space->entries()[static_cast<size_t>(s.tensor)];
+            const auto& e = P_->space->entries()[static_cast<size_t>(s.tensor)];
             FillTask f{};
             // lifted box
             const int nd = static_cast<int>(e.spec.shape.size());

@@ -120,6 +120,9 @@ public:
     Executor& operator=(const Executor&) = delete;
 
     int gpu_of_phys(int phys) const;
+    /// drive the bound buffers with a re-computed plan of the same transition (same
+    /// configs, world map, model and buffer geometry); takes effect at the next prepare()
+    void set_plan(const core::PlanCore& P);
     /// memory-aware stages: destination ranks in execution order, one launch group
     /// per stage (a stage starts after all reads of earlier stages completed)
     void set_stage_order(const std::vector<int>& dst_order, const std::vector<int>& cuts = {});
@@ -172,7 +175,7 @@ public:
     std::int64_t verify(int side, std::uint64_t seed, cudaStream_t stream, std::int64_t* first_bad);
 
     const ExecStats& stats() const { return stats_; }
-    const core::PlanCore& plan() const { return P_; }
+    const core::PlanCore& plan() const { return *P_; }
 
 private:
     std::vector<FillTask> fill_tasks(int side) const;
@@ -181,7 +184,7 @@ private:
     int run_fused(cudaStream_t stream);
     void upload_tasks(const std::vector<FillTask>& tasks, cudaStream_t stream);
 
-    const core::PlanCore& P_;
+    const core::PlanCore* P_;
     ExecConfig cfg_;
     int per_gpu_ = 1;
     int sms_ = 148;

@@ -69,7 +69,7 @@ def test_config5_shape_full_depth_vs_oracle_buffers():
     with pytest.raises(A.ConfigError, match="not fully sourced"):
         RoutingPlan.from_scenario(sc)
     plan, n = _gpu_vs_oracle(sc)
-    assert n == 8 * 4  # 8 destination ranks x (param, master, m, v)
+    assert n == 8 * 5  # 8 destination ranks x (param, master, m, v, scalars)
     _gpu_vs_oracle(sc.reversed())
 
 
