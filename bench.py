@@ -253,6 +253,10 @@ def run_ours(args):
     t0 = time.perf_counter()
     ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)
     plan_back_s = time.perf_counter() - t0
+    dbar = None
+    if world > 1:
+        from paper_2605_18815_b200.runtime import device_barrier
+        dbar = device_barrier(rank, world, dev)
     # forward and backward transitions share buffers: A (TP8) and B (DP2xTP4)
     fwd = Transition(ab, n, rank, dev, alloc=False)
     bwd = Transition(ba, n, rank, dev, alloc=False)
@@ -293,8 +297,8 @@ def run_ours(args):
     elif multi_arena:
         fwd.ex.prepare()
         bwd.ex.prepare()
-        fwd.run = lambda st: run_stages(fwd.ex, st, world)
-        bwd.run = lambda st: run_stages(bwd.ex, st, world)
+        fwd.run = lambda st: run_stages(fwd.ex, st, world, barrier=dbar)
+        bwd.run = lambda st: run_stages(bwd.ex, st, world, barrier=dbar)
         reprepare = (fwd.ex.prepare, bwd.ex.prepare)
     else:
         fwd.connect()
@@ -310,10 +314,10 @@ def run_ours(args):
             dist.barrier()
 
     def settle():
-        # every rank's pushes have landed before anyone reads or overwrites them
+        # every rank's pushes have landed before anyone reads or overwrites them: the
+        # device-side SynchronizeAll, enqueued on the stream (no host round trip)
         if world > 1:
-            torch.cuda.synchronize()
-            barrier()
+            dbar(sp)
 
     for _ in range(args.warmup):
         fwd.run(sp)
@@ -345,13 +349,15 @@ def run_ours(args):
         t_start.record(stream)
         for i in range(args.steps):
             e0, e1, e2 = ev[i]
+            # N>1: the device barrier sits inside each interval, so a transition's time
+            # runs until every rank's pushes have landed (max over ranks below)
             e0.record(stream)
             fwd.run(sp)
+            settle()
             e1.record(stream)
-            settle()
             bwd.run(sp)
-            e2.record(stream)
             settle()
+            e2.record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -397,6 +403,8 @@ def run_ours(args):
         settle()
     torch.cuda.synchronize()
     bad_e2e = bwd.ex.verify(A.SIDE_DST, seed)[0]  # the last way back restored A
+    if dbar is not None and dbar.timed_out():  # a device barrier gave up waiting
+        bad_e2e += 1
     e2e_t = torch.tensor([statistics.mean(e2e_ts), statistics.mean(e2e_plan), statistics.mean(e2e_prep),
                           float(bad_e2e)], dtype=torch.float64, device="cuda")
     if world > 1:

@@ -435,6 +435,19 @@ int rs_exec_verify(rs_exec_t* e, int side, uint64_t seed, void* stream, int64_t*
  * readback; synchronous on `stream`) */
 int rs_exec_read(rs_exec_t* e, int side, int rank, int buf, int64_t offset, void* host, int64_t bytes, void* stream);
 int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out);
+/* ---- SynchronizeAll on the device: a cross-GPU flag barrier enqueued on a
+ * stream, so memory-aware stages and consecutive transitions need no host round trip.
+ * Each rank creates one, exports its handle, imports every peer's (cudaIpc), then every
+ * rank enqueues the same sequence of rs_sync_barrier calls. A spin that exceeds the
+ * timeout (20 s) gives up and sets the status rs_sync_status reports. */
+typedef struct rs_sync rs_sync_t;
+int rs_sync_create(int rank, int world, int device, rs_sync_t** out);
+void rs_sync_destroy(rs_sync_t* s);
+int rs_sync_export(const rs_sync_t* s, void* out, size_t cap, size_t* len);
+int rs_sync_import(rs_sync_t* s, int peer, const void* blob, size_t len);
+int rs_sync_barrier(rs_sync_t* s, void* stream);
+int rs_sync_status(rs_sync_t* s, int* timed_out);
+
 /* drive the executor's bound buffers with a re-computed plan of the same transition (same
  * configs, world map, model and buffer geometry: RS_ERR_CONFIG otherwise); the next
  * rs_exec_prepare builds descriptors from it. The plan must outlive its use. */

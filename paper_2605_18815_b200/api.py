@@ -507,6 +507,40 @@ class Multicast:
         self.close()
 
 
+class DeviceBarrier:
+    """SynchronizeAll on the device (rs_sync_*): a cross-GPU flag barrier
+    enqueued on a stream. Build with runtime.device_barrier (exchanges the handles)."""
+
+    def __init__(self, rank: int, world: int, device: int):
+        h = C.c_void_p()
+        A.check(A.lib().rs_sync_create(rank, world, device, C.byref(h)))
+        self.h = h.value
+        self.rank, self.world, self.device = rank, world, device
+
+    def __del__(self):
+        if getattr(self, "h", None) and _alive():
+            A.lib().rs_sync_destroy(self.h)
+            self.h = None
+
+    def export(self) -> bytes:
+        n = C.c_size_t()
+        buf = C.create_string_buffer(256)
+        A.check(A.lib().rs_sync_export(self.h, buf, 256, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def import_peer(self, peer: int, blob: bytes) -> None:
+        A.check(A.lib().rs_sync_import(self.h, peer, blob, len(blob)))
+
+    def __call__(self, stream: int = 0) -> None:
+        """Enqueue one barrier on `stream` (every rank enqueues the same sequence)."""
+        A.check(A.lib().rs_sync_barrier(self.h, C.c_void_p(stream)))
+
+    def timed_out(self) -> bool:
+        v = C.c_int()
+        A.check(A.lib().rs_sync_status(self.h, C.byref(v)))
+        return bool(v.value)
+
+
 class VmmBuffer:
     """One shareable VMM device buffer (rs_vmm_*): allocated here, or a peer's imported
     from its POSIX descriptor and mapped for this GPU."""

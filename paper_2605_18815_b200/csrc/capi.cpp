@@ -19,6 +19,7 @@
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
 #include "reshard/schedule.hpp"
+#include "reshard/sync.hpp"
 #include "reshard/validate.hpp"
 
 namespace reshard {
@@ -48,6 +49,10 @@ struct rs_schedule {
 
 struct rs_arena {
     std::unique_ptr<mem::Arena> a;
+};
+
+struct rs_sync {
+    std::unique_ptr<sync::DeviceBarrier> b;
 };
 
 struct rs_exec {
@@ -743,6 +748,48 @@ int rs_exec_prepare(rs_exec_t* e) {
 int rs_exec_prepare_staged(rs_exec_t* e) {
     return guarded([&] {
         e->ex->prepare(true);
+        return RS_OK;
+    });
+}
+
+int rs_sync_create(int rank, int world, int device, rs_sync_t** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto s = std::make_unique<rs_sync>();
+        s->b = std::make_unique<sync::DeviceBarrier>(rank, world, device);
+        *out = s.release();
+        return RS_OK;
+    });
+}
+
+void rs_sync_destroy(rs_sync_t* s) { delete s; }
+
+int rs_sync_export(const rs_sync_t* s, void* out, size_t cap, size_t* len) {
+    return guarded([&] {
+        const std::vector<std::uint8_t> v = s->b->export_handle();
+        *len = v.size();
+        if (out && cap >= v.size()) std::memcpy(out, v.data(), v.size());
+        return RS_OK;
+    });
+}
+
+int rs_sync_import(rs_sync_t* s, int peer, const void* blob, size_t len) {
+    return guarded([&] {
+        s->b->import_handle(peer, static_cast<const std::uint8_t*>(blob), len);
+        return RS_OK;
+    });
+}
+
+int rs_sync_barrier(rs_sync_t* s, void* stream) {
+    return guarded([&] {
+        s->b->arrive_and_wait(static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
+int rs_sync_status(rs_sync_t* s, int* timed_out) {
+    return guarded([&] {
+        *timed_out = s->b->status();
         return RS_OK;
     });
 }

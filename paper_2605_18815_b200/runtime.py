@@ -454,16 +454,36 @@ def setup_multicast(source, ex: Executor, rank: int, world: int, device: int, ta
     return [mcs[k] for k in sorted(mcs)]
 
 
-def run_stages(ex: Executor, stream: int, world: int) -> None:
+def device_barrier(rank: int, world: int, device: int, group=None):
+    """The device-side SynchronizeAll of this rank (api.DeviceBarrier), with every peer's
+    flag array mapped (handles exchanged over `group`). Collective."""
+    import torch.distributed as dist
+
+    from .api import DeviceBarrier
+    b = DeviceBarrier(rank, world, device)
+    if world > 1:
+        blobs: List[Optional[bytes]] = [None] * world
+        dist.all_gather_object(blobs, b.export(), group=group)
+        for peer, blob in enumerate(blobs):
+            b.import_peer(peer, blob)
+    return b
+
+
+def run_stages(ex: Executor, stream: int, world: int, barrier=None) -> None:
     """Memory-aware stages across GPUs: a stage may write chunks that the previous stage
-    read on another GPU, so every stage boundary is a global barrier."""
+    read on another GPU, so every stage boundary is a global barrier — on the device
+    (`barrier`, a DeviceBarrier: nothing returns to the host between stages) or, without
+    one, a host synchronize + dist.barrier."""
     import torch
     import torch.distributed as dist
     for s in range(ex.num_stages()):
         ex.run_stage(s, stream)
         if world > 1:
-            torch.cuda.synchronize()
-            dist.barrier()
+            if barrier is not None:
+                barrier(stream)
+            else:
+                torch.cuda.synchronize()
+                dist.barrier()
     # replica dedup: the copies from each GPU's primary replica, once every stage has landed
     # (a later write than planned never clobbers live data; the primary's chunks are final).
     # Local to each GPU and ordered on its stream: whatever reads them next (a push from

@@ -17,8 +17,8 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import Arena, RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import (Transition, exchange_arena, global_stage_cuts, init_dist, run_stages,  # noqa: E402
-                                           shared_arena)
+from paper_2605_18815_b200.runtime import (Transition, device_barrier, exchange_arena, global_stage_cuts, init_dist,  # noqa: E402
+                                           run_stages, shared_arena)
 
 
 def main():
@@ -26,6 +26,7 @@ def main():
     rank, world, local, shared = init_dist()
     seed = 0xA7E4
     fails = 0
+    dev_barrier = device_barrier(rank, world, local)
     # groups 0: one group per stage (most aliasing); 2: the stage order in two halves
     # groups < 0: the schedule ladder under a per-GPU cap (config 5 depth-scaled: old + new
     # state does not fit, the arena has to rebuild it in layer bands; the analogue of the
@@ -62,19 +63,23 @@ def main():
         bad = []
         import time
         ms = []
-        for _ in range(2):
+        # stage boundaries as host barriers, then as the device-side SynchronizeAll
+        for dbar in (None, None, dev_barrier, dev_barrier):
+            sp = torch.cuda.current_stream().cuda_stream
             t0 = time.perf_counter()
-            run_stages(fwd.ex, 0, world)
+            run_stages(fwd.ex, sp, world, barrier=dbar)
             torch.cuda.synchronize()
             dist.barrier()
             ms.append(round(1e3 * (time.perf_counter() - t0), 1))
             bad.append(fwd.ex.verify(A.SIDE_DST, seed)[0])
-            run_stages(bwd.ex, 0, world)
+            run_stages(bwd.ex, sp, world, barrier=dbar)
             torch.cuda.synchronize()
             dist.barrier()
             bad.append(bwd.ex.verify(A.SIDE_DST, seed)[0])
+        if dev_barrier.timed_out():
+            bad.append(-1)
         st = arena.stats()
-        print(f"[rank {rank}] {sc.name} groups={groups} bands={st.bands}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, forward {ms} ms, physical {st.physical_bytes/1e9:.2f} GB "
+        print(f"[rank {rank}] {sc.name} groups={groups} bands={st.bands}: stages {fwd.ex.num_stages()}/{bwd.ex.num_stages()}, mismatches {bad}, forward {ms} ms (host, host, device, device barriers), physical {st.physical_bytes/1e9:.2f} GB "
               f"(old {st.a_bytes/1e9:.2f} + new {st.b_bytes/1e9:.2f}, aliased {st.aliased_bytes/1e9:.2f})", flush=True)
         fails += sum(1 for b in bad if b)
         del fwd, bwd, arena

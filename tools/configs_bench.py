@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
-from paper_2605_18815_b200.runtime import Transition, dist_env, run_stages, shared_arena  # noqa: E402
+from paper_2605_18815_b200.runtime import Transition, device_barrier, dist_env, run_stages, shared_arena  # noqa: E402
 
 NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 nominal
 
@@ -48,7 +48,7 @@ def scenario(cfg: int, layers: int):
     raise SystemExit(f"unknown config {cfg}")
 
 
-def run_one(sc, rank, world, local, reps, arena_cap=0.0):
+def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False):
     plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
     arena = None
     if arena_cap:
@@ -59,7 +59,10 @@ def run_one(sc, rank, world, local, reps, arena_cap=0.0):
         tr = Transition(plan, world, rank, local, alloc=False)
         arena.bind(tr.ex, None, cuts)
         tr.ex.prepare()
-        tr.run = lambda stream=0: run_stages(tr.ex, stream, world)
+        # stage boundaries: the device-side SynchronizeAll (no host round trip), or host
+        # synchronize + dist.barrier with --host-barriers
+        dbar = None if host_barriers else device_barrier(rank, world, local)
+        tr.run = lambda stream=0: run_stages(tr.ex, stream, world, barrier=dbar)
     else:
         tr = Transition(plan, world, rank, local)
         tr.connect()
@@ -105,6 +108,7 @@ def run_one(sc, rank, world, local, reps, arena_cap=0.0):
     if arena is not None:
         st = arena.stats()
         out["arena"] = {"cap_gb": arena_cap, "physical_gb": round(st.physical_bytes / 1e9, 2),
+                        "stage_barriers": "host" if host_barriers else "device",
                         "old_gb": round(st.a_bytes / 1e9, 2), "new_gb": round(st.b_bytes / 1e9, 2),
                         "aliased_gb": round(st.aliased_bytes / 1e9, 2), "bands": st.bands, "stages": ex.num_stages()}
     del tr, ex, arena
@@ -119,13 +123,15 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--arena-cap", type=float, default=0.0,
                     help="GB per GPU: run under the memory-aware arena (old + new need not fit)")
+    ap.add_argument("--host-barriers", action="store_true",
+                    help="arena stages separated by host synchronize + dist.barrier instead of the device barrier")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for cfg in args.config or [1, 4]:
-        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap)
+        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap, args.host_barriers)
         if rank == 0:
             print(json.dumps(res), flush=True)
     if world > 1:
