@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <queue>
 #include <stdexcept>
 #include <string>
@@ -73,51 +74,86 @@ __device__ __forceinline__ void st_vec<true, uint4>(uint4* p, const uint4& v) {
                  : "memory");
 }
 
+/// 256-bit vector (sm_100: LDG.E.256 / STG.E.256): half the memory instructions per
+/// byte of the 16-byte path, and each peer store carries 32 B of payload per NVLink write
+struct alignas(32) V32 {
+    unsigned w[8];
+};
+template <>
+__device__ __forceinline__ V32 ld_stream<V32>(const V32* p) {
+    V32 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+                   "=r"(r.w[7])
+                 : "l"(p));
+    return r;
+}
+template <>
+__device__ __forceinline__ void st_vec<false, V32>(V32* p, const V32& v) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+                 "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+
+/// One tile with vectors of type T (the tile's addresses, pitches and row size are
+/// multiples of sizeof(T)); the CTA's threads stride over it keeping kUnroll
+/// independent loads in flight before storing.
+template <typename T, bool MC, int kUnroll = kUnroll>
+__device__ __forceinline__ void copy_tile(const Tile& tl) {
+    const unsigned vpr = tl.row_bytes / sizeof(T);
+    if (tl.rows == 1) {
+        const T* __restrict__ s = reinterpret_cast<const T*>(tl.src);
+        T* __restrict__ d = reinterpret_cast<T*>(tl.dst);
+        unsigned i = threadIdx.x;
+        for (; i + (kUnroll - 1) * kThreads < vpr; i += kUnroll * kThreads) {
+            T r[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(s + i + u * kThreads);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) st_vec<MC>(d + i + u * kThreads, r[u]);
+        }
+        for (; i < vpr; i += kThreads) st_vec<MC>(d + i, ld_stream(s + i));
+    } else {
+        const unsigned n = tl.rows * vpr;
+        for (unsigned i = threadIdx.x; i < n; i += kUnroll * kThreads) {
+            T r[kUnroll];
+            unsigned row[kUnroll], col[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const unsigned e = i + u * kThreads;
+                row[u] = e / vpr;
+                col[u] = e - row[u] * vpr;
+                if (e < n) r[u] = ld_stream(reinterpret_cast<const T*>(tl.src + row[u] * tl.src_pitch) + col[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const unsigned e = i + u * kThreads;
+                if (e < n) st_vec<MC>(reinterpret_cast<T*>(tl.dst + row[u] * tl.dst_pitch) + col[u], r[u]);
+            }
+        }
+    }
+}
+
 /// Copy tiles of alignment class V (all addresses, pitches and row sizes are
-/// multiples of V). Persistent grid: CTA b takes tiles b, b+grid, ... Each thread
-/// keeps kUnroll independent loads in flight before storing. MC: the destination is a
-/// multicast address (16-B class only).
-template <int V, bool MC = false>
-__global__ void __launch_bounds__(kThreads) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles, std::uint64_t sbase,
+/// multiples of V). Persistent grid: CTA b takes tiles b, b+grid, ... MC: the
+/// destination is a multicast address (16-B class only). W32: 16-B-class tiles that are
+/// also 32-B aligned move as 256-bit vectors.
+template <int V, bool MC = false, bool W32 = false>
+__global__ void __launch_bounds__(kThreads, W32 ? 2 : 1) copy_tiles_kernel(const Tile* __restrict__ tiles, int ntiles, std::uint64_t sbase,
                                                               std::uint64_t dbase) {
     using T = typename VecT<V>::T;
     for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
         Tile tl = tiles[ti];
         tl.src += sbase;
         tl.dst += dbase;
-        const unsigned vpr = tl.row_bytes / V;
-        if (tl.rows == 1) {
-            const T* __restrict__ s = reinterpret_cast<const T*>(tl.src);
-            T* __restrict__ d = reinterpret_cast<T*>(tl.dst);
-            unsigned i = threadIdx.x;
-            for (; i + (kUnroll - 1) * kThreads < vpr; i += kUnroll * kThreads) {
-                T r[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) r[u] = ld_stream(s + i + u * kThreads);
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) st_vec<MC>(d + i + u * kThreads, r[u]);
-            }
-            for (; i < vpr; i += kThreads) st_vec<MC>(d + i, ld_stream(s + i));
-        } else {
-            const unsigned n = tl.rows * vpr;
-            for (unsigned i = threadIdx.x; i < n; i += kUnroll * kThreads) {
-                T r[kUnroll];
-                unsigned row[kUnroll], col[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const unsigned e = i + u * kThreads;
-                    row[u] = e / vpr;
-                    col[u] = e - row[u] * vpr;
-                    if (e < n)
-                        r[u] = ld_stream(reinterpret_cast<const T*>(tl.src + row[u] * tl.src_pitch) + col[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    const unsigned e = i + u * kThreads;
-                    if (e < n) st_vec<MC>(reinterpret_cast<T*>(tl.dst + row[u] * tl.dst_pitch) + col[u], r[u]);
-                }
+        if constexpr (W32 && V == 16 && !MC) {
+            const std::uint64_t a = tl.src | tl.dst | tl.row_bytes | (tl.rows > 1 ? (tl.src_pitch | tl.dst_pitch) : 0);
+            if ((a & 31) == 0) {
+                copy_tile<V32, false, 2>(tl);  // 2 x 32 B in flight = the 16-B path's 4 x 16 B
+                continue;
             }
         }
+        copy_tile<T, MC>(tl);
     }
 }
 
@@ -718,30 +754,63 @@ void TileSet::fence(cudaStream_t stream) const {
     }
 }
 
+namespace {
+
+/// resident CTAs per SM of a copy kernel (cached): the persistent grid never asks for
+/// more CTAs than can be resident at once, so no CTA waits for a whole wave to finish
+template <class K>
+int resident_ctas(K kernel) {
+    static std::mutex mu;
+    static std::map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    const void* key = reinterpret_cast<const void*>(kernel);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+    cache[key] = b;
+    return b;
+}
+
+bool vec32_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("RS_VEC32");
+        return !(v && std::string(v) == "0");
+    }();
+    return on;
+}
+
+}  // namespace
+
 int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm,
                     bool bulk, int key_mod, int key_rem) const {
     int launches = 0;
-    const int grid_cap = sms * (ctas_per_sm > 0 ? ctas_per_sm : 4);
+    const int want = ctas_per_sm > 0 ? ctas_per_sm : 4;
     const Tile* base = static_cast<const Tile*>(dev);
+    const bool w32 = vec32_enabled();
+    auto grid_of = [&](auto kernel, int n) { return std::min(n, sms * std::min(want, resident_ctas(kernel))); };
     for (const Group& g : groups) {
         if (key_mod > 0 && g.key % key_mod != key_rem) continue;
         if (key_mod < 0 && g.key != key_rem) continue;  // exact key (one memory-aware stage)
         const int n = g.count;
-        const int grid = std::min(n, grid_cap);
         const Tile* t = base + g.begin;
         switch (g.cls) {
             case 0:
                 if (bulk) {
                     const int g2 = std::min(n, sms * kBulkCtasPerSm);
                     bulk_tiles_kernel<kBulkStages, kBulkStage><<<g2, 32, kBulkStages * kBulkStage, stream>>>(t, n, sbase, dbase);
+                } else if (w32) {
+                    auto k = copy_tiles_kernel<16, false, true>;
+                    k<<<grid_of(k, n), kThreads, 0, stream>>>(t, n, sbase, dbase);
                 } else {
-                    copy_tiles_kernel<16><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase);
+                    auto k = copy_tiles_kernel<16>;
+                    k<<<grid_of(k, n), kThreads, 0, stream>>>(t, n, sbase, dbase);
                 }
                 break;
-            case 1: copy_tiles_kernel<8><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
-            case 2: copy_tiles_kernel<4><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
-            case 3: copy_tiles_kernel<2><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
-            default: copy_tiles_kernel<1><<<grid, kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            case 1: copy_tiles_kernel<8><<<grid_of(copy_tiles_kernel<8>, n), kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            case 2: copy_tiles_kernel<4><<<grid_of(copy_tiles_kernel<4>, n), kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            case 3: copy_tiles_kernel<2><<<grid_of(copy_tiles_kernel<2>, n), kThreads, 0, stream>>>(t, n, sbase, dbase); break;
+            default: copy_tiles_kernel<1><<<grid_of(copy_tiles_kernel<1>, n), kThreads, 0, stream>>>(t, n, sbase, dbase); break;
         }
         ++launches;
     }
