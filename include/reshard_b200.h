@@ -238,6 +238,21 @@ int rs_edm_wait(rs_edm_t* e, double* init_s, int* build_rc);
  * training steps of train_step_s fit into init_s */
 int rs_edm_accounting(double init_s, double switch_s, double window_s, double train_step_s, int mode,
                       rs_edm_accounting_t* out);
+/* New-world NCCL communicators built natively: a fresh unique id (rank 0
+ * of the new world draws it, the caller broadcasts the 128 bytes), then the world
+ * communicator (ncclCommInitRankConfig, blocking = 0) and one ncclCommSplit per dimension
+ * (colors[RS_DIM_*] < 0: skip), polled to completion on the calling thread — the EDM side
+ * thread. Cached per configuration (*cache_hit). libnccl.so.2 is loaded at run time. */
+#define RS_NCCL_ID_BYTES 128
+int rs_nccl_unique_id(void* out, size_t cap);
+int rs_nccl_version(char* out, size_t cap);
+int rs_edm_comm_create(rs_edm_t* e, const rs_cfg_t* cfg, const void* uid, int nranks, int rank, int device,
+                       const int colors[5], int* cache_hit, double* init_s, double* split_s);
+/* the ncclComm_t of dimension `dim` (-1: world) of a created configuration, or NULL */
+int rs_edm_comm_get(rs_edm_t* e, const rs_cfg_t* cfg, int dim, void** comm);
+/* all-reduce (sum) of one 1.0f over that communicator on `stream`: *sum = its size */
+int rs_edm_comm_check(rs_edm_t* e, const rs_cfg_t* cfg, int dim, void* stream, float* sum);
+int rs_edm_comm_destroy(rs_edm_t* e, const rs_cfg_t* cfg);
 
 int rs_xor_peer(int i, int s, int n);
 /* MemoryAwareChunk: stage index per step (steps ascending, cost[k]

@@ -16,6 +16,7 @@
 #include "reshard/arena.hpp"
 #include "reshard/edm.hpp"
 #include "reshard/fdx.hpp"
+#include "reshard/nccl_comm.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/plan_core.hpp"
 #include "reshard/schedule.hpp"
@@ -1346,7 +1347,68 @@ int rs_arena_bind_size(const rs_arena_t* a, int layout, int rank, int buf, int64
 
 struct rs_edm {
     edm::Manager m;
+    edm::CommCache comms;
 };
+
+namespace {
+std::string comm_key(const rs_cfg_t* c) {
+    return strfmt("dp%d.tp%d.pp%d.ep%d.z%d.%s", c->dp, c->tp, c->pp, c->ep, c->zero, c->order ? c->order : "pp-dp-tp");
+}
+}  // namespace
+
+int rs_nccl_unique_id(void* out, size_t cap) {
+    return guarded([&] {
+        if (cap < edm::kNcclIdBytes) throw ConfigError("rs_nccl_unique_id: buffer smaller than 128 bytes");
+        edm::nccl_unique_id(static_cast<std::uint8_t*>(out));
+        return RS_OK;
+    });
+}
+
+int rs_nccl_version(char* out, size_t cap) {
+    return guarded([&] {
+        const std::string v = edm::nccl_version();
+        if (cap) {
+            std::strncpy(out, v.c_str(), cap - 1);
+            out[cap - 1] = 0;
+        }
+        return RS_OK;
+    });
+}
+
+int rs_edm_comm_create(rs_edm_t* e, const rs_cfg_t* cfg, const void* uid, int nranks, int rank, int device,
+                       const int colors[5], int* cache_hit, double* init_s, double* split_s) {
+    return guarded([&] {
+        bool hit = false;
+        const edm::CommSet& s = e->comms.get_or_create(comm_key(cfg), static_cast<const std::uint8_t*>(uid), nranks,
+                                                       rank, device, colors, &hit);
+        if (cache_hit) *cache_hit = hit ? 1 : 0;
+        if (init_s) *init_s = hit ? 0.0 : s.init_s;
+        if (split_s) *split_s = hit ? 0.0 : s.split_s;
+        return RS_OK;
+    });
+}
+
+int rs_edm_comm_get(rs_edm_t* e, const rs_cfg_t* cfg, int dim, void** comm) {
+    return guarded([&] {
+        const edm::CommSet* s = e->comms.find(comm_key(cfg));
+        *comm = !s ? nullptr : dim < 0 ? s->world : dim < edm::kCommDims ? s->dims[dim] : nullptr;
+        return RS_OK;
+    });
+}
+
+int rs_edm_comm_check(rs_edm_t* e, const rs_cfg_t* cfg, int dim, void* stream, float* sum) {
+    return guarded([&] {
+        *sum = e->comms.check_allreduce(comm_key(cfg), dim, static_cast<cudaStream_t>(stream));
+        return RS_OK;
+    });
+}
+
+int rs_edm_comm_destroy(rs_edm_t* e, const rs_cfg_t* cfg) {
+    return guarded([&] {
+        e->comms.destroy(comm_key(cfg));
+        return RS_OK;
+    });
+}
 
 int rs_edm_create(rs_edm_t** out) {
     return guarded([&] {

@@ -3,7 +3,9 @@
 
 What the EDM builds for a new configuration, off the critical path:
   * its communicator groups (get_or_create_groups, cached per ParallelConfig;
-    rank lists derived in C++ by rs_config_groups, torch process groups optional),
+    rank lists derived in C++ by rs_config_groups) and its NCCL communicators, built
+    natively and non-blocking (create_nccl_comms: world ncclCommInitRankConfig with
+    blocking = 0, one ncclCommSplit per dimension; torch process groups optional),
   * the transition itself: plan (C++ planner), executor, destination buffers,
     cudaIpc peer mappings (exchanged over a dedicated gloo control group so the side
     thread never touches the NCCL group the training loop uses) and the device
@@ -66,6 +68,13 @@ def _bind(L):
         ("rs_edm_ready", [vp, P(C.c_int)]),
         ("rs_edm_wait", [vp, P(C.c_double), P(C.c_int)]),
         ("rs_edm_accounting", [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, P(_Accounting)]),
+        ("rs_nccl_unique_id", [vp, C.c_size_t]),
+        ("rs_nccl_version", [C.c_char_p, C.c_size_t]),
+        ("rs_edm_comm_create", [vp, P(A.Cfg_t), vp, C.c_int, C.c_int, C.c_int, P(C.c_int), P(C.c_int),
+                                P(C.c_double), P(C.c_double)]),
+        ("rs_edm_comm_get", [vp, P(A.Cfg_t), C.c_int, P(vp)]),
+        ("rs_edm_comm_check", [vp, P(A.Cfg_t), C.c_int, vp, P(C.c_float)]),
+        ("rs_edm_comm_destroy", [vp, P(A.Cfg_t)]),
     ):
         fn = getattr(L, name)
         fn.argtypes = args
@@ -86,6 +95,23 @@ def overlap_accounting(init_s: float, switch_s: float, window_s: Optional[float]
                                              train_step_s or 0.0, _MODES[mode], C.byref(out)))
     return {"mode": mode, "init_s": out.init_s, "overlapped_s": out.overlapped_s, "switch_s": out.switch_s,
             "exposed_s": out.exposed_s, "overlap_ratio": None if out.ratio < 0 else out.ratio}
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId of the libnccl in this process (128 bytes)."""
+    buf = C.create_string_buffer(128)
+    A.check(_bind(A.lib()).rs_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def nccl_version() -> str:
+    buf = C.create_string_buffer(32)
+    A.check(_bind(A.lib()).rs_nccl_version(buf, 32))
+    return buf.value.decode()
+
+
+def _cfg_t(cfg: Cfg):
+    return A.Cfg_t(cfg.dp, cfg.tp, cfg.pp, cfg.ep, int(cfg.zero), cfg.order.encode())
 
 
 class ElasticDeviceManager:
@@ -147,6 +173,47 @@ class ElasticDeviceManager:
         A.check(self._lib.rs_edm_groups(self.h, C.byref(c), DIMS[dim], out, cfg.world(), C.byref(ng), C.byref(gs),
                                         C.byref(hit)))
         return [list(out[g * gs.value:(g + 1) * gs.value]) for g in range(ng.value)]
+
+    def create_nccl_comms(self, cfg: Cfg, rank: int, nranks: int, device: int, member_rank: int, group=None) -> dict:
+        """The new world's NCCL communicators, built natively and non-blocking:
+        rank 0 draws a unique id, broadcast over `group` (the gloo control group: the side
+        thread never touches the training loop's NCCL group); then the world communicator
+        and one split per dimension, polled to completion on this (side) thread. Process
+        `rank` joins, per dimension, the group of virtual rank `member_rank` of `cfg` (its
+        first hosted rank: with one rank per GPU these are exactly cfg's groups). Cached per
+        configuration; returns {"cache_hit", "init_s", "split_s"}."""
+        import torch.distributed as dist
+        uid = [nccl_unique_id() if rank == 0 else None]
+        if nranks > 1:
+            dist.broadcast_object_list(uid, src=0 if group is None else dist.get_global_rank(group, 0), group=group)
+        colors = (C.c_int * 5)()
+        for d, i in DIMS.items():
+            groups = self.get_or_create_groups(cfg).groups[d]
+            colors[i] = next(g for g, members in enumerate(groups) if member_rank in members)
+        hit, t_init, t_split = C.c_int(), C.c_double(), C.c_double()
+        c = _cfg_t(cfg)
+        A.check(self._lib.rs_edm_comm_create(self.h, C.byref(c), uid[0], nranks, rank, device, colors, C.byref(hit),
+                                             C.byref(t_init), C.byref(t_split)))
+        return {"cache_hit": bool(hit.value), "init_s": t_init.value, "split_s": t_split.value}
+
+    def nccl_comm(self, cfg: Cfg, dim: Optional[str] = None) -> int:
+        """The ncclComm_t (as an address) of `cfg`'s world (dim None) or dimension, or 0."""
+        p = C.c_void_p()
+        c = _cfg_t(cfg)
+        A.check(self._lib.rs_edm_comm_get(self.h, C.byref(c), -1 if dim is None else DIMS[dim], C.byref(p)))
+        return p.value or 0
+
+    def check_nccl_comm(self, cfg: Cfg, dim: Optional[str] = None, stream: int = 0) -> float:
+        """All-reduce (sum) of 1.0 over that communicator: returns its size."""
+        out = C.c_float()
+        c = _cfg_t(cfg)
+        A.check(self._lib.rs_edm_comm_check(self.h, C.byref(c), -1 if dim is None else DIMS[dim], C.c_void_p(stream),
+                                            C.byref(out)))
+        return out.value
+
+    def destroy_nccl_comms(self, cfg: Cfg) -> None:
+        c = _cfg_t(cfg)
+        A.check(self._lib.rs_edm_comm_destroy(self.h, C.byref(c)))
 
     def control_group(self):
         """gloo group for side-thread control traffic (IPC handle exchange)."""

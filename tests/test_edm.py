@@ -101,3 +101,27 @@ def test_accounting_modes():
     r = overlap_accounting(init_s=4.0, switch_s=1.0, window_s=10.0, mode="blocking")
     assert r["overlapped_s"] == 0.0 and r["exposed_s"] == 5.0 and r["overlap_ratio"] == 0.0
     assert overlap_accounting(0.0, 0.0)["overlap_ratio"] is None
+
+
+@pytest.mark.gpu
+def test_native_nccl_communicators_single_rank():
+    """The EDM's native, non-blocking NCCL communicator build (world + one split per
+    dimension) on a one-rank world: cached per configuration, and an all-reduce over each
+    communicator sums to its size. (Multi-rank worlds run in tools/edm_bench.py.)"""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2605_18815_b200.edm import ElasticDeviceManager, nccl_version
+    from paper_2605_18815_b200.scenarios import Cfg
+    assert nccl_version().startswith("2.")
+    edm = ElasticDeviceManager()
+    cfg = Cfg(dp=1, zero=True)
+    info = edm.create_nccl_comms(cfg, rank=0, nranks=1, device=0, member_rank=0)
+    assert not info["cache_hit"] and info["init_s"] > 0
+    assert edm.nccl_comm(cfg) != 0 and edm.nccl_comm(cfg, "dp") != 0
+    s = torch.cuda.Stream()
+    assert edm.check_nccl_comm(cfg, None, s.cuda_stream) == 1.0
+    assert edm.check_nccl_comm(cfg, "tp", s.cuda_stream) == 1.0
+    assert edm.create_nccl_comms(cfg, rank=0, nranks=1, device=0, member_rank=0)["cache_hit"]
+    edm.destroy_nccl_comms(cfg)
+    assert edm.nccl_comm(cfg) == 0

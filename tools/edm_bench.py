@@ -24,8 +24,8 @@ from paper_2605_18815_b200 import _capi as A  # noqa: E402
 from paper_2605_18815_b200 import scenarios as S  # noqa: E402
 from paper_2605_18815_b200.api import RoutingPlan  # noqa: E402
 from paper_2605_18815_b200.edm import ElasticDeviceManager, overlap_accounting  # noqa: E402
-from paper_2605_18815_b200.runtime import (Transition, init_dist, run_dedup_early, setup_multicast,  # noqa: E402
-                                           share_buffers)
+from paper_2605_18815_b200.runtime import (Transition, init_dist, local_ranks, run_dedup_early,  # noqa: E402
+                                           setup_multicast, share_buffers)
 
 
 def main():
@@ -40,9 +40,13 @@ def main():
                     help="--dedup with the replica copies overlapping the tail of the pushes")
     ap.add_argument("--multicast", action="store_true",
                     help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
+    ap.add_argument("--no-nccl-comms", action="store_true",
+                    help="skip the new world's NCCL communicators (always skipped when ranks share a GPU)")
     args = ap.parse_args()
     args.dedup = args.dedup or args.dedup_early
     rank, world, local, shared = init_dist()
+    # NCCL refuses two ranks of one communicator on one GPU
+    nccl_comms = not args.no_nccl_comms and not shared
     early = (torch.cuda.Stream(), dist.new_group(backend="gloo")) if args.dedup_early else None
     shrink, grow = S.config3(args.layers)
     grow.balance = args.balance
@@ -76,6 +80,14 @@ def main():
             plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
             t["plan_s"] = time.perf_counter() - t0
             tr = Transition(plan, world, rank, local, alloc=False)
+            if nccl_comms:
+                # the new world's NCCL communicators, natively and non-blocking on this side
+                # thread (the training loop keeps its own NCCL group busy meanwhile)
+                t1 = time.perf_counter()
+                mine = local_ranks(plan, tr.ex, A.SIDE_DST) or [0]
+                info = edm.create_nccl_comms(sc.dst, rank, world, local, member_rank=mine[0], group=ctrl)
+                t["nccl_comms_s"] = time.perf_counter() - t1
+                t["nccl_init_s"], t["nccl_split_s"], t["nccl_cache_hit"] = info["init_s"], info["split_s"], info["cache_hit"]
             tr.ex.set_replica_dedup(args.dedup, early=args.dedup_early)
             keep = []
             if args.multicast:
@@ -179,6 +191,17 @@ def main():
                 dist.barrier()
             switch_s = time.perf_counter() - t0
             bad = tr.ex.verify(A.SIDE_DST, seed)[0]
+            if nccl_comms:
+                # the new world's communicators work: an all-reduce over the world and each
+                # dimension sums to the communicator's size
+                sizes = {"world": edm.check_nccl_comm(sc.dst)}
+                for d in ("dp", "tp", "pp"):
+                    sizes[d] = edm.check_nccl_comm(sc.dst, d)
+                tprep["nccl_allreduce_sizes"] = sizes
+                if sizes["world"] != world:
+                    bad += 1
+                if mode == "blocking":  # the overlapped run builds the new world from scratch
+                    edm.destroy_nccl_comms(sc.dst)
             init = torch.tensor([edm.init_s, window_s, switch_s, float(bad)], dtype=torch.float64, device="cuda")
             dist.all_reduce(init, op=dist.ReduceOp.MAX)
             init_s, window_s, switch_s, bad = init.tolist()
