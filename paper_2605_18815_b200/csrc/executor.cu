@@ -1142,6 +1142,11 @@ void Executor::prepare(bool staged) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkStage));
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);  // descriptors changed: recapture
     graph_exec_ = nullptr;
+    {
+        const char* gr = std::getenv("RS_GRAPH");
+        auto_graph_ = !(gr && std::string(gr) == "0") && here < (1ll << 30) && !staged;
+        runs_since_prepare_ = 0;
+    }
     prepared_ = true;
 }
 
@@ -1171,7 +1176,7 @@ int Executor::run_graph(cudaStream_t stream) {
         cudaGraph_t g = nullptr;
         RS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         try {
-            graph_launches_ = run(stream);
+            graph_launches_ = run_direct(stream);
         } catch (...) {
             cudaStreamEndCapture(stream, &g);
             if (g) cudaGraphDestroy(g);
@@ -1192,6 +1197,15 @@ int Executor::run_graph(cudaStream_t stream) {
 
 int Executor::run(cudaStream_t stream) {
     if (!prepared_) throw ConfigError("run before prepare");
+    // transitions under 1 GiB per GPU are launch-bound: replay them from a CUDA graph
+    // (captured per prepare and stream; RS_GRAPH=0 disables)
+    // the first run after a prepare goes direct (a one-shot reconfiguration would pay the
+    // capture for nothing); repeated runs capture once and replay
+    if (auto_graph_ && runs_since_prepare_++ > 0) return run_graph(stream);
+    return run_direct(stream);
+}
+
+int Executor::run_direct(cudaStream_t stream) {
     RS_CUDA(cudaSetDevice(cfg_.device));
     if (!mc_ || mc_->groups.empty()) return run_fused(stream);
     // the multicast stream runs concurrently with the fused pushes (the root's NVLink

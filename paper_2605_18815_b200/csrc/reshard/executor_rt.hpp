@@ -182,6 +182,7 @@ private:
     void compute_dups(const std::vector<CopyOp>& ops);
     int launch_multicast(cudaStream_t stream) const;
     int run_fused(cudaStream_t stream);
+    int run_direct(cudaStream_t stream);
     void upload_tasks(const std::vector<FillTask>& tasks, cudaStream_t stream);
 
     const core::PlanCore* P_;
@@ -222,6 +223,8 @@ private:
     cudaGraphExec_t graph_exec_ = nullptr;
     cudaStream_t graph_stream_ = nullptr;
     int graph_launches_ = 0;
+    bool auto_graph_ = false;  // run() replays a CUDA graph (small, launch-bound transitions)
+    int runs_since_prepare_ = 0;
     cudaEvent_t mc_ev_[3] = {nullptr, nullptr, nullptr};
     std::map<std::pair<int, int>, Channel> channels_;
     bool staged_ = false;
