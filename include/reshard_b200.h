@@ -291,6 +291,8 @@ typedef struct {
     int64_t launches;      /* kernel launches per rs_exec_run */
     int64_t mc_bytes;      /* bytes delivered to peers by NVLS multicast stores */
     int64_t dup_bytes;     /* replica bytes copied on this GPU by rs_exec_run_dup */
+    int64_t scatter_bytes; /* bytes of promoted Scatter collectives this GPU pushes as their root */
+    int64_t gather_bytes;  /* bytes of promoted Gather collectives this GPU pulls as their root */
 } rs_exec_stats_t;
 
 /* ---- memory-aware arena (Algorithm 1 FreeObsoleteBuffers / eager free,
@@ -467,6 +469,13 @@ int rs_sync_status(rs_sync_t* s, int* timed_out);
  * configs, world map, model and buffer geometry: RS_ERR_CONFIG otherwise); the next
  * rs_exec_prepare builds descriptors from it. The plan must outlive its use. */
 int rs_exec_set_plan(rs_exec_t* e, const rs_plan_t* p);
+/* Execute the promoted collectives of optimize_primitives
+ * as their own primitives: a Scatter is pushed by its root, a Gather is PULLED by its root
+ * (the destination GPU reads every source's slice over NVLink into its contiguous region;
+ * one receiver's ingress is the bound and peer loads outrun peer stores there). The
+ * source buffers must then be mapped on the destination too: call before
+ * rs_exec_ipc_export, on every rank. Takes effect at the next prepare. */
+int rs_exec_set_collectives(rs_exec_t* e, int on);
 /* GPU index (in [0, n_gpus)) the executor places physical device `phys` on */
 int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu);
 

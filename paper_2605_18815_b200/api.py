@@ -194,6 +194,12 @@ class Executor:
         A.check(A.lib().rs_exec_set_plan(self.h, plan.h))
         self.plan = plan
 
+    def set_collectives(self, on: bool = True) -> None:
+        """Execute optimize_primitives' Scatter (root pushes) and Gather (root pulls over
+        NVLink) as their own primitives; call before ipc_export on every rank (a Gather's
+        root maps the source buffers too). Takes effect at the next prepare()."""
+        A.check(A.lib().rs_exec_set_collectives(self.h, int(on)))
+
     def gpu_of_phys(self, phys: int) -> int:
         """GPU index this executor places physical device `phys` on."""
         g = C.c_int()

@@ -803,6 +803,13 @@ int rs_exec_set_plan(rs_exec_t* e, const rs_plan_t* p) {
     });
 }
 
+int rs_exec_set_collectives(rs_exec_t* e, int on) {
+    return guarded([&] {
+        e->ex->set_collectives(on != 0);
+        return RS_OK;
+    });
+}
+
 int rs_exec_gpu_of_phys(const rs_exec_t* e, int phys, int* gpu) {
     return guarded([&] {
         *gpu = e->ex->gpu_of_phys(phys);
@@ -914,6 +921,8 @@ int rs_exec_stats(const rs_exec_t* e, rs_exec_stats_t* out) {
         out->launches = s.launches;
         out->mc_bytes = s.mc_bytes;
         out->dup_bytes = s.dup_bytes;
+        out->scatter_bytes = s.scatter_bytes;
+        out->gather_bytes = s.gather_bytes;
         return RS_OK;
     });
 }

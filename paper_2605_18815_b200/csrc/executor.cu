@@ -18,6 +18,7 @@
 
 #include "reshard/executor.hpp"
 #include "reshard/executor_rt.hpp"
+#include "reshard/schedule.hpp"
 
 namespace reshard {
 namespace exec {
@@ -409,6 +410,11 @@ Executor::~Executor() {
 
 int Executor::gpu_of_phys(int phys) const { return phys / per_gpu_; }
 
+void Executor::set_collectives(bool on) {
+    collectives_ = on;
+    prepared_ = false;
+}
+
 void Executor::set_plan(const core::PlanCore& P) {
     // a re-computed plan of the same transition drives the bound buffers: the layouts
     // (configs, world map, model, buffer sizes) must be identical
@@ -503,11 +509,14 @@ void* Executor::buffer(int side, int rank, int buf, std::int64_t* bytes) const {
 }
 
 std::vector<std::uint8_t> Executor::export_ipc() const {
-    // [int32 count] then per local dst buffer: int32 rank, int32 buf, int64 offset, handle
+    // [int32 count] then per local buffer: int32 rank, int32 buf | (source side << 8),
+    // int64 offset, handle. Destination buffers always (peers push into them); source
+    // buffers too when collectives are on (a Gather's root pulls from them)
     std::vector<std::uint8_t> out(4, 0);
     int count = 0;
-    for (size_t r = 0; r < bufs_[1].size(); ++r) {
-        const RankBufs& rb = bufs_[1][r];
+    for (int side = 1; side >= (collectives_ ? 0 : 1); --side)
+    for (size_t r = 0; r < bufs_[side].size(); ++r) {
+        const RankBufs& rb = bufs_[side][r];
         if (rb.gpu != cfg_.gpu) continue;
         for (int b = 0; b < kNumBufs; ++b) {
             if (!rb.ptr[b]) continue;
@@ -517,7 +526,7 @@ std::vector<std::uint8_t> Executor::export_ipc() const {
                 throw CudaError("cuMemGetAddressRange failed");
             cudaIpcMemHandle_t h;
             RS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
-            const std::int32_t rr = static_cast<std::int32_t>(r), bb = b;
+            const std::int32_t rr = static_cast<std::int32_t>(r), bb = b | (side == 0 ? 1 << 8 : 0);
             const std::int64_t off = static_cast<std::int64_t>(reinterpret_cast<CUdeviceptr>(rb.ptr[b]) - base);
             const size_t at = out.size();
             out.resize(at + 16 + sizeof h);
@@ -548,7 +557,10 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
         std::memcpy(&off, blob + at + 8, 8);
         std::memcpy(&h, blob + at + 16, sizeof h);
         at += 16 + sizeof h;
-        RankBufs& rb = bufs_[1].at(static_cast<size_t>(r));
+        const int side = (b >> 8) & 1 ? 0 : 1;
+        b &= 0xff;
+        if (b < 0 || b >= kNumBufs) throw ConfigError("ipc blob: bad buffer id");
+        RankBufs& rb = bufs_[side].at(static_cast<size_t>(r));
         if (rb.gpu == cfg_.gpu) continue;
         void* base = nullptr;
         auto key = std::string(reinterpret_cast<const char*>(&h), sizeof h);
@@ -973,6 +985,18 @@ void Executor::prepare(bool staged) {
     dup_->buckets.clear();
     dup_->lanes.clear();
     compute_dups(ops);
+    // promoted collectives (optimize_primitives over the plan's box transfers, the
+    // schedule's own rule): Scatter ops are pushed by the root as usual, Gather ops are
+    // pulled by the root from the sources' mapped buffers
+    box_coll_.clear();
+    if (collectives_ && !staged) {
+        std::vector<std::int64_t> residual;
+        const std::vector<sched::Fragment> frags = sched::plan_fragments(*P_, {});
+        box_coll_.assign(P_->box.size(), 0);
+        for (const sched::CommOp& c : sched::optimize_primitives(*P_, frags, &residual, true))
+            if (c.kind == sched::CommKind::Scatter || c.kind == sched::CommKind::Gather)
+                for (std::int64_t f : c.frags) box_coll_[static_cast<size_t>(f)] = static_cast<std::int8_t>(c.kind);
+    }
     // early dedup: launch 1 is a tail of this GPU's other peer pushes, long enough to hide the
     // replica copies (HBM, ~4.5x the NVLink push rate; RS_DUP_TAIL_FRAC, default 0.4 of the
     // largest per-GPU replica bytes); everything else, the primaries first, is launch 0
@@ -1066,7 +1090,22 @@ void Executor::prepare(bool staged) {
             }
             continue;
         }
+        const int coll = (!box_coll_.empty() && op.box >= 0) ? box_coll_[static_cast<size_t>(op.box)] : 0;
+        if (coll == static_cast<int>(sched::CommKind::Gather) && !staged && S.gpu != D.gpu) {
+            // Gather: the root (destination GPU) pulls every source's slice over NVLink
+            if (!dst_here) continue;
+            if (!S.ptr[op.src_buf] || !D.ptr[op.dst_buf])
+                throw ConfigError(strfmt("gather pull: source rank %d buffer %d not mapped here (set_collectives on every "
+                                         "rank before the ipc exchange)", op.src_side_rank, op.src_buf));
+            stats_.gather_bytes += total;
+            has_remote_ = true;
+            fused_->add(stage_of(op), reinterpret_cast<std::uint64_t>(S.ptr[op.src_buf]) + static_cast<std::uint64_t>(op.src_off),
+                        reinterpret_cast<std::uint64_t>(D.ptr[op.dst_buf]) + static_cast<std::uint64_t>(op.dst_off), op.rows,
+                        op.row_bytes, op.src_pitch, op.dst_pitch, kTile, cfg_.n_gpus + S.gpu);
+            continue;
+        }
         if (!src_here) continue;  // pushed by the source's GPU
+        if (coll == static_cast<int>(sched::CommKind::Scatter) && !dst_here) stats_.scatter_bytes += total;
         if (op_mc[oi]) {
             if (!S.ptr[op.src_buf]) throw ConfigError("prepare: multicast source buffer not bound");
             if (op_lead[oi]) mc_src_bytes_ += total;

@@ -134,7 +134,12 @@ struct Emitter {
 std::vector<CopyOp> build_ops(const PlanCore& P) {
     std::vector<CopyOp> ops;
     Emitter E{P, ops};
-    for (const core::BoxXfer& b : P.box) E.box(b.kind, b.tensor, b.src, b.dst, b.lo, b.hi);
+    for (size_t i = 0; i < P.box.size(); ++i) {
+        const core::BoxXfer& b = P.box[i];
+        const size_t first = ops.size();
+        E.box(b.kind, b.tensor, b.src, b.dst, b.lo, b.hi);
+        for (size_t k = first; k < ops.size(); ++k) ops[k].box = static_cast<int>(i);
+    }
     for (const core::BoxXfer& b : P.box_retain) E.box(b.kind, b.tensor, b.src, b.dst, b.lo, b.hi);
     const int nt = P.ntensors();
     auto overridden = [&](int j, int t) {

@@ -23,6 +23,7 @@ struct CopyOp {
     int dst_rank, dst_buf;       // dst virtual rank, buffer
     std::int64_t src_off, dst_off, rows, row_bytes, src_pitch, dst_pitch;
     int tensor = -1;             // model tensor the bytes belong to (-1: scalar blob)
+    int box = -1;                // index of the plan box transfer it moves (PlanCore::box), else -1
 };
 
 /// Device tile: <= kTileBytes of one CopyOp, absolute pointers.

@@ -43,6 +43,8 @@ struct ExecStats {
     std::int64_t ce_bytes = 0;                         // peer-bound bytes moved by copy engines
     std::int64_t mc_bytes = 0;                         // bytes delivered by multicast stores
     std::int64_t dup_bytes = 0;                        // replica bytes copied on the destination GPU
+    std::int64_t scatter_bytes = 0;                    // promoted Scatter bytes pushed as root
+    std::int64_t gather_bytes = 0;                     // promoted Gather bytes pulled as root
 };
 
 struct RankBufs {
@@ -123,6 +125,11 @@ public:
     /// drive the bound buffers with a re-computed plan of the same transition (same
     /// configs, world map, model and buffer geometry); takes effect at the next prepare()
     void set_plan(const core::PlanCore& P);
+    /// execute optimize_primitives' Scatter / Gather collectives as primitives: a
+    /// Scatter is pushed by its root; a Gather is pulled by its root (destination GPU)
+    /// from the peers' source buffers, which export_ipc then shares too. Set on every
+    /// rank before export_ipc; takes effect at the next prepare().
+    void set_collectives(bool on);
     /// memory-aware stages: destination ranks in execution order, one launch group
     /// per stage (a stage starts after all reads of earlier stages completed)
     void set_stage_order(const std::vector<int>& dst_order, const std::vector<int>& cuts = {});
@@ -212,6 +219,8 @@ private:
     std::unique_ptr<TileSet> mc_;  // multicast tiles (dst = multicast address)
     std::unique_ptr<TileSet> dup_;  // replica copies on this GPU (run_dup)
     bool dedup_ = false;
+    bool collectives_ = false;
+    std::vector<std::int8_t> box_coll_;  // per plan box transfer: 0 p2p, 2 Scatter, 3 Gather (sched::CommKind)
     std::vector<int> dup_primary_;  // per op: dst rank holding the primary copy, or -1
     std::vector<char> dup_lead_;    // per op: it carries a region other ranks on its GPU copy
     bool dup_early_ = false;

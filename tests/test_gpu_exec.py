@@ -486,3 +486,17 @@ def test_random_moe_models_vs_oracle_buffers(seed):
                 assert tensors[(1, r, b)].cpu().numpy().tobytes() == ref.buffer(r, b), (r, b)
                 n += 1
     assert n > 0
+
+
+def test_promoted_scatter_gather_executed():
+    """optimize_primitives' Scatter (TP1 -> TP4, root pushes) and Gather (TP4 -> TP1, root
+    pulls over NVLink) executed as primitives across 4 rank processes: bit-exact, and the
+    root moves exactly the schedule's promoted bytes (tests/mgpu_collectives_check.py)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+                        "--master-addr", "127.0.0.1", "--master-port", "29549",
+                        os.path.join(root, "tests", "mgpu_collectives_check.py"), "4"],
+                       capture_output=True, text=True, timeout=600)
+    assert "COLL_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
