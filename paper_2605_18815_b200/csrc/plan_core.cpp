@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <thread>
 
 namespace reshard {
 namespace core {
@@ -156,6 +157,31 @@ struct Pending {
     int dst_phys, dst_rank;
     std::vector<int> cands;
 };
+
+/// fn(i) for i in [0, n) on up to hardware_concurrency threads (contiguous blocks); the
+/// planner's per-route / per-rank-pair work is independent, results are merged in order
+template <class F>
+void parallel_for(size_t n, F&& fn) {
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>({n, hw, 16});
+    if (nt <= 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::vector<std::exception_ptr> err(nt);
+    for (size_t t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            try {
+                for (size_t i = t; i < n; i += nt) fn(i);
+            } catch (...) {
+                err[t] = std::current_exception();
+            }
+        });
+    for (auto& x : th) x.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
 
 }  // namespace
 
@@ -477,8 +503,10 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     std::vector<Pending> pend;
     std::vector<size_t> route_begin, route_end;
     const int ns = srcc.world_size();
-    for (const RouteInfo& r : P.routes) {
-        route_begin.push_back(pend.size());
+    std::vector<std::vector<Pending>> per_route(P.routes.size());
+    parallel_for(P.routes.size(), [&](size_t ri) {
+        const RouteInfo& r = P.routes[ri];
+        std::vector<Pending>& out = per_route[ri];
         if (r.dst_rank >= 0) {
             const RankGeom& D = P.dst.ranks[static_cast<size_t>(r.dst_rank)];
             const RankGeom* own = r.src_rank >= 0 ? &P.src.ranks[static_cast<size_t>(r.src_rank)] : nullptr;
@@ -504,11 +532,15 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
                         if (cands.empty())
                             throw ConfigError(strfmt("unreachable state: no source holds %s %s needed by device %d",
                                                      ts.tensor_id.c_str(), format_box(cell).c_str(), r.phys));
-                        pend.push_back(Pending{0, t, std::move(cell), r.phys, r.dst_rank, std::move(cands)});
+                        out.push_back(Pending{0, t, std::move(cell), r.phys, r.dst_rank, std::move(cands)});
                     }
                 }
             }
         }
+    });
+    for (auto& v : per_route) {
+        route_begin.push_back(pend.size());
+        for (Pending& x : v) pend.push_back(std::move(x));
         route_end.push_back(pend.size());
     }
     const size_t n_param = pend.size();
@@ -598,17 +630,19 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     if (srcc.zero_enabled) {
         const int ndst = dstc.world_size();
         std::vector<std::vector<const stair::Triple*>> by_dst(static_cast<size_t>(ndst));
-        for (int k = 0; k < ns; ++k)
-            for (int j = 0; j < ndst; ++j) {
-                const RankGeom& J = P.dst.ranks[static_cast<size_t>(j)];
-                const int own = P.wm.src_rank_of(J.phys);
-                if (own == k) continue;  // R_j ∩ S_own = ∅
-                const RankGeom* O = own >= 0 ? &P.src.ranks[static_cast<size_t>(own)] : nullptr;
-                for (int t = 0; t < nt; ++t) {
-                    stair::Triple T;
-                    if (make_triple(space, t, P.src.ranks[static_cast<size_t>(k)], J, O, &T)) P.triples.push_back(T);
-                }
+        std::vector<std::vector<stair::Triple>> per_pair(static_cast<size_t>(ns) * ndst);
+        parallel_for(per_pair.size(), [&](size_t kj) {
+            const int k = static_cast<int>(kj) / ndst, j = static_cast<int>(kj) % ndst;
+            const RankGeom& J = P.dst.ranks[static_cast<size_t>(j)];
+            const int own = P.wm.src_rank_of(J.phys);
+            if (own == k) return;  // R_j ∩ S_own = ∅
+            const RankGeom* O = own >= 0 ? &P.src.ranks[static_cast<size_t>(own)] : nullptr;
+            for (int t = 0; t < nt; ++t) {
+                stair::Triple T;
+                if (make_triple(space, t, P.src.ranks[static_cast<size_t>(k)], J, O, &T)) per_pair[kj].push_back(T);
             }
+        });
+        for (const auto& v : per_pair) P.triples.insert(P.triples.end(), v.begin(), v.end());
         for (const stair::Triple& T : P.triples) by_dst[static_cast<size_t>(T.dst)].push_back(&T);
         for (const RouteInfo& r : P.routes) {
             if (r.src_rank < 0 || r.dst_rank < 0) continue;
@@ -629,10 +663,25 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         if (d2_possible) {
             // cursor position after box pendings (params, grads) for the extension
             std::int64_t cur = cursor;
-            for (const RouteInfo& r : P.routes) {
+            std::vector<D2Route> per_route(P.routes.size());
+            auto route_d2 = [&](size_t ri, std::int64_t* c) {
+                const RouteInfo& r = P.routes[ri];
+                if (r.dst_rank >= 0)
+                    per_route[ri] = d2_route(P, r.dst_rank, by_dst[static_cast<size_t>(r.dst_rank)], allow_oversourced, c);
+            };
+            if (opts.balance_fanout) {  // the cursor threads through the routes in order
+                for (size_t ri = 0; ri < P.routes.size(); ++ri) route_d2(ri, &cur);
+            } else {  // proximity rule: routes are independent
+                parallel_for(P.routes.size(), [&](size_t ri) {
+                    std::int64_t unused = 0;
+                    route_d2(ri, &unused);
+                });
+            }
+            for (size_t ri = 0; ri < P.routes.size(); ++ri) {
+                const RouteInfo& r = P.routes[ri];
                 if (r.dst_rank < 0) continue;
                 const int j = r.dst_rank;
-                D2Route R = d2_route(P, j, by_dst[static_cast<size_t>(j)], allow_oversourced, &cur);
+                D2Route& R = per_route[ri];
                 if (R.bad.empty()) continue;
                 if (!allow_oversourced)
                     throw ConfigError(strfmt("unreachable state: optimizer interval [%lld:%lld] for device %d not fully sourced",
@@ -660,29 +709,36 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         }
         // transfer count + bytes: the triples' runs, minus those inside over-sourced
         // intervals, plus the D2 runs that replace them
-        for (const stair::Triple& T : P.triples) flat_elems += triple_count(T);
-        flat_elems += d2_patch_elems - d2_regular_elems;
-        {
-            // count transfers exactly: merged runs per (src,dst) group
-            // per band in O(1): rows x pieces, minus row-to-row merges when the pattern
-            // wraps (first piece at column 0, last at the row end), minus a merge with the
-            // previous band / triple of the same (src, dst) when they abut
-            std::int64_t cnt = 0;
-            int cs = -1, cd = -1;
-            std::int64_t last_hi = -1;
-            for (const stair::Triple& T : P.triples)
+        // (src, dst) groups of consecutive triples are independent: count them in parallel
+        std::vector<size_t> gstart;
+        for (size_t i = 0; i < P.triples.size(); ++i)
+            if (i == 0 || P.triples[i].src != P.triples[i - 1].src || P.triples[i].dst != P.triples[i - 1].dst)
+                gstart.push_back(i);
+        gstart.push_back(P.triples.size());
+        std::vector<std::int64_t> g_elems(gstart.size(), 0), g_runs(gstart.size(), 0);
+        parallel_for(gstart.size() - 1, [&](size_t g) {
+            std::int64_t cnt = 0, el = 0, last_hi = -1;
+            for (size_t i = gstart[g]; i < gstart[g + 1]; ++i) {
+                const stair::Triple& T = P.triples[i];
+                el += triple_count(T);
+                // per band in O(1): rows x pieces, minus row-to-row merges when the pattern
+                // wraps (first piece at column 0, last at the row end), minus a merge with the
+                // previous band / triple of the same (src, dst) when they abut
                 for_each_band(T, [&](const std::int64_t* p, std::int64_t u, std::int64_t v, const stair::Iv* cols, int n) {
                     const std::int64_t first_lo = stair::flat_of(T.t, p, u, cols[0].lo);
                     const bool wrap = cols[0].lo == 0 && cols[n - 1].hi == T.t.cols;
-                    std::int64_t c = (v - u) * n - (wrap ? v - u - 1 : 0);
-                    if (T.src == cs && T.dst == cd && first_lo == last_hi) --c;
-                    cnt += c;
-                    cs = T.src;
-                    cd = T.dst;
+                    cnt += (v - u) * n - (wrap ? v - u - 1 : 0) - (first_lo == last_hi ? 1 : 0);
                     last_hi = stair::flat_of(T.t, p, v - 1, cols[n - 1].hi);
                 });
-            P.n_flat = cnt - d2_regular_runs + static_cast<std::int64_t>(P.d2_runs.size());
-        }
+            }
+            g_runs[g] = cnt;
+            g_elems[g] = el;
+        });
+        for (size_t g = 0; g + 1 < gstart.size(); ++g) flat_elems += g_elems[g];
+        flat_elems += d2_patch_elems - d2_regular_elems;
+        std::int64_t total_runs = 0;
+        for (size_t g = 0; g + 1 < gstart.size(); ++g) total_runs += g_runs[g];
+        P.n_flat = total_runs - d2_regular_runs + static_cast<std::int64_t>(P.d2_runs.size());
     }
 
     // ---- scalars (routing.hpp:341-353)
