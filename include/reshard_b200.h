@@ -337,6 +337,11 @@ int rs_memory_schedule_level(const rs_plan_t* plan_ab, int n_gpus, int level, in
  * across GPUs, take the first level whose footprint fits on every rank */
 int rs_memory_schedule_footprints(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                                   int n_gpus, int gpu, int64_t* out, int cap, int* n);
+/* the same ladder with each level's modeled seconds (per stage group: the busiest GPU's
+ * NVLink / HBM bound plus a barrier; both directions): pick the fastest level that fits
+ * the cap on every GPU */
+int rs_memory_schedule_costs(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
+                             int n_gpus, int gpu, int64_t* bytes, double* seconds, int cap, int* n);
 /* the plan's stage cuts of direction `dir` (1 = a barrier precedes that position) */
 int rs_memory_plan_cuts(const rs_plan_t* plan_ab, const rs_plan_t* plan_ba, int64_t chunk_bytes, int with_grads,
                         int n_gpus, int gpu, int groups, int bands, int dir, int* cuts, int cap, int* n);

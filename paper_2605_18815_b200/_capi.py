@@ -225,6 +225,8 @@ def _late_bindings(L):
         ("rs_memory_plan_cuts", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_int), C.c_int,
                                  P(C.c_int)]),
         ("rs_memory_schedule_footprints", [vp, vp, i64, C.c_int, C.c_int, C.c_int, P(i64), C.c_int, P(C.c_int)]),
+        ("rs_memory_schedule_costs", [vp, vp, i64, C.c_int, C.c_int, C.c_int, P(i64), P(C.c_double), C.c_int,
+                                      P(C.c_int)]),
         ("rs_memory_plan_ex", [vp, vp, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(ArenaStats_t), P(i64), P(C.c_int),
                                P(C.c_int), C.c_int]),
         ("rs_memory_min_groups", [vp, vp, i64, C.c_int, C.c_int, C.c_int, i64, P(C.c_int), P(i64)]),

@@ -659,6 +659,17 @@ def memory_schedule_footprints(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpu
     return list(out[: n.value])
 
 
+def memory_schedule_costs(ab: RoutingPlan, ba: Optional[RoutingPlan], n_gpus: int, gpu: int,
+                          chunk_bytes: int = 0, with_grads: bool = False):
+    """[(physical bytes on `gpu`, modeled seconds)] at every level of the schedule ladder."""
+    n = C.c_int()
+    b = (C.c_int64 * 4096)()
+    t = (C.c_double * 4096)()
+    A.check(A.lib().rs_memory_schedule_costs(ab.h, ba.h if ba else None, chunk_bytes, int(with_grads), n_gpus, gpu,
+                                             b, t, 4096, C.byref(n)))
+    return [(b[i], t[i]) for i in range(n.value)]
+
+
 def memory_schedule_level(ab: RoutingPlan, level: int, n_gpus: int = 1):
     """(bands, groups) of a schedule level of the n_gpus ladder (groups -1: rounds)."""
     b, g = C.c_int(), C.c_int()

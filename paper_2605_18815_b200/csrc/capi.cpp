@@ -1111,6 +1111,21 @@ int rs_memory_schedule(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_b
     });
 }
 
+int rs_memory_schedule_costs(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus,
+                             int gpu, int64_t* bytes, double* seconds, int cap, int* n) {
+    return guarded([&] {
+        if (n_gpus < 1 || gpu < 0 || gpu >= n_gpus) throw ConfigError("bad arena placement");
+        const auto f = mem::schedule_costs(ab->core, ba ? &ba->core : nullptr, chunk_bytes > 0 ? chunk_bytes : (32ll << 20),
+                                           with_grads != 0, n_gpus, gpu);
+        *n = static_cast<int>(f.size());
+        for (int i = 0; i < *n && i < cap; ++i) {
+            bytes[i] = f[static_cast<size_t>(i)].first;
+            seconds[i] = f[static_cast<size_t>(i)].second;
+        }
+        return RS_OK;
+    });
+}
+
 int rs_memory_schedule_footprints(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes, int with_grads, int n_gpus,
                                   int gpu, int64_t* out, int cap, int* n) {
     return guarded([&] {

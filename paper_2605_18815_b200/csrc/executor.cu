@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <queue>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -578,27 +579,34 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
 
 void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
                   std::int64_t dp, std::int64_t kTile, int lane) {
+    // recorded here, cut into tiles by finalize() on host threads
     if (rows <= 0 || rb <= 0) return;
+    pending.push_back(Pending{src, dst, rows, rb, sp, dp, kTile, key, lane});
+}
+
+void TileSet::expand(const Pending& q, std::vector<std::vector<Tile>>& bk, std::vector<std::vector<std::uint8_t>>& ln) {
+    std::int64_t rows = q.rows, rb = q.rb;
+    const std::int64_t sp = q.sp, dp = q.dp, kTile = q.kTile;
     if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
         rb *= rows;
         rows = 1;
     }
-    if (static_cast<int>(buckets.size()) < (key + 1) * 5) {
-        buckets.resize(static_cast<size_t>(key + 1) * 5);
-        lanes.resize(buckets.size());
+    if (static_cast<int>(bk.size()) < (q.key + 1) * 5) {
+        bk.resize(static_cast<size_t>(q.key + 1) * 5);
+        ln.resize(bk.size());
     }
     auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
         Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
                static_cast<std::uint32_t>(nb)};
         std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
         if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-        const size_t b = static_cast<size_t>(key) * 5 + class_index(align_class(a));
-        buckets[b].push_back(t);
-        lanes[b].push_back(static_cast<std::uint8_t>(lane));
+        const size_t b = static_cast<size_t>(q.key) * 5 + class_index(align_class(a));
+        bk[b].push_back(t);
+        ln[b].push_back(static_cast<std::uint8_t>(q.lane));
     };
     if (rows == 1 || rb >= kTile) {
         for (std::int64_t r = 0; r < rows; ++r) {
-            std::uint64_t s = src + static_cast<std::uint64_t>(r * sp), d = dst + static_cast<std::uint64_t>(r * dp);
+            std::uint64_t s = q.src + static_cast<std::uint64_t>(r * sp), d = q.dst + static_cast<std::uint64_t>(r * dp);
             std::int64_t left = rb;
             // peel an unaligned head so the body runs 16-byte vectors when both sides
             // share the same misalignment (relative offsets keep it: bases are 256-B aligned)
@@ -623,7 +631,7 @@ void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t ro
         const std::int64_t per = std::max<std::int64_t>(1, kTile / rb);
         for (std::int64_t r = 0; r < rows; r += per) {
             const std::int64_t nr = std::min(per, rows - r);
-            emit(src + static_cast<std::uint64_t>(r * sp), dst + static_cast<std::uint64_t>(r * dp), nr, rb);
+            emit(q.src + static_cast<std::uint64_t>(r * sp), q.dst + static_cast<std::uint64_t>(r * dp), nr, rb);
         }
     }
 }
@@ -683,20 +691,90 @@ void interleave_lanes(std::vector<Tile>* v, const std::vector<std::uint8_t>& lan
 }  // namespace
 
 void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging) {
+    // 1) cut the recorded copies into tiles on host threads: contiguous slices of the
+    //    record list, one bucket set per thread, concatenated in slice order (the same
+    //    tile order a single thread produces)
+    const size_t nrec = pending.size();
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::max<size_t>(1, std::min<size_t>({hw, 16, nrec / 256 + 1}));
+    std::vector<std::vector<std::vector<Tile>>> tb(nt);
+    std::vector<std::vector<std::vector<std::uint8_t>>> tl(nt);
+    {
+        auto work = [&](size_t t) {
+            const size_t lo = nrec * t / nt, hi = nrec * (t + 1) / nt;
+            for (size_t i = lo; i < hi; ++i) expand(pending[i], tb[t], tl[t]);
+        };
+        std::vector<std::thread> th;
+        for (size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+    }
+    pending.clear();
+    size_t nb = 0;
+    for (const auto& v : tb) nb = std::max(nb, v.size());
+    // 2) one group per non-empty bucket (key * 5 + class, ascending)
     host.clear();
     groups.clear();
-    for (size_t b = 0; b < buckets.size(); ++b) {
-        auto& v = buckets[b];
-        if (v.empty()) continue;
-        if (interleave) interleave_lanes(&v, lanes[b]);
+    std::vector<size_t> begin(nb, 0);
+    size_t total = 0;
+    for (size_t b = 0; b < nb; ++b) {
+        size_t n = 0;
+        for (size_t t = 0; t < nt; ++t) n += b < tb[t].size() ? tb[t][b].size() : 0;
+        begin[b] = total;
+        if (!n) continue;
         const int c = static_cast<int>(b % 5);
-        groups.push_back({c, static_cast<int>(host.size()), static_cast<int>(v.size()), static_cast<int>(b / 5)});
-        host.insert(host.end(), v.begin(), v.end());
-        if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(v.size());
+        groups.push_back({c, static_cast<int>(total), static_cast<int>(n), static_cast<int>(b / 5)});
+        if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(n);
+        total += n;
     }
-    buckets.clear();
-    lanes.clear();
-    if (!host.empty()) {
+    // 3) assemble straight into the pinned staging buffer (threads per bucket slice);
+    //    buckets with several destination lanes are interleaved first
+    Tile* out = nullptr;
+    if (total) {
+        if (!staging) throw std::logic_error("TileSet::finalize needs a staging buffer");
+        if (staging->size() < total * sizeof(Tile)) staging->grow(total * sizeof(Tile) * 5 / 4);
+        out = static_cast<Tile*>(staging->ptr);
+    }
+    std::vector<std::thread> th;
+    for (size_t b = 0; b < nb; ++b) {
+        size_t n = 0, lanes_seen = 0;
+        std::uint8_t lane0 = 0;
+        bool multi_lane = false;
+        for (size_t t = 0; t < nt; ++t) {
+            if (b >= tb[t].size()) continue;
+            n += tb[t][b].size();
+            if (interleave)
+                for (std::uint8_t l : tl[t][b]) {
+                    if (lanes_seen++ == 0) lane0 = l;
+                    else if (l != lane0) multi_lane = true;
+                }
+        }
+        if (!n) continue;
+        if (interleave && multi_lane) {
+            std::vector<Tile> v;
+            std::vector<std::uint8_t> l;
+            v.reserve(n);
+            l.reserve(n);
+            for (size_t t = 0; t < nt; ++t) {
+                if (b >= tb[t].size()) continue;
+                v.insert(v.end(), tb[t][b].begin(), tb[t][b].end());
+                l.insert(l.end(), tl[t][b].begin(), tl[t][b].end());
+            }
+            interleave_lanes(&v, l);
+            std::memcpy(out + begin[b], v.data(), n * sizeof(Tile));
+            continue;
+        }
+        size_t at = begin[b];
+        for (size_t t = 0; t < nt; ++t) {
+            if (b >= tb[t].size() || tb[t][b].empty()) continue;
+            const Tile* src = tb[t][b].data();
+            const size_t cnt = tb[t][b].size();
+            th.emplace_back([=] { std::memcpy(out + at, src, cnt * sizeof(Tile)); });
+            at += cnt;
+        }
+    }
+    for (auto& x : th) x.join();
+    if (total) {
         // two descriptor buffers used in turn: a re-prepare uploads into the one the last
         // launch did not read, so it may overlap kernels of the previous prepare still in
         // flight. Both are kept across re-prepares: with peer access enabled every
@@ -708,27 +786,21 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
             fence_pool.push_back(e);
         }
         fences[cur].clear();
-        if (host.size() * sizeof(Tile) > dev_bytes[cur]) {
+        if (total * sizeof(Tile) > dev_bytes[cur]) {
             if (dev_buf[cur]) cudaFree(dev_buf[cur]);
             dev_buf[cur] = nullptr;
-            dev_bytes[cur] = host.size() * sizeof(Tile) * 5 / 4;
+            dev_bytes[cur] = total * sizeof(Tile) * 5 / 4;
             RS_CUDA(cudaMalloc(&dev_buf[cur], dev_bytes[cur]));
         }
         dev = dev_buf[cur];
         // private non-blocking stream: descriptor uploads never serialize with the
         // caller's (training) streams, so the EDM can prepare in the background
-        const size_t bytes = host.size() * sizeof(Tile);
-        if (staging && staging->size() < bytes) staging->grow(bytes);
-        if (staging) {  // pinned staging: DMA at PCIe speed instead of a pageable bounce
-            std::memcpy(staging->ptr, host.data(), bytes);
-            RS_CUDA(cudaMemcpyAsync(dev, staging->ptr, bytes, cudaMemcpyHostToDevice, upload));
-        } else {
-            RS_CUDA(cudaMemcpyAsync(dev, host.data(), bytes, cudaMemcpyHostToDevice, upload));
-        }
+        RS_CUDA(cudaMemcpyAsync(dev, out, total * sizeof(Tile), cudaMemcpyHostToDevice, upload));
         RS_CUDA(cudaStreamSynchronize(upload));
     }
+    ntiles = total;
     if (stats) {
-        stats->tiles += static_cast<std::int64_t>(host.size());
+        stats->tiles += static_cast<std::int64_t>(total);
         stats->launches += static_cast<std::int64_t>(groups.size());
     }
 }
@@ -962,8 +1034,7 @@ void Executor::prepare(bool staged) {
     ce_min_bytes_ = ce ? std::atoll(ce) : 0;
     channels_.clear();
     if (!fused_) fused_ = std::make_unique<TileSet>();  // reused: keeps its device buffer
-    fused_->buckets.clear();
-    fused_->lanes.clear();
+    fused_->pending.clear();
     {
         const char* to = std::getenv("RS_TILE_ORDER");
         fused_->interleave = !(to && std::string(to) == "op");
@@ -982,8 +1053,7 @@ void Executor::prepare(bool staged) {
     }
     if (!mc_) mc_ = std::make_unique<TileSet>();
     if (!dup_) dup_ = std::make_unique<TileSet>();
-    dup_->buckets.clear();
-    dup_->lanes.clear();
+    dup_->pending.clear();
     compute_dups(ops);
     // promoted collectives (optimize_primitives over the plan's box transfers, the
     // schedule's own rule): Scatter ops are pushed by the root as usual, Gather ops are
@@ -1023,8 +1093,7 @@ void Executor::prepare(bool staged) {
         }
     }
     mc_src_bytes_ = 0;
-    mc_->buckets.clear();
-    mc_->lanes.clear();
+    mc_->pending.clear();
     // ops delivered by a multicast store stream: -1 no, else the multicast address; the
     // first op of each source region (lead) emits the tiles, the other members' copies ride along
     std::vector<std::uint64_t> op_mc(ops.size(), 0);

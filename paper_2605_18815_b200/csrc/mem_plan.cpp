@@ -46,6 +46,13 @@ UnitMap::UnitMap(const core::PlanCore& P, int bands) : nb(std::max(1, bands)), n
     for (size_t t = 0; t < ents.size(); ++t) band_of_tensor[t] = ents[t].spec.layer * nb / L;
 }
 
+/// source pipeline stages a band-interleaved group takes one band from: the source
+/// config's pp degree when it divides the band count, else 1
+int interleave_stride(const core::PlanCore& P, int nb) {
+    const int S = std::max(1, P.src_cfg.pp);
+    return nb % S == 0 ? S : 1;
+}
+
 namespace {
 
 // One greedy pass over the units. kFreed: the stage freeing the most old bytes anywhere.
@@ -180,6 +187,20 @@ MemoryPlan plan_memory(const core::PlanCore& ab, const core::PlanCore* ba, std::
 MemoryPlan plan_memory_ops(const core::PlanCore& ab, const core::PlanCore* ba, const std::vector<exec::CopyOp>& ops_ab,
                            const std::vector<exec::CopyOp>& ops_ba, std::int64_t C, bool with_grads, int n_gpus, int gpu,
                            int groups, int bands) {
+    if (groups == kBandInterleaved) {
+        // bands in an order that takes one band from each source pipeline stage per
+        // group, all destination ranks of a band together: every group draws on every
+        // source GPU and feeds every destination GPU, and each group's new data can reuse
+        // the old chunks of the groups before it
+        const UnitMap U(ab, bands);
+        const int S = interleave_stride(ab, U.nb);
+        std::vector<int> order;
+        for (int i = 0; i < U.nb; ++i) {
+            const int band = (i % S) * (U.nb / S) + i / S;
+            for (int j = 0; j < U.nd; ++j) order.push_back(j * U.nb + band);
+        }
+        return plan_with_order(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, U.nb / S, bands, order);
+    }
     if (groups < 0) {  // rounds: one unit per GPU per group
         const int G = std::max(1, n_gpus);
         const int units = UnitMap(ab, bands).count();
@@ -351,6 +372,8 @@ std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab, int n_gpus)
         for (int k = 1; k < units; k *= 2) ks.push_back(k);
         ks.push_back(units);
         bool rounds_done = G < 2 || rounds < 2;
+        // across GPUs: the band-interleaved order (every group spans every GPU's links)
+        if (G >= 2 && n >= 2) v.push_back({n, kBandInterleaved});
         for (int k : ks) {
             if (!rounds_done && k >= rounds) {
                 v.push_back({n, -1});
@@ -402,6 +425,60 @@ std::vector<std::int64_t> schedule_footprints(const core::PlanCore& ab, const co
     std::vector<std::int64_t> out;
     for (const ScheduleLevel& L : schedule_levels(ab, n_gpus))
         out.push_back(plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, L.groups, L.bands).stats.physical_bytes);
+    return out;
+}
+
+double estimate_seconds(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,
+                        const std::vector<exec::CopyOp>& ops_ab, const std::vector<exec::CopyOp>& ops_ba, int n_gpus) {
+    // a stage group runs as one launch per GPU: its time is the busiest GPU's bound —
+    // NVLink out, NVLink in, or HBM (local copies read + write, peer traffic once) — plus
+    // one barrier; groups run one after another
+    constexpr double kNvlink = 690e9, kHbm = 6200e9, kBarrier = 30e-6;
+    const int G = std::max(1, n_gpus);
+    double total = 0.0;
+    for (int d = 0; d < (ba ? 2 : 1); ++d) {
+        const core::PlanCore& P = d == 0 ? ab : *ba;
+        const std::vector<exec::CopyOp>& ops = d == 0 ? ops_ab : ops_ba;
+        const UnitMap U(P, mp.bands);
+        const std::vector<int> pos = positions(mp.order[d], static_cast<size_t>(U.count()));
+        std::vector<int> grp(mp.order[d].size(), 0);
+        int ng = 0;
+        for (size_t s = 0; s < grp.size(); ++s) {
+            if (s == 0 || (s < mp.cut[d].size() && mp.cut[d][s])) ++ng;
+            grp[s] = ng - 1;
+        }
+        ng = std::max(ng, 1);
+        const int per = gpu_block(P, G);
+        std::vector<double> out(static_cast<size_t>(ng) * G, 0.0), in(out.size(), 0.0), loc(out.size(), 0.0);
+        for (const exec::CopyOp& op : ops) {
+            const int gs = P.wm.src_phys[static_cast<size_t>(op.src_side_rank)] / per;
+            const int gd = P.wm.dst_phys[static_cast<size_t>(op.dst_rank)] / per;
+            const size_t k = static_cast<size_t>(grp[static_cast<size_t>(pos[static_cast<size_t>(U.unit(op.dst_rank, op.tensor))])]);
+            const double b = static_cast<double>(op.rows) * static_cast<double>(op.row_bytes);
+            if (gs == gd) loc[k * G + gs] += b;
+            else out[k * G + gs] += b, in[k * G + gd] += b;
+        }
+        for (int k = 0; k < ng; ++k) {
+            double t = 0.0;
+            for (int g = 0; g < G; ++g) {
+                const size_t i = static_cast<size_t>(k) * G + g;
+                t = std::max({t, out[i] / kNvlink, in[i] / kNvlink, (2 * loc[i] + out[i] + in[i]) / kHbm});
+            }
+            total += t + kBarrier;
+        }
+    }
+    return total;
+}
+
+std::vector<std::pair<std::int64_t, double>> schedule_costs(const core::PlanCore& ab, const core::PlanCore* ba,
+                                                            std::int64_t C, bool with_grads, int n_gpus, int gpu) {
+    const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
+    const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
+    std::vector<std::pair<std::int64_t, double>> out;
+    for (const ScheduleLevel& L : schedule_levels(ab, n_gpus)) {
+        const MemoryPlan mp = plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, L.groups, L.bands);
+        out.push_back({mp.stats.physical_bytes, estimate_seconds(mp, ab, ba, ops_ab, ops_ba, n_gpus)});
+    }
     return out;
 }
 

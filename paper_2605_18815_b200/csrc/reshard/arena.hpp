@@ -92,8 +92,13 @@ int min_stage_groups(const core::PlanCore& ab, const core::PlanCore* ba, std::in
                      int gpu, std::int64_t cap, std::int64_t* physical);
 /// The schedule ladder, cheapest first: for bands 1, 2, 4, ... (up to the layer count)
 /// group counts from one (no aliasing) to one per unit (most aliasing).
+/// groups value of the band-interleaved order: bands ordered so each concurrency group
+/// holds one band of every source pipeline stage, all destination ranks of a band
+/// together (groups = bands / src pp)
+constexpr int kBandInterleaved = -2;
+int interleave_stride(const core::PlanCore& P, int nb);
 struct ScheduleLevel {
-    int bands, groups;  // groups -1: rounds (one unit per GPU per group)
+    int bands, groups;  // groups -1: rounds (one unit per GPU per group); -2: band-interleaved
 };
 std::vector<ScheduleLevel> schedule_levels(const core::PlanCore& ab, int n_gpus = 1);
 /// first level of the ladder whose plan fits `cap` on `gpu` (-1: none; *physical = the
@@ -104,6 +109,14 @@ int choose_schedule(const core::PlanCore& ab, const core::PlanCore* ba, std::int
 /// rank marks its feasible levels, the group takes the first level feasible everywhere)
 std::vector<std::int64_t> schedule_footprints(const core::PlanCore& ab, const core::PlanCore* ba, std::int64_t chunk,
                                               bool with_grads, int n_gpus, int gpu);
+/// Modeled time of a plan's stages (both directions): per concurrency group the busiest
+/// GPU's NVLink-out / NVLink-in / HBM bound plus a barrier, groups in sequence. Used to
+/// pick, among the schedule levels that fit the cap everywhere, the fastest.
+double estimate_seconds(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,
+                        const std::vector<exec::CopyOp>& ops_ab, const std::vector<exec::CopyOp>& ops_ba, int n_gpus);
+/// (physical bytes on `gpu`, modeled seconds) at every level of the ladder
+std::vector<std::pair<std::int64_t, double>> schedule_costs(const core::PlanCore& ab, const core::PlanCore* ba,
+                                                            std::int64_t chunk, bool with_grads, int n_gpus, int gpu);
 /// Group consecutive stages that may run concurrently (fills mp.cut): a barrier only
 /// where a stage overwrites a chunk an earlier stage of the running group still reads.
 void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,

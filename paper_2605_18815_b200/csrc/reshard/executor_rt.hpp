@@ -71,10 +71,16 @@ struct TileSet {
     struct Group {
         int cls, begin, count, key;
     };
-    std::vector<std::vector<Tile>> buckets;  // [key * 5 + class] while building
-    std::vector<std::vector<std::uint8_t>> lanes;  // per bucket tile: destination lane (GPU)
+    /// a recorded 2-D copy (add), cut into tiles at finalize
+    struct Pending {
+        std::uint64_t src, dst;
+        std::int64_t rows, rb, sp, dp, kTile;
+        int key, lane;
+    };
+    std::vector<Pending> pending;
     bool interleave = false;  // finalize: interleave lanes in proportion to their bytes
-    std::vector<Tile> host;
+    std::vector<Tile> host;   // unused since finalize assembles in pinned staging
+    size_t ntiles = 0;
     std::vector<Group> groups;
     void* dev = nullptr;                    // descriptors of the last finalize (dev_buf[cur])
     void* dev_buf[2] = {nullptr, nullptr};  // used in turn by successive finalizes
@@ -96,6 +102,9 @@ struct TileSet {
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
              std::int64_t dp, std::int64_t kTile, int lane = 0);
     void finalize(ExecStats* stats, cudaStream_t upload, struct PinnedBuf* staging);
+    /// tiles of one recorded copy into per-bucket vectors (key * 5 + alignment class)
+    static void expand(const Pending& q, std::vector<std::vector<Tile>>& buckets,
+                       std::vector<std::vector<std::uint8_t>>& lanes);
     /// launch groups in key order; key_mod > 0 restricts to keys with key % key_mod == key_rem
     int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk,
                int key_mod = 0, int key_rem = 0) const;

@@ -269,19 +269,26 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
     import torch
     import torch.distributed as dist
 
-    from .api import Arena, memory_schedule_footprints, memory_schedule_level
+    from .api import Arena, memory_schedule_costs, memory_schedule_level
     if cap_bytes <= 0:
         cap_bytes = torch.cuda.mem_get_info(device)[0] - (1 << 30)
-    # every rank marks the ladder levels that fit its cap; the first level feasible on all
-    need = memory_schedule_footprints(ab, ba, world, rank, chunk_bytes)
+    # every rank marks the ladder levels that fit its cap and models each level's time
+    # (stage groups in sequence, each bound by its busiest GPU's NVLink or HBM); the group
+    # takes the fastest level feasible on all GPUs (max over ranks of the modeled time:
+    # each rank models with its own stage cuts, the union of cuts only adds groups)
+    costs = memory_schedule_costs(ab, ba, world, rank, chunk_bytes)
+    need = [b for b, _ in costs]
     ok = torch.tensor([1 if x <= cap_bytes else 0 for x in need], dtype=torch.int32, device="cuda")
+    est = torch.tensor([t for _, t in costs], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        dist.all_reduce(est, op=dist.ReduceOp.MAX)
     fits = [i for i, v in enumerate(ok.tolist()) if v]
     if not fits:
         raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs >= {min(need) / 1e9:.2f} GB, "
                                               f"cap {cap_bytes / 1e9:.2f} GB)")
-    lv = fits[0]
+    t = est.tolist()
+    lv = min(fits, key=lambda i: (t[i], i))
     bands, k = memory_schedule_level(ab, lv, world)
     arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k, bands=bands)
     exchange_arena(arena, rank, world, tag)
