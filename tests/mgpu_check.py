@@ -27,6 +27,9 @@ def main():
     # --random K: only K random toy MoE models (the generator of tests/test_spec_kats.py)
     n_random = int(sys.argv[sys.argv.index("--random") + 1]) if "--random" in sys.argv else 0
     dedup = dedup or early
+    # --oracle: every local buffer compared byte for byte with the oracle's CPU executor
+    # (forward destinations, and the source layout the way back rebuilds)
+    check_oracle = "--oracle" in sys.argv
     # more ranks than GPUs (e.g. 8 ranks on a 4-GPU box, or 2/4 on a 1-GPU box) exercise
     # the N>1 placement: ranks sharing a device still exchange cudaIpc handles / VMM
     # descriptors and push through them (gloo plumbing, runtime.init_dist)
@@ -53,6 +56,7 @@ def main():
         fwd = Transition(ab, world, rank, local, alloc=False)
         bwd = Transition(ba, world, rank, local, alloc=False)
         keep = []
+        mine = {}  # (side of the forward plan, rank, buf) -> this rank's tensor
         if vmm:
             from paper_2605_18815_b200.runtime import share_buffers
             tag = f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}"
@@ -68,6 +72,7 @@ def main():
                     if n and g == rank:
                         t = torch.zeros(n, dtype=torch.uint8, device="cuda")
                         keep.append(t)
+                        mine[(side_ab, r, b)] = t
                         fwd.ex.bind(side_ab, r, b, t.data_ptr(), n)
                         bwd.ex.bind(1 - side_ab, r, b, t.data_ptr(), n)
         if dedup:
@@ -109,12 +114,29 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
+        ora = 0
+        if check_oracle and mine:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyoracle as O
+            osc = O.OScenario(sc.text())
+            osrc = O.OState(osc, 0)
+            osrc.load(seed)
+            odst = O.OState(osc, 1)
+            O.execute(O.OPlan(osc, True), osrc, odst, nthreads=4)
+            for (side, r, b), t in mine.items():
+                if side == A.SIDE_DST and t.cpu().numpy().tobytes() != odst.buffer(r, b):
+                    ora += 1
         bwd_run()
         torch.cuda.synchronize()
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
+        if check_oracle and mine:
+            for (side, r, b), t in mine.items():
+                if side == A.SIDE_SRC and t.cpu().numpy().tobytes() != osrc.buffer(r, b):
+                    ora += 1
+            bad_b += ora
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''}{'(early)' if early else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'oracle-checked ' if check_oracle and mine else ''}{'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''}{'(early)' if early else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep
