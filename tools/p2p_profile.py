@@ -27,17 +27,20 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--gpus", type=int, default=2)
+    ap.add_argument("--same-device", action="store_true",
+                    help="place every executor's GPU on device 0 (one-GPU boxes: the one-process multi-executor path)")
     args = ap.parse_args()
     G = args.gpus
-    if torch.cuda.device_count() < G:
+    dev = (lambda g: 0) if args.same_device else (lambda g: g)
+    if not args.same_device and torch.cuda.device_count() < G:
         print(json.dumps({"skipped": f"needs {G} GPUs"}))
         return
     for a in range(G):
         for b in range(G):
-            if a != b:
-                enable_peer_access(a, b)
+            if dev(a) != dev(b):
+                enable_peer_access(dev(a), dev(b))
     plan = RoutingPlan.from_scenario(S.config2(args.layers))
-    ex = [Executor(plan, n_gpus=G, gpu=g, device=g) for g in range(G)]
+    ex = [Executor(plan, n_gpus=G, gpu=g, device=dev(g)) for g in range(G)]
     keep = []
     for side in (A.SIDE_SRC, A.SIDE_DST):
         n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
@@ -46,31 +49,31 @@ def main():
                 _, nbytes, g = ex[0].buffer(side, r, b)
                 if not nbytes:
                     continue
-                t = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{g}")
+                t = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{dev(g)}")
                 keep.append(t)
                 for e in ex:  # every executor sees every buffer (peer pointers for the other GPU's)
                     e.bind(side, r, b, t.data_ptr(), nbytes)
     seed = 0xD00D
     streams = []
     for g, e in enumerate(ex):
-        torch.cuda.set_device(g)
+        torch.cuda.set_device(dev(g))
         e.prepare()
         e.fill(A.SIDE_SRC, seed)
-        streams.append(torch.cuda.Stream(device=g))
+        streams.append(torch.cuda.Stream(device=dev(g)))
     for g in range(G):
-        torch.cuda.synchronize(g)
+        torch.cuda.synchronize(dev(g))
 
     def step():
         evs = []
         for g, e in enumerate(ex):
-            with torch.cuda.device(g):
+            with torch.cuda.device(dev(g)):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(streams[g])
                 e.run(streams[g].cuda_stream)
                 e1.record(streams[g])
                 evs.append((e0, e1))
         for g in range(G):
-            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(dev(g))
         return [a.elapsed_time(b) for a, b in evs]
 
     step()
