@@ -140,9 +140,9 @@ const CommSet& CommCache::get_or_create(const std::string& key, const std::uint8
     t0 = std::chrono::steady_clock::now();
     for (int d = 0; d < kCommDims; ++d) {
         if (!colors || colors[d] < 0) continue;
-        ncclConfig_t c2 = nonblocking_config();
+        // config NULL: the child inherits the parent's (non-blocking) configuration
         ncclComm_t sub = nullptr;
-        check(N.split(world, colors[d], rank, &sub, &c2), "ncclCommSplit");
+        check(N.split(world, colors[d], rank, &sub, nullptr), "ncclCommSplit");
         s->dims[d] = sub;
         if (sub) wait_ready(sub, "ncclCommSplit");
     }
