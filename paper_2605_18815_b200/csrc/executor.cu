@@ -1309,7 +1309,9 @@ int Executor::run(cudaStream_t stream) {
     // (captured per prepare and stream; RS_GRAPH=0 disables)
     // the first run after a prepare goes direct (a one-shot reconfiguration would pay the
     // capture for nothing); repeated runs capture once and replay
-    if (auto_graph_ && runs_since_prepare_++ > 0) return run_graph(stream);
+    // (the legacy default stream cannot be captured: it always runs direct)
+    const bool capturable = stream != nullptr && stream != cudaStreamLegacy && stream != cudaStreamPerThread;
+    if (auto_graph_ && capturable && runs_since_prepare_++ > 0) return run_graph(stream);
     return run_direct(stream);
 }
 

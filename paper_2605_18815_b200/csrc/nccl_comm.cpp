@@ -140,11 +140,14 @@ const CommSet& CommCache::get_or_create(const std::string& key, const std::uint8
     t0 = std::chrono::steady_clock::now();
     for (int d = 0; d < kCommDims; ++d) {
         if (!colors || colors[d] < 0) continue;
-        // config NULL: the child inherits the parent's (non-blocking) configuration
+        // config NULL: the child inherits the parent's (non-blocking) configuration. The
+        // split is an operation on the parent too: both must be ready before the next one
         ncclComm_t sub = nullptr;
+        wait_ready(world, "ncclCommSplit (parent)");
         check(N.split(world, colors[d], rank, &sub, nullptr), "ncclCommSplit");
         s->dims[d] = sub;
         if (sub) wait_ready(sub, "ncclCommSplit");
+        wait_ready(world, "ncclCommSplit (parent)");
     }
     s->split_s = since(t0);
     std::lock_guard<std::mutex> lk(mu_);
