@@ -142,12 +142,15 @@ const CommSet& CommCache::get_or_create(const std::string& key, const std::uint8
         if (!colors || colors[d] < 0) continue;
         // config NULL: the child inherits the parent's (non-blocking) configuration. The
         // split is an operation on the parent too: both must be ready before the next one
-        ncclComm_t sub = nullptr;
+        // A non-blocking split may publish the child handle only when it completes, so
+        // its destination is the heap-resident CommSet slot, read after the parent is ready
         wait_ready(world, "ncclCommSplit (parent)");
-        check(N.split(world, colors[d], rank, &sub, nullptr), "ncclCommSplit");
-        s->dims[d] = sub;
-        if (sub) wait_ready(sub, "ncclCommSplit");
+        check(N.split(world, colors[d], rank, reinterpret_cast<ncclComm_t*>(&s->dims[d]), nullptr), "ncclCommSplit");
         wait_ready(world, "ncclCommSplit (parent)");
+        void* volatile* slot = &s->dims[d];  // written by NCCL's async thread
+        for (int spin = 0; !*slot && spin < 100000; ++spin) std::this_thread::sleep_for(std::chrono::microseconds(100));
+        if (!s->dims[d]) throw exec::CudaError("ncclCommSplit: no communicator returned");
+        wait_ready(static_cast<ncclComm_t>(s->dims[d]), "ncclCommSplit");
     }
     s->split_s = since(t0);
     std::lock_guard<std::mutex> lk(mu_);
