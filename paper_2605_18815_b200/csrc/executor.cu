@@ -694,6 +694,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     // 1) cut the recorded copies into tiles on host threads: contiguous slices of the
     //    record list, one bucket set per thread, concatenated in slice order (the same
     //    tile order a single thread produces)
+    const auto t_fin0 = std::chrono::steady_clock::now();
     const size_t nrec = pending.size();
     const size_t hw = std::max(1u, std::thread::hardware_concurrency());
     const size_t nt = std::max<size_t>(1, std::min<size_t>({hw, 16, nrec / 256 + 1}));
@@ -710,6 +711,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         for (auto& x : th) x.join();
     }
     pending.clear();
+    const auto t_cut = std::chrono::steady_clock::now();
     size_t nb = 0;
     for (const auto& v : tb) nb = std::max(nb, v.size());
     // 2) one group per non-empty bucket (key * 5 + class, ascending)
@@ -774,6 +776,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         }
     }
     for (auto& x : th) x.join();
+    const auto t_asm = std::chrono::steady_clock::now();
     if (total) {
         // two descriptor buffers used in turn: a re-prepare uploads into the one the last
         // launch did not read, so it may overlap kernels of the previous prepare still in
@@ -799,6 +802,13 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         RS_CUDA(cudaStreamSynchronize(upload));
     }
     ntiles = total;
+    if (std::getenv("RS_TIMING") && total > 4096) {
+        const auto t_up = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[reshard] finalize: cut %.2f ms (%zu threads), assemble %.2f ms, upload %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(t_cut - t_fin0).count(), nt,
+                     std::chrono::duration<double, std::milli>(t_asm - t_cut).count(),
+                     std::chrono::duration<double, std::milli>(t_up - t_asm).count());
+    }
     if (stats) {
         stats->tiles += static_cast<std::int64_t>(total);
         stats->launches += static_cast<std::int64_t>(groups.size());

@@ -2,6 +2,7 @@
 // retained regions, scalar broadcast) as 2-D strided byte copies between the
 // physical buffers of DESIGN.md §3. Pure host code; GPU-independent.
 #include <algorithm>
+#include <thread>
 
 #include "reshard/executor.hpp"
 
@@ -145,9 +146,30 @@ std::vector<CopyOp> build_ops(const PlanCore& P) {
     auto overridden = [&](int j, int t) {
         return !P.d2_tensor_dst.empty() && P.d2_tensor_dst[static_cast<size_t>(j) * nt + t];
     };
-    for (const stair::Triple& T : P.triples)
-        if (!overridden(T.dst, T.tensor)) E.triple(T);
-    for (const stair::Triple& T : P.retain_triples) E.triple(T);
+    {
+        // the ZeRO triples (thousands, each a band sweep) on host threads: contiguous
+        // slices into their own op lists, appended in slice order (the sequential order)
+        std::vector<const stair::Triple*> tv;
+        tv.reserve(P.triples.size() + P.retain_triples.size());
+        for (const stair::Triple& T : P.triples)
+            if (!overridden(T.dst, T.tensor)) tv.push_back(&T);
+        for (const stair::Triple& T : P.retain_triples) tv.push_back(&T);
+        const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+        const size_t nth = std::max<size_t>(1, std::min<size_t>({hw, 16, tv.size() / 64 + 1}));
+        std::vector<std::vector<CopyOp>> part(nth);
+        auto work = [&](size_t t) {
+            Emitter Et{P, part[t]};
+            for (size_t i = tv.size() * t / nth; i < tv.size() * (t + 1) / nth; ++i) Et.triple(*tv[i]);
+        };
+        std::vector<std::thread> th;
+        for (size_t t = 1; t < nth; ++t) th.emplace_back(work, t);
+        work(0);
+        for (auto& x : th) x.join();
+        size_t n = ops.size();
+        for (const auto& v : part) n += v.size();
+        ops.reserve(n);
+        for (auto& v : part) ops.insert(ops.end(), v.begin(), v.end());
+    }
     // D2 extension: a tensor of a destination rank holding multi-candidate elements is
     // re-derived from its triples' runs minus the segments another source was chosen for
     // (d2_multi, (dst, lo) order); every other element has exactly one source
