@@ -69,7 +69,9 @@ def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False):
     ex = tr.ex
     seed = 0x5EED5
     ex.fill(A.SIDE_SRC, seed)
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: transitions under 1 GiB per GPU replay from a CUDA graph from
+    # their second run on, and the legacy default stream cannot be captured
+    stream = torch.cuda.Stream()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
