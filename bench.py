@@ -429,13 +429,15 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": local_rw}
             # DRAM read + write of the same forward transition from the committed ncu capture
             # (one launch per concurrency group, summed like `achieved`)
-            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic_n1_L32.json")
-            if args.layers == 32 and os.path.exists(tp):
+            prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+            tp = next((os.path.join(prof, f) for f in ("r02_traffic_n1_L32.json", "r01_traffic_n1_L32.json")
+                       if os.path.exists(os.path.join(prof, f))), "")
+            if args.layers == 32 and tp:
                 with open(tp) as f:
                     cap = json.load(f)
                 if cap.get("algorithmic_bytes_forward") == local_rw:
                     roof["traffic"] = cap["forward"]["traffic"]
-                    roof["traffic_source"] = "profiles/r01_traffic_n1_L32.json (ncu dram__bytes_read.sum + write.sum)"
+                    roof["traffic_source"] = f"profiles/{os.path.basename(tp)} (ncu dram__bytes_read.sum + write.sum)"
         else:
             # T_roof = max_g max(out_g / NVLink, in_g / NVLink, HBM_g / B_HBM); the
             # binding GPU's NVLink bytes over the measured (max over ranks) transition time
