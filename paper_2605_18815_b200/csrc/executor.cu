@@ -654,38 +654,44 @@ namespace {
 // HBM) progresses in proportion to its bytes: CTAs walk the tile list front to back, so
 // in op order (sorted by destination rank) all senders would converge on the same
 // receivers at the same time and leave other links idle.
-void interleave_lanes(std::vector<Tile>* v, const std::vector<std::uint8_t>& lane) {
+/// Lane interleave straight into `out`: the tiles arrive as spans (a bucket's per-thread
+/// pieces, in order) with their lanes; each step emits the next tile of the lane whose
+/// progress fraction after that tile is smallest (lowest lane on ties). Lanes are few
+/// (peers + local + pull sources), so a scan beats a heap.
+void interleave_into(Tile* out, const std::vector<std::pair<const Tile*, const std::uint8_t*>>& spans,
+                     const std::vector<size_t>& lens) {
     int nl = 0;
-    for (std::uint8_t l : lane) nl = std::max(nl, l + 1);
-    if (nl < 2) return;
-    std::vector<std::vector<std::uint32_t>> q(static_cast<size_t>(nl));
+    size_t n = 0;
+    for (size_t k = 0; k < spans.size(); ++k) {
+        for (size_t i = 0; i < lens[k]; ++i) nl = std::max(nl, spans[k].second[i] + 1);
+        n += lens[k];
+    }
+    std::vector<std::vector<const Tile*>> q(static_cast<size_t>(nl));
     std::vector<double> total(static_cast<size_t>(nl), 0.0), done(static_cast<size_t>(nl), 0.0);
-    auto bytes = [&](const Tile& t) { return static_cast<double>(t.rows) * t.row_bytes; };
-    for (size_t i = 0; i < v->size(); ++i) {
-        q[lane[i]].push_back(static_cast<std::uint32_t>(i));
-        total[lane[i]] += bytes((*v)[i]);
-    }
-    std::vector<size_t> head(static_cast<size_t>(nl), 0);
-    std::vector<Tile> out;
-    out.reserve(v->size());
-    using Item = std::pair<double, int>;  // (progress fraction after the lane's next tile, lane)
-    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> pq;
-    auto push = [&](int l) {
-        if (head[static_cast<size_t>(l)] < q[static_cast<size_t>(l)].size()) {
-            const Tile& t = (*v)[q[static_cast<size_t>(l)][head[static_cast<size_t>(l)]]];
-            pq.push({(done[static_cast<size_t>(l)] + 0.5 * bytes(t)) / total[static_cast<size_t>(l)], l});
+    auto bytes = [](const Tile& t) { return static_cast<double>(t.rows) * t.row_bytes; };
+    for (size_t k = 0; k < spans.size(); ++k)
+        for (size_t i = 0; i < lens[k]; ++i) {
+            const std::uint8_t l = spans[k].second[i];
+            q[l].push_back(spans[k].first + i);
+            total[l] += bytes(spans[k].first[i]);
         }
+    std::vector<size_t> head(static_cast<size_t>(nl), 0);
+    std::vector<double> key(static_cast<size_t>(nl), 0.0);
+    auto refresh = [&](int l) {
+        const size_t L = static_cast<size_t>(l);
+        key[L] = head[L] < q[L].size() ? (done[L] + 0.5 * bytes(*q[L][head[L]])) / total[L] : 1e300;
     };
-    for (int l = 0; l < nl; ++l) push(l);
-    while (!pq.empty()) {
-        const int l = pq.top().second;
-        pq.pop();
-        const Tile& t = (*v)[q[static_cast<size_t>(l)][head[static_cast<size_t>(l)]++]];
-        done[static_cast<size_t>(l)] += bytes(t);
-        out.push_back(t);
-        push(l);
+    for (int l = 0; l < nl; ++l) refresh(l);
+    for (size_t o = 0; o < n; ++o) {
+        int best = 0;
+        for (int l = 1; l < nl; ++l)
+            if (key[static_cast<size_t>(l)] < key[static_cast<size_t>(best)]) best = l;
+        const size_t B = static_cast<size_t>(best);
+        const Tile& t = *q[B][head[B]++];
+        done[B] += bytes(t);
+        out[o] = t;
+        refresh(best);
     }
-    v->swap(out);
 }
 
 }  // namespace
@@ -753,17 +759,15 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         }
         if (!n) continue;
         if (interleave && multi_lane) {
-            std::vector<Tile> v;
-            std::vector<std::uint8_t> l;
-            v.reserve(n);
-            l.reserve(n);
+            std::vector<std::pair<const Tile*, const std::uint8_t*>> spans;
+            std::vector<size_t> lens;
             for (size_t t = 0; t < nt; ++t) {
-                if (b >= tb[t].size()) continue;
-                v.insert(v.end(), tb[t][b].begin(), tb[t][b].end());
-                l.insert(l.end(), tl[t][b].begin(), tl[t][b].end());
+                if (b >= tb[t].size() || tb[t][b].empty()) continue;
+                spans.push_back({tb[t][b].data(), tl[t][b].data()});
+                lens.push_back(tb[t][b].size());
             }
-            interleave_lanes(&v, l);
-            std::memcpy(out + begin[b], v.data(), n * sizeof(Tile));
+            Tile* dst = out + begin[b];
+            th.emplace_back([dst, spans = std::move(spans), lens = std::move(lens)] { interleave_into(dst, spans, lens); });
             continue;
         }
         size_t at = begin[b];
