@@ -526,7 +526,8 @@ def run_ours(args):
                             "descriptor build and upload + the transition + 8-byte result readback"},
             "clocks": clk.summary(),
         }
-        out["gpu_launches"] = (st_f.launches + bwd.ex.stats().launches) * args.steps
+        # copy launches of both transitions per step, plus the two device barriers at N>1
+        out["gpu_launches"] = (st_f.launches + bwd.ex.stats().launches + (2 if world > 1 else 0)) * args.steps
         if arena is not None:
             a = arena.stats()
             out["memory"] = {"physical_gb": round(a.physical_bytes / 1e9, 2), "old_layout_gb": round(a.a_bytes / 1e9, 2),
