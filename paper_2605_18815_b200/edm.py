@@ -133,10 +133,15 @@ class ElasticDeviceManager:
         self._torch_cost_s = 0.0
         self.init_s = 0.0
 
-    def __del__(self):
+    def close(self) -> None:
+        """Join the side thread and destroy the cached NCCL communicators now (before the
+        process group and the CUDA context go away)."""
         if getattr(self, "h", None) and A is not None and A._lib is not None:
             A.lib().rs_edm_destroy(self.h)
             self.h = None
+
+    def __del__(self):
+        self.close()
 
     @staticmethod
     def _key(cfg: Cfg) -> Tuple:

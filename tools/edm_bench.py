@@ -245,6 +245,8 @@ def main():
                           "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast, "dedup": args.dedup, "dedup_early": args.dedup_early,
                           "results": results}), flush=True)
     dist.barrier()
+    edm.close()  # the new worlds' NCCL communicators before the process group
+    dist.barrier()
     dist.destroy_process_group()
 
 
