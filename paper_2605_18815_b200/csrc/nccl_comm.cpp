@@ -80,6 +80,20 @@ ncclConfig_t nonblocking_config() {
     return cfg;
 }
 
+/// non-blocking communicators: finalize (flush), wait, then destroy
+void destroy_comm(void* c) {
+    if (!c) return;
+    const Nccl& N = Nccl::get();
+    ncclComm_t comm = static_cast<ncclComm_t>(c);
+    if (N.finalize(comm) == ncclInProgress) {
+        try {
+            wait_ready(comm, "ncclCommFinalize");
+        } catch (...) {
+        }
+    }
+    N.destroy(comm);
+}
+
 double since(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -104,9 +118,9 @@ CommCache::~CommCache() {
     for (auto& kv : cache_) {
         CommSet& s = *kv.second;
         cudaSetDevice(s.device);
-        for (void*& c : s.dims)
-            if (c) Nccl::get().destroy(static_cast<ncclComm_t>(c)), c = nullptr;
-        if (s.world) Nccl::get().destroy(static_cast<ncclComm_t>(s.world)), s.world = nullptr;
+        for (void*& c : s.dims) destroy_comm(c), c = nullptr;
+        destroy_comm(s.world);
+        s.world = nullptr;
     }
 }
 
@@ -199,9 +213,8 @@ void CommCache::destroy(const std::string& key) {
         cache_.erase(it);
     }
     cudaSetDevice(s->device);
-    for (void* c : s->dims)
-        if (c) Nccl::get().destroy(static_cast<ncclComm_t>(c));
-    if (s->world) Nccl::get().destroy(static_cast<ncclComm_t>(s->world));
+    for (void* c : s->dims) destroy_comm(c);
+    destroy_comm(s->world);
 }
 
 }  // namespace edm
