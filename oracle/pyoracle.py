@@ -175,7 +175,8 @@ class OState:
     def buffer(self, rank: int, buf: int) -> bytes:
         n = C.c_int64()
         p = lib().or_state_buffer(self.h, rank, buf, C.byref(n))
-        return C.string_at(p, n.value) if n.value else b""
+        # ctypes.string_at takes a C int size: buffers past 2 GiB go through an array view
+        return (C.c_char * n.value).from_address(p).raw if n.value else b""
 
     def buffer_ptr(self, rank: int, buf: int):
         n = C.c_int64()

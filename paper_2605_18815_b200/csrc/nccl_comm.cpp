@@ -77,6 +77,7 @@ void wait_ready(ncclComm_t c, const char* what) {
 ncclConfig_t nonblocking_config() {
     ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
     cfg.blocking = 0;
+    cfg.splitShare = 1;  // the per-dimension splits share the world communicator's resources
     return cfg;
 }
 

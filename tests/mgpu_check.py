@@ -115,7 +115,11 @@ def main():
         dist.barrier()
         bad_b = fwd.ex.verify(A.SIDE_DST, seed)[0]
         ora = 0
-        if check_oracle and mine:
+        # the oracle holds every rank's old and new state in host memory, in every rank
+        # process: only scenarios whose state is small (a few GB) are compared byte for byte
+        small = 2 * (ab.bytes_moved() + ab.bytes_retained()) < 8e9
+        oracle_now = check_oracle and mine and small
+        if oracle_now:
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
             import pyoracle as O
             osc = O.OScenario(sc.text())
@@ -130,13 +134,13 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
         bad_a = bwd.ex.verify(A.SIDE_DST, seed)[0]
-        if check_oracle and mine:
+        if oracle_now:
             for (side, r, b), t in mine.items():
                 if side == A.SIDE_SRC and t.cpu().numpy().tobytes() != osrc.buffer(r, b):
                     ora += 1
             bad_b += ora
         st = fwd.ex.stats()
-        print(f"[rank {rank}] {'oracle-checked ' if check_oracle and mine else ''}{'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''}{'(early)' if early else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
+        print(f"[rank {rank}] {'oracle-checked ' if oracle_now else ''}{'staged' if staged else 'vmm' if vmm else 'fused'}{'+dedup' if dedup else ''}{'(early)' if early else ''} {sc.name}: dst mismatches {bad_b}, round-trip mismatches {bad_a}, "
               f"local {st.local_bytes/1e9:.2f} GB, remote {st.remote_bytes/1e9:.2f} GB", flush=True)
         failures += int(bad_a != 0) + int(bad_b != 0)
         del fwd, bwd, keep
