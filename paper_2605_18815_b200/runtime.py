@@ -133,14 +133,20 @@ class StagedTransition:
     def _exchange(self, chans, stream, per_op=False):
         import torch
         import torch.distributed as dist
+        # gloo (ranks sharing one GPU) moves host tensors only: the packed channel
+        # buffers bounce through host memory there; NCCL sends them from HBM
+        host = dist.get_backend(self.group) == "gloo"
         sends, recvs = [], []
         for src, dst, gs, gd, nbytes, _ in chans:
             if gs == self.gpu:
                 buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
                 self.ex.pack(src, dst, buf.data_ptr(), stream)
+                if host:
+                    torch.cuda.synchronize()
+                    buf = buf.cpu()
                 sends.append((buf, gd, src, dst))
             elif gd == self.gpu:
-                recvs.append((torch.empty(nbytes, dtype=torch.uint8, device="cuda"), gs, src, dst))
+                recvs.append((torch.empty(nbytes, dtype=torch.uint8, device="cpu" if host else "cuda"), gs, src, dst))
         if per_op:  # naive: one blocking message per op, in the global channel order
             for src, dst, gs, gd, nbytes, _ in chans:
                 if self.gpu not in (gs, gd):
@@ -162,7 +168,12 @@ class StagedTransition:
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
         for buf, _, src, dst in recvs:
+            if host:
+                buf = buf.to("cuda")
+                torch.cuda.synchronize()
             self.ex.unpack(src, dst, buf.data_ptr(), stream)
+            if host:
+                torch.cuda.synchronize()  # the bounce buffer must outlive the unpack
 
     def run(self, stream: int = 0) -> None:
         self.ex.run(stream)  # same-GPU moves, fused

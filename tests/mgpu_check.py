@@ -84,8 +84,9 @@ def main():
             fwd_run, bwd_run = fwd.run, bwd.run
         elif staged:
             from paper_2605_18815_b200.runtime import StagedTransition
-            fwd_run = StagedTransition(ab, fwd.ex, world, rank).run
-            bwd_run = StagedTransition(ba, bwd.ex, world, rank).run
+            mode = sys.argv[sys.argv.index("--mode") + 1] if "--mode" in sys.argv else "async"
+            fwd_run = StagedTransition(ab, fwd.ex, world, rank, mode=mode).run
+            bwd_run = StagedTransition(ba, bwd.ex, world, rank, mode=mode).run
         else:
             fwd.connect()
             bwd.connect()

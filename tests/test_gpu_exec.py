@@ -506,3 +506,21 @@ def test_promoted_scatter_gather_executed():
                         os.path.join(root, "tests", "mgpu_collectives_check.py"), "4"],
                        capture_output=True, text=True, timeout=600)
     assert "COLL_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("mode", ["async", "naive"])
+def test_staged_schedule_transport(mode):
+    """Algorithm 1's buffered execution driven by the transition schedule (memory-aware
+    stages of XOR steps, per-peer packed channels): NCCL send/recv between GPUs, or on a
+    one-GPU box gloo between rank processes sharing the device; every scenario's round
+    trip bit-exact (tests/mgpu_check.py --staged)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = "29551" if mode == "async" else "29553"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
+                        "--master-addr", "127.0.0.1", "--master-port", port,
+                        os.path.join(root, "tests", "mgpu_check.py"), "1", "--random", "6", "--staged", "--mode", mode,
+                        "--oracle"],
+                       capture_output=True, text=True, timeout=900)
+    assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
