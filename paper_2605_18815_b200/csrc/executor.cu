@@ -584,25 +584,23 @@ void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t ro
     pending.push_back(Pending{src, dst, rows, rb, sp, dp, kTile, key, lane});
 }
 
-void TileSet::expand(const Pending& q, std::vector<std::vector<Tile>>& bk, std::vector<std::vector<std::uint8_t>>& ln) {
+namespace {
+
+/// Cut one recorded copy into tiles: emit(bucket = key * 5 + alignment class, tile, lane)
+template <class Emit>
+void cut_tiles(const TileSet::Pending& q, Emit&& emit_to) {
     std::int64_t rows = q.rows, rb = q.rb;
     const std::int64_t sp = q.sp, dp = q.dp, kTile = q.kTile;
     if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
         rb *= rows;
         rows = 1;
     }
-    if (static_cast<int>(bk.size()) < (q.key + 1) * 5) {
-        bk.resize(static_cast<size_t>(q.key + 1) * 5);
-        ln.resize(bk.size());
-    }
     auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
-        Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
-               static_cast<std::uint32_t>(nb)};
+        const Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
+                     static_cast<std::uint32_t>(nb)};
         std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
         if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-        const size_t b = static_cast<size_t>(q.key) * 5 + class_index(align_class(a));
-        bk[b].push_back(t);
-        ln[b].push_back(static_cast<std::uint8_t>(q.lane));
+        emit_to(static_cast<size_t>(q.key) * 5 + class_index(align_class(a)), t);
     };
     if (rows == 1 || rb >= kTile) {
         for (std::int64_t r = 0; r < rows; ++r) {
@@ -635,6 +633,8 @@ void TileSet::expand(const Pending& q, std::vector<std::vector<Tile>>& bk, std::
         }
     }
 }
+
+}  // namespace
 
 void PinnedBuf::grow(size_t bytes) {
     if (ptr) cudaFreeHost(ptr);
@@ -697,109 +697,124 @@ void interleave_into(Tile* out, const std::vector<std::pair<const Tile*, const s
 }  // namespace
 
 void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging) {
-    // 1) cut the recorded copies into tiles on host threads: contiguous slices of the
-    //    record list, one bucket set per thread, concatenated in slice order (the same
-    //    tile order a single thread produces)
+    // Cut the recorded copies into tiles on host threads, straight into their final
+    // places in the pinned staging buffer: pass 1 counts each thread's tiles per bucket
+    // (key * 5 + alignment class), a prefix over (bucket, thread) fixes every thread's
+    // write offsets, pass 2 writes. Contiguous record slices per thread, so the order is
+    // the single-thread order. Buckets with several destination lanes are written to a
+    // side array and interleaved into place.
     const auto t_fin0 = std::chrono::steady_clock::now();
     const size_t nrec = pending.size();
     const size_t hw = std::max(1u, std::thread::hardware_concurrency());
     const size_t nt = std::max<size_t>(1, std::min<size_t>({hw, 16, nrec / 256 + 1}));
-    std::vector<std::vector<std::vector<Tile>>> tb(nt);
-    std::vector<std::vector<std::vector<std::uint8_t>>> tl(nt);
-    {
-        auto work = [&](size_t t) {
-            const size_t lo = nrec * t / nt, hi = nrec * (t + 1) / nt;
-            for (size_t i = lo; i < hi; ++i) expand(pending[i], tb[t], tl[t]);
-        };
+    int max_key = -1;
+    for (const Pending& q : pending) max_key = std::max(max_key, q.key);
+    const size_t nb = static_cast<size_t>(max_key + 1) * 5;
+    std::vector<std::vector<size_t>> cnt(nt, std::vector<size_t>(nb, 0));
+    std::vector<std::vector<std::uint8_t>> lane_mask(nt, std::vector<std::uint8_t>(nb, 0));  // bit 0: seen, bit 1: several lanes
+    std::vector<std::vector<std::uint8_t>> lane0(nt, std::vector<std::uint8_t>(nb, 0));
+    auto parallel = [&](auto&& fn) {
         std::vector<std::thread> th;
-        for (size_t t = 1; t < nt; ++t) th.emplace_back(work, t);
-        work(0);
+        for (size_t t = 1; t < nt; ++t) th.emplace_back(fn, t);
+        fn(0);
         for (auto& x : th) x.join();
-    }
-    pending.clear();
+    };
+    parallel([&](size_t t) {
+        for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
+            const Pending& q = pending[i];
+            cut_tiles(q, [&](size_t b, const Tile&) {
+                ++cnt[t][b];
+                if (!(lane_mask[t][b] & 1)) lane_mask[t][b] = 1, lane0[t][b] = static_cast<std::uint8_t>(q.lane);
+                else if (lane0[t][b] != q.lane) lane_mask[t][b] |= 2;
+            });
+        }
+    });
     const auto t_cut = std::chrono::steady_clock::now();
-    size_t nb = 0;
-    for (const auto& v : tb) nb = std::max(nb, v.size());
-    // 2) one group per non-empty bucket (key * 5 + class, ascending)
-    host.clear();
     groups.clear();
-    std::vector<size_t> begin(nb, 0);
+    std::vector<size_t> begin(nb, 0), bucket_n(nb, 0);
+    std::vector<char> multi(nb, 0);
     size_t total = 0;
     for (size_t b = 0; b < nb; ++b) {
         size_t n = 0;
-        for (size_t t = 0; t < nt; ++t) n += b < tb[t].size() ? tb[t][b].size() : 0;
+        int l0 = -1;
+        for (size_t t = 0; t < nt; ++t) {
+            n += cnt[t][b];
+            if (!(lane_mask[t][b] & 1)) continue;
+            if (lane_mask[t][b] & 2) multi[b] = 1;
+            if (l0 < 0) l0 = lane0[t][b];
+            else if (l0 != lane0[t][b]) multi[b] = 1;
+        }
+        if (!interleave) multi[b] = 0;
         begin[b] = total;
+        bucket_n[b] = n;
         if (!n) continue;
         const int c = static_cast<int>(b % 5);
         groups.push_back({c, static_cast<int>(total), static_cast<int>(n), static_cast<int>(b / 5)});
         if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(n);
         total += n;
     }
-    // 3) assemble straight into the pinned staging buffer (threads per bucket slice);
-    //    buckets with several destination lanes are interleaved first
     Tile* out = nullptr;
     if (total) {
         if (!staging) throw std::logic_error("TileSet::finalize needs a staging buffer");
         if (staging->size() < total * sizeof(Tile)) staging->grow(total * sizeof(Tile) * 5 / 4);
         out = static_cast<Tile*>(staging->ptr);
     }
-    std::vector<std::thread> th;
+    // side arrays of the multi-lane buckets (tiles + lanes, interleaved afterwards)
+    std::vector<std::vector<Tile>> side_t(nb);
+    std::vector<std::vector<std::uint8_t>> side_l(nb);
+    for (size_t b = 0; b < nb; ++b)
+        if (multi[b]) side_t[b].resize(bucket_n[b]), side_l[b].resize(bucket_n[b]);
+    // per (thread, bucket) write cursor: the bucket's start + the earlier threads' counts
+    std::vector<std::vector<size_t>> cur(nt, std::vector<size_t>(nb, 0));
     for (size_t b = 0; b < nb; ++b) {
-        size_t n = 0, lanes_seen = 0;
-        std::uint8_t lane0 = 0;
-        bool multi_lane = false;
-        for (size_t t = 0; t < nt; ++t) {
-            if (b >= tb[t].size()) continue;
-            n += tb[t][b].size();
-            if (interleave)
-                for (std::uint8_t l : tl[t][b]) {
-                    if (lanes_seen++ == 0) lane0 = l;
-                    else if (l != lane0) multi_lane = true;
-                }
-        }
-        if (!n) continue;
-        if (interleave && multi_lane) {
-            std::vector<std::pair<const Tile*, const std::uint8_t*>> spans;
-            std::vector<size_t> lens;
-            for (size_t t = 0; t < nt; ++t) {
-                if (b >= tb[t].size() || tb[t][b].empty()) continue;
-                spans.push_back({tb[t][b].data(), tl[t][b].data()});
-                lens.push_back(tb[t][b].size());
-            }
-            Tile* dst = out + begin[b];
-            th.emplace_back([dst, spans = std::move(spans), lens = std::move(lens)] { interleave_into(dst, spans, lens); });
-            continue;
-        }
-        size_t at = begin[b];
-        for (size_t t = 0; t < nt; ++t) {
-            if (b >= tb[t].size() || tb[t][b].empty()) continue;
-            const Tile* src = tb[t][b].data();
-            const size_t cnt = tb[t][b].size();
-            th.emplace_back([=] { std::memcpy(out + at, src, cnt * sizeof(Tile)); });
-            at += cnt;
-        }
+        size_t at = multi[b] ? 0 : begin[b];
+        for (size_t t = 0; t < nt; ++t) cur[t][b] = at, at += cnt[t][b];
     }
-    for (auto& x : th) x.join();
+    parallel([&](size_t t) {
+        std::vector<size_t>& c = cur[t];
+        for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
+            const Pending& q = pending[i];
+            cut_tiles(q, [&](size_t b, const Tile& tile) {
+                if (multi[b]) {
+                    side_l[b][c[b]] = static_cast<std::uint8_t>(q.lane);
+                    side_t[b][c[b]++] = tile;
+                } else {
+                    out[c[b]++] = tile;
+                }
+            });
+        }
+    });
+    {
+        std::vector<std::thread> th;
+        for (size_t b = 0; b < nb; ++b)
+            if (multi[b] && bucket_n[b])
+                th.emplace_back([&, b] {
+                    const std::vector<std::pair<const Tile*, const std::uint8_t*>> spans{{side_t[b].data(), side_l[b].data()}};
+                    interleave_into(out + begin[b], spans, {bucket_n[b]});
+                });
+        for (auto& x : th) x.join();
+    }
+    pending.clear();
     const auto t_asm = std::chrono::steady_clock::now();
     if (total) {
         // two descriptor buffers used in turn: a re-prepare uploads into the one the last
         // launch did not read, so it may overlap kernels of the previous prepare still in
         // flight. Both are kept across re-prepares: with peer access enabled every
         // cudaMalloc/cudaFree also edits the peers' mappings (measured: 0.6 s stalls)
-        cur ^= 1;
+        cur_buf_flip();
+        if (total * sizeof(Tile) > dev_bytes[this->cur]) {
+            if (dev_buf[this->cur]) cudaFree(dev_buf[this->cur]);
+            dev_buf[this->cur] = nullptr;
+            dev_bytes[this->cur] = total * sizeof(Tile) * 5 / 4;
+            RS_CUDA(cudaMalloc(&dev_buf[this->cur], dev_bytes[this->cur]));
+        }
         // the upload into dev_buf[cur] waits for every launch that read it
-        for (cudaEvent_t e : fences[cur]) {
+        for (cudaEvent_t e : fences[this->cur]) {
             RS_CUDA(cudaStreamWaitEvent(upload, e, 0));
             fence_pool.push_back(e);
         }
-        fences[cur].clear();
-        if (total * sizeof(Tile) > dev_bytes[cur]) {
-            if (dev_buf[cur]) cudaFree(dev_buf[cur]);
-            dev_buf[cur] = nullptr;
-            dev_bytes[cur] = total * sizeof(Tile) * 5 / 4;
-            RS_CUDA(cudaMalloc(&dev_buf[cur], dev_bytes[cur]));
-        }
-        dev = dev_buf[cur];
+        fences[this->cur].clear();
+        dev = dev_buf[this->cur];
         // private non-blocking stream: descriptor uploads never serialize with the
         // caller's (training) streams, so the EDM can prepare in the background
         RS_CUDA(cudaMemcpyAsync(dev, out, total * sizeof(Tile), cudaMemcpyHostToDevice, upload));
@@ -808,7 +823,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     ntiles = total;
     if (std::getenv("RS_TIMING") && total > 4096) {
         const auto t_up = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[reshard] finalize: cut %.2f ms (%zu threads), assemble %.2f ms, upload %.2f ms\n",
+        std::fprintf(stderr, "[reshard] finalize: count %.2f ms (%zu threads), write %.2f ms, upload %.2f ms\n",
                      std::chrono::duration<double, std::milli>(t_cut - t_fin0).count(), nt,
                      std::chrono::duration<double, std::milli>(t_asm - t_cut).count(),
                      std::chrono::duration<double, std::milli>(t_up - t_asm).count());

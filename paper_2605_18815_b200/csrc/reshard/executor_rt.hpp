@@ -102,9 +102,7 @@ struct TileSet {
     void add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
              std::int64_t dp, std::int64_t kTile, int lane = 0);
     void finalize(ExecStats* stats, cudaStream_t upload, struct PinnedBuf* staging);
-    /// tiles of one recorded copy into per-bucket vectors (key * 5 + alignment class)
-    static void expand(const Pending& q, std::vector<std::vector<Tile>>& buckets,
-                       std::vector<std::vector<std::uint8_t>>& lanes);
+    void cur_buf_flip() { cur ^= 1; }
     /// launch groups in key order; key_mod > 0 restricts to keys with key % key_mod == key_rem
     int launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbase, int sms, int ctas_per_sm, bool bulk,
                int key_mod = 0, int key_rem = 0) const;
