@@ -316,6 +316,11 @@ int rs_arena_stage_order(const rs_arena_t* a, int dir, int* out, int cap, int* n
  * share one stage and run concurrently); position 0 is always 1 */
 int rs_arena_stage_cuts(const rs_arena_t* a, int dir, int* out, int cap, int* n);
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out);
+/* FreeObsoleteBuffers at run time (one-way arenas on one GPU): once
+ * stage `stage` of the transition has completed, unmap every old-layout chunk last read in
+ * a stage <= `stage` and return the physical chunks the new layout does not reuse to the
+ * driver (cuMemUnmap + cuMemRelease). *freed: bytes released by this call. */
+int rs_arena_release_through(rs_arena_t* a, int stage, int64_t* freed);
 /* host-only memory plan (no GPU): stats and the execution-simulation check
  * (violations == 0 means every read sees its own data) */
 /* fewest concurrency groups of the stage order whose memory plan for `gpu` fits

@@ -373,6 +373,14 @@ class Arena:
         A.check(A.lib().rs_arena_stage_cuts(self.h, direction, out, 65536, C.byref(n)))
         return list(out[: n.value])
 
+    def release_through(self, stage: int) -> int:
+        """FreeObsoleteBuffers at run time (one-way arenas on one GPU): after stage `stage`
+        has completed, unmap the old-layout chunks it made dead and release the physical
+        memory the new layout does not reuse. Returns the bytes released."""
+        n = C.c_int64()
+        A.check(A.lib().rs_arena_release_through(self.h, stage, C.byref(n)))
+        return n.value
+
     def stats(self) -> A.ArenaStats_t:
         s = A.ArenaStats_t()
         A.check(A.lib().rs_arena_stats(self.h, C.byref(s)))

@@ -120,6 +120,16 @@ Arena::Arena(const core::PlanCore& ab, const core::PlanCore* ba, const ArenaConf
                                       static_cast<long long>(v), gpu));
     bands_ = mp.bands;
     const bool shareable = n_gpus > 1;
+    one_way_ = ba == nullptr && n_gpus == 1;
+    if (one_way_) {
+        a_last_stage_ = last_read_stage(mp, ab, exec::build_ops(ab));
+        a_unmapped_.resize(mp.bufs[0].size());
+        for (size_t i = 0; i < mp.bufs[0].size(); ++i) a_unmapped_[i].assign(mp.bufs[0][i].phys.size(), 0);
+        b_uses_.assign(static_cast<size_t>(mp.nphys), 0);
+        for (const BufPlan& m : mp.bufs[1])
+            for (int p : m.phys)
+                if (p >= 0) b_uses_[static_cast<size_t>(p)] = 1;
+    }
     order_[0] = mp.order[0];
     order_[1] = mp.order[1];
     cut_[0] = mp.cut[0];
@@ -272,6 +282,31 @@ void Arena::import_peer(const std::vector<int>& fds, const std::vector<std::uint
     }
 }
 
+std::int64_t Arena::release_through(int stage) {
+    if (!one_way_) throw ConfigError("arena release: only one-way arenas on one GPU release old-layout chunks");
+    const Drv& D = Drv::get();
+    if (cudaSetDevice(cfg_.device) != cudaSuccess) throw exec::CudaError("cudaSetDevice failed");
+    const std::int64_t C = cfg_.chunk_bytes;
+    std::int64_t freed = 0;
+    for (size_t i = 0; i < bufs_[0].size(); ++i) {
+        BufMap& m = bufs_[0][i];
+        if (!m.mapped_vmm || m.own_handle || m.remote || m.phys.empty()) continue;
+        for (size_t c = 0; c < m.phys.size(); ++c) {
+            if (a_unmapped_[i][c] || a_last_stage_[i][c] > stage) continue;
+            drv_check(D.unmap(m.va + c * static_cast<std::uint64_t>(C), static_cast<size_t>(C)), "cuMemUnmap");
+            a_unmapped_[i][c] = 1;
+            const int p = m.phys[c];
+            if (!b_uses_[static_cast<size_t>(p)] && handles_[static_cast<size_t>(p)]) {
+                drv_check(D.release(handles_[static_cast<size_t>(p)]), "cuMemRelease");
+                handles_[static_cast<size_t>(p)] = 0;
+                freed += C;
+            }
+        }
+    }
+    released_bytes_ += freed;
+    return freed;
+}
+
 Arena::~Arena() {
     const Drv& D = Drv::get();
     cudaSetDevice(cfg_.device);
@@ -288,11 +323,19 @@ Arena::~Arena() {
                 cudaFree(reinterpret_cast<void*>(m.va));
                 continue;
             }
-            D.unmap(m.va, static_cast<size_t>(m.reserved));
+            if (l == 0 && !a_unmapped_.empty()) {  // some chunks already unmapped at run time
+                const std::int64_t C = cfg_.chunk_bytes;
+                const size_t i = static_cast<size_t>(&m - bufs_[0].data());
+                for (size_t c = 0; c < m.phys.size(); ++c)
+                    if (!a_unmapped_[i][c]) D.unmap(m.va + c * static_cast<std::uint64_t>(C), static_cast<size_t>(C));
+            } else {
+                D.unmap(m.va, static_cast<size_t>(m.reserved));
+            }
             D.addr_free(m.va, static_cast<size_t>(m.reserved));
             if (m.own_handle) D.release(m.handle);
         }
-    for (std::uint64_t h : handles_) D.release(h);
+    for (std::uint64_t h : handles_)
+        if (h) D.release(h);
 }
 
 void* Arena::ptr(int layout, int rank, int buf) const {

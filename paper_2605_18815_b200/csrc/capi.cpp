@@ -1194,6 +1194,13 @@ int rs_memory_plan(const rs_plan_t* ab, const rs_plan_t* ba, int64_t chunk_bytes
     return rs_memory_plan_ex(ab, ba, chunk_bytes, with_grads, 1, 0, 0, 1, stats, violations, order_ab, order_ba, cap);
 }
 
+int rs_arena_release_through(rs_arena_t* a, int stage, int64_t* freed) {
+    return guarded([&] {
+        *freed = a->a->release_through(stage);
+        return RS_OK;
+    });
+}
+
 int rs_arena_stats(const rs_arena_t* a, rs_arena_stats_t* out) {
     return guarded([&] {
         const mem::ArenaStats& s = a->a->stats();

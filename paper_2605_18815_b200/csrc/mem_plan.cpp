@@ -582,6 +582,26 @@ void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanC
     }
 }
 
+std::vector<std::vector<int>> last_read_stage(const MemoryPlan& mp, const core::PlanCore& ab,
+                                              const std::vector<exec::CopyOp>& ops_ab) {
+    // executed stage of each position: positions between two cuts share one launch group
+    const std::vector<StageIo> io = stage_io(mp, ab, ops_ab, mp.order[0], 0);
+    std::vector<int> stage(io.size(), 0);
+    int st = -1;
+    for (size_t s = 0; s < io.size(); ++s) {
+        if (s == 0 || (s < mp.cut[0].size() && mp.cut[0][s])) ++st;
+        stage[s] = st;
+    }
+    std::vector<std::vector<int>> out(mp.bufs[0].size());
+    for (size_t i = 0; i < mp.bufs[0].size(); ++i) out[i].assign(mp.bufs[0][i].phys.size(), -1);
+    for (size_t s = 0; s < io.size(); ++s)
+        for (size_t k = 0; k < io[s].reads.size(); k += 3) {
+            int& x = out[static_cast<size_t>(io[s].reads[k + 1])][static_cast<size_t>(io[s].reads[k + 2])];
+            x = std::max(x, stage[s]);
+        }
+    return out;
+}
+
 std::int64_t simulate_memory_plan(const MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba) {
     // owner[p] = (layout, buffer index, chunk index) whose data physical chunk p holds;
     // stages between two cuts run concurrently (one group), groups run in order

@@ -121,6 +121,10 @@ std::vector<std::pair<std::int64_t, double>> schedule_costs(const core::PlanCore
 /// where a stage overwrites a chunk an earlier stage of the running group still reads.
 void plan_stage_cuts(MemoryPlan& mp, const core::PlanCore& ab, const core::PlanCore* ba,
                      const std::vector<exec::CopyOp>& ops_ab, const std::vector<exec::CopyOp>& ops_ba);
+/// Executed stage (launch group, after the cuts) of the last read of every A chunk, per
+/// A buffer (-1: never read)
+std::vector<std::vector<int>> last_read_stage(const MemoryPlan& mp, const core::PlanCore& ab,
+                                              const std::vector<exec::CopyOp>& ops_ab);
 /// Replays the staged execution chunk by chunk (A->B, then B->A) tracking which
 /// logical chunk each physical chunk holds; counts reads of clobbered data and
 /// same-group read/write races. 0 == the aliasing is safe.
@@ -154,6 +158,12 @@ public:
     void bind_multicast(class Multicast& mc, int layout, int rank, int buf) const;
     /// bytes a multicast object must span to bind that buffer whole
     std::int64_t bind_size(int layout, int rank, int buf) const;
+    /// FreeObsoleteBuffers at run time (one-way arenas on one GPU): once stage `stage` of
+    /// A->B has completed, unmap every old-layout chunk whose last read was in a stage <=
+    /// `stage` and return the physical chunks the new layout does not reuse to the driver
+    /// (cuMemUnmap + cuMemRelease). Returns the bytes released by this call.
+    std::int64_t release_through(int stage);
+    std::int64_t released_bytes() const { return released_bytes_; }
 
 private:
     struct BufMap {
@@ -173,6 +183,11 @@ private:
     ArenaStats stats_;
     int nranks_[2] = {0, 0};
     int n_gpus_ = 1;
+    bool one_way_ = false;
+    std::vector<std::vector<int>> a_last_stage_;     // [A buffer][chunk]
+    std::vector<std::vector<char>> a_unmapped_;      // [A buffer][chunk]
+    std::vector<char> b_uses_;                       // physical chunk -> mapped by a B chunk
+    std::int64_t released_bytes_ = 0;
 };
 
 /// One shareable VMM device buffer (POSIX-FD handle): allocated on this process's GPU,

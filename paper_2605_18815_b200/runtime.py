@@ -509,6 +509,26 @@ def run_stages(ex: Executor, stream: int, world: int, barrier=None) -> None:
     ex.run_dup(stream)
 
 
+def run_releasing(ex: Executor, arena, stream) -> int:
+    """A one-way transition on one GPU that hands consumed source memory back while it runs
+    (Algorithm 1 FreeObsoleteBuffers): every memory-aware stage is
+    enqueued at once with an event after each; the host then waits for stage s and
+    releases the old-layout chunks s made dead while the GPU runs stage s+1.
+    `stream` is a torch stream. Returns the bytes released."""
+    import torch
+    evs = []
+    for s in range(ex.num_stages()):
+        ex.run_stage(s, stream.cuda_stream)
+        e = torch.cuda.Event()
+        e.record(stream)
+        evs.append(e)
+    freed = 0
+    for s, e in enumerate(evs):
+        e.synchronize()
+        freed += arena.release_through(s)
+    return freed
+
+
 def run_dedup_early(ex: Executor, stream, side_stream, group=None) -> None:
     """One transition with early replica dedup (Executor.set_replica_dedup(early=True)):
     stage 0 = the pushes of regions other ranks on the destination GPU copy plus most of the
