@@ -20,6 +20,7 @@
 #include "reshard/executor.hpp"
 #include "reshard/executor_rt.hpp"
 #include "reshard/schedule.hpp"
+#include "reshard/pool.hpp"
 
 namespace reshard {
 namespace exec {
@@ -705,20 +706,14 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     // side array and interleaved into place.
     const auto t_fin0 = std::chrono::steady_clock::now();
     const size_t nrec = pending.size();
-    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::max<size_t>(1, std::min<size_t>({hw, 16, nrec / 256 + 1}));
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(pool::size(), nrec / 256 + 1));
     int max_key = -1;
     for (const Pending& q : pending) max_key = std::max(max_key, q.key);
     const size_t nb = static_cast<size_t>(max_key + 1) * 5;
     std::vector<std::vector<size_t>> cnt(nt, std::vector<size_t>(nb, 0));
     std::vector<std::vector<std::uint8_t>> lane_mask(nt, std::vector<std::uint8_t>(nb, 0));  // bit 0: seen, bit 1: several lanes
     std::vector<std::vector<std::uint8_t>> lane0(nt, std::vector<std::uint8_t>(nb, 0));
-    auto parallel = [&](auto&& fn) {
-        std::vector<std::thread> th;
-        for (size_t t = 1; t < nt; ++t) th.emplace_back(fn, t);
-        fn(0);
-        for (auto& x : th) x.join();
-    };
+    auto parallel = [&](auto&& fn) { pool::run(nt, fn); };
     parallel([&](size_t t) {
         for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
             const Pending& q = pending[i];
@@ -785,14 +780,14 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         }
     });
     {
-        std::vector<std::thread> th;
+        std::vector<size_t> mb;
         for (size_t b = 0; b < nb; ++b)
-            if (multi[b] && bucket_n[b])
-                th.emplace_back([&, b] {
-                    const std::vector<std::pair<const Tile*, const std::uint8_t*>> spans{{side_t[b].data(), side_l[b].data()}};
-                    interleave_into(out + begin[b], spans, {bucket_n[b]});
-                });
-        for (auto& x : th) x.join();
+            if (multi[b] && bucket_n[b]) mb.push_back(b);
+        pool::run(mb.size(), [&](size_t k) {
+            const size_t b = mb[k];
+            const std::vector<std::pair<const Tile*, const std::uint8_t*>> spans{{side_t[b].data(), side_l[b].data()}};
+            interleave_into(out + begin[b], spans, {bucket_n[b]});
+        });
     }
     pending.clear();
     const auto t_asm = std::chrono::steady_clock::now();

@@ -5,6 +5,7 @@
 #include <thread>
 
 #include "reshard/executor.hpp"
+#include "reshard/pool.hpp"
 
 namespace reshard {
 namespace exec {
@@ -154,17 +155,12 @@ std::vector<CopyOp> build_ops(const PlanCore& P) {
         for (const stair::Triple& T : P.triples)
             if (!overridden(T.dst, T.tensor)) tv.push_back(&T);
         for (const stair::Triple& T : P.retain_triples) tv.push_back(&T);
-        const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-        const size_t nth = std::max<size_t>(1, std::min<size_t>({hw, 16, tv.size() / 64 + 1}));
+        const size_t nth = std::max<size_t>(1, std::min<size_t>(pool::size(), tv.size() / 64 + 1));
         std::vector<std::vector<CopyOp>> part(nth);
-        auto work = [&](size_t t) {
+        pool::run(nth, [&](size_t t) {
             Emitter Et{P, part[t]};
             for (size_t i = tv.size() * t / nth; i < tv.size() * (t + 1) / nth; ++i) Et.triple(*tv[i]);
-        };
-        std::vector<std::thread> th;
-        for (size_t t = 1; t < nth; ++t) th.emplace_back(work, t);
-        work(0);
-        for (auto& x : th) x.join();
+        });
         size_t n = ops.size();
         for (const auto& v : part) n += v.size();
         ops.reserve(n);

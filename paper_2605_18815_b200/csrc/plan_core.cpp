@@ -2,6 +2,7 @@
 // proximity rules), ZeRO triples, D2 detection/extension, flat-run expansion and
 // the reference dump format.
 #include "reshard/plan_core.hpp"
+#include "reshard/pool.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -158,29 +159,11 @@ struct Pending {
     std::vector<int> cands;
 };
 
-/// fn(i) for i in [0, n) on up to hardware_concurrency threads (contiguous blocks); the
-/// planner's per-route / per-rank-pair work is independent, results are merged in order
+/// the planner's per-route / per-rank-pair loops on the host worker pool (contiguous
+/// slices; results are merged in order by the callers)
 template <class F>
 void parallel_for(size_t n, F&& fn) {
-    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>({n, hw, 16});
-    if (nt <= 1) {
-        for (size_t i = 0; i < n; ++i) fn(i);
-        return;
-    }
-    std::vector<std::thread> th;
-    std::vector<std::exception_ptr> err(nt);
-    for (size_t t = 0; t < nt; ++t)
-        th.emplace_back([&, t] {
-            try {
-                for (size_t i = t; i < n; i += nt) fn(i);
-            } catch (...) {
-                err[t] = std::current_exception();
-            }
-        });
-    for (auto& x : th) x.join();
-    for (auto& e : err)
-        if (e) std::rethrow_exception(e);
+    pool::parallel_for(n, std::forward<F>(fn));
 }
 
 }  // namespace

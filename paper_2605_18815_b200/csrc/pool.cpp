@@ -1,0 +1,119 @@
+// Persistent host worker pool (reshard/pool.hpp).
+#include "reshard/pool.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace reshard {
+namespace pool {
+
+namespace {
+
+thread_local bool t_in_pool = false;
+
+class Pool {
+public:
+    Pool() {
+        const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
+        nthreads_ = std::min<std::size_t>(hw, 16);
+        for (std::size_t i = 1; i < nthreads_; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    std::size_t size() const { return nthreads_; }
+
+    void run(std::size_t n, const std::function<void(std::size_t)>& fn) {
+        if (n == 0) return;
+        if (n == 1 || t_in_pool || nthreads_ == 1) {  // inline: tiny loops and nested calls
+            for (std::size_t t = 0; t < n; ++t) fn(t);
+            return;
+        }
+        std::lock_guard<std::mutex> serial(run_mu_);  // one parallel loop at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            n_ = n;
+            next_.store(0);
+            pending_ = n;
+            error_ = nullptr;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+        fn_ = nullptr;
+        if (error_) std::rethrow_exception(error_);
+    }
+
+private:
+    void work() {
+        const bool was = t_in_pool;
+        t_in_pool = true;
+        for (;;) {
+            const std::size_t t = next_.fetch_add(1);
+            if (t >= n_) break;
+            std::exception_ptr e;
+            try {
+                (*fn_)(t);
+            } catch (...) {
+                e = std::current_exception();
+            }
+            std::lock_guard<std::mutex> lk(mu_);
+            if (e && !error_) error_ = e;
+            if (--pending_ == 0) done_cv_.notify_all();
+        }
+        t_in_pool = was;
+    }
+
+    void loop() {
+        std::uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+                if (!fn_) continue;
+            }
+            work();
+        }
+    }
+
+    std::size_t nthreads_ = 1;
+    std::vector<std::thread> workers_;
+    std::mutex mu_, run_mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(std::size_t)>* fn_ = nullptr;
+    std::size_t n_ = 0, pending_ = 0;
+    std::atomic<std::size_t> next_{0};
+    std::uint64_t gen_ = 0;
+    bool stop_ = false;
+    std::exception_ptr error_;
+};
+
+Pool& instance() {
+    static Pool p;
+    return p;
+}
+
+}  // namespace
+
+std::size_t size() { return instance().size(); }
+
+void run(std::size_t n, const std::function<void(std::size_t)>& fn) { instance().run(n, fn); }
+
+}  // namespace pool
+}  // namespace reshard
