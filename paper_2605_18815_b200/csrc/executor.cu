@@ -748,11 +748,21 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(n);
         total += n;
     }
+    (void)staging;
     Tile* out = nullptr;
     if (total) {
-        if (!staging) throw std::logic_error("TileSet::finalize needs a staging buffer");
-        if (staging->size() < total * sizeof(Tile)) staging->grow(total * sizeof(Tile) * 5 / 4);
-        out = static_cast<Tile*>(staging->ptr);
+        // descriptors alternate between two slots (host pinned + device): this finalize
+        // fills slot cur^1 while launches of the previous one may still read slot cur
+        cur_buf_flip();
+        PinnedBuf*& hb = hbuf[this->cur];
+        if (!hb) hb = new PinnedBuf();
+        for (cudaEvent_t e : hfences[this->cur]) {  // earlier uploads out of this pinned slot
+            RS_CUDA(cudaEventSynchronize(e));
+            fence_pool.push_back(e);
+        }
+        hfences[this->cur].clear();
+        if (hb->size() < total * sizeof(Tile)) hb->grow(total * sizeof(Tile) * 5 / 4);
+        out = static_cast<Tile*>(hb->ptr);
     }
     // side arrays of the multi-lane buckets (tiles + lanes, interleaved afterwards)
     std::vector<std::vector<Tile>> side_t(nb);
@@ -792,29 +802,25 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     pending.clear();
     const auto t_asm = std::chrono::steady_clock::now();
     if (total) {
-        // two descriptor buffers used in turn: a re-prepare uploads into the one the last
-        // launch did not read, so it may overlap kernels of the previous prepare still in
-        // flight. Both are kept across re-prepares: with peer access enabled every
-        // cudaMalloc/cudaFree also edits the peers' mappings (measured: 0.6 s stalls)
-        cur_buf_flip();
+        // two device descriptor buffers used in turn; both are kept across re-prepares:
+        // with peer access enabled every cudaMalloc/cudaFree also edits the peers'
+        // mappings (measured: 0.6 s stalls)
         if (total * sizeof(Tile) > dev_bytes[this->cur]) {
             if (dev_buf[this->cur]) cudaFree(dev_buf[this->cur]);
             dev_buf[this->cur] = nullptr;
             dev_bytes[this->cur] = total * sizeof(Tile) * 5 / 4;
             RS_CUDA(cudaMalloc(&dev_buf[this->cur], dev_bytes[this->cur]));
         }
-        // the upload into dev_buf[cur] waits for every launch that read it
-        for (cudaEvent_t e : fences[this->cur]) {
-            RS_CUDA(cudaStreamWaitEvent(upload, e, 0));
-            fence_pool.push_back(e);
-        }
+        // the first upload into dev_buf[cur] follows every launch that read it
+        for (cudaEvent_t e : wait_first) fence_pool.push_back(e);
+        wait_first = std::move(fences[this->cur]);
         fences[this->cur].clear();
         dev = dev_buf[this->cur];
-        // private non-blocking stream: descriptor uploads never serialize with the
-        // caller's (training) streams, so the EDM can prepare in the background
-        RS_CUDA(cudaMemcpyAsync(dev, out, total * sizeof(Tile), cudaMemcpyHostToDevice, upload));
-        RS_CUDA(cudaStreamSynchronize(upload));
+        uploaded.assign(groups.size(), 0);
+    } else {
+        uploaded.clear();
     }
+    (void)upload;
     ntiles = total;
     if (std::getenv("RS_TIMING") && total > 4096) {
         const auto t_up = std::chrono::steady_clock::now();
@@ -830,11 +836,47 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
 }
 
 TileSet::~TileSet() {
+    for (auto& v : hfences)
+        for (cudaEvent_t e : v) cudaEventSynchronize(e), cudaEventDestroy(e);
+    for (cudaEvent_t e : wait_first) cudaEventDestroy(e);
+    for (PinnedBuf* b : hbuf) delete b;
     for (void* p : dev_buf)
         if (p) cudaFree(p);
     for (auto& v : fences)
         for (cudaEvent_t e : v) cudaEventDestroy(e);
     for (cudaEvent_t e : fence_pool) cudaEventDestroy(e);
+}
+
+cudaEvent_t TileSet::take_event() const {
+    cudaEvent_t e = nullptr;
+    if (!fence_pool.empty()) {
+        e = fence_pool.back();
+        fence_pool.pop_back();
+    } else {
+        RS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return e;
+}
+
+void TileSet::upload_group(size_t gi, cudaStream_t stream) const {
+    if (gi >= uploaded.size() || uploaded[gi]) return;
+    for (cudaEvent_t e : wait_first) {
+        RS_CUDA(cudaStreamWaitEvent(stream, e, 0));
+        fence_pool.push_back(e);
+    }
+    wait_first.clear();
+    const Group& g = groups[gi];
+    const Tile* src = static_cast<const Tile*>(hbuf[cur]->ptr) + g.begin;
+    RS_CUDA(cudaMemcpyAsync(static_cast<Tile*>(dev) + g.begin, src, static_cast<size_t>(g.count) * sizeof(Tile),
+                            cudaMemcpyHostToDevice, stream));
+    cudaEvent_t e = take_event();
+    RS_CUDA(cudaEventRecord(e, stream));
+    hfences[cur].push_back(e);
+    uploaded[gi] = 1;
+}
+
+void TileSet::flush_uploads(cudaStream_t stream) const {
+    for (size_t gi = 0; gi < uploaded.size(); ++gi) upload_group(gi, stream);
 }
 
 void TileSet::fence(cudaStream_t stream) const {
@@ -897,9 +939,11 @@ int TileSet::launch(cudaStream_t stream, std::uint64_t sbase, std::uint64_t dbas
     const Tile* base = static_cast<const Tile*>(dev);
     const bool w32 = vec32_enabled();
     auto grid_of = [&](auto kernel, int n) { return std::min(n, sms * std::min(want, resident_ctas(kernel))); };
-    for (const Group& g : groups) {
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const Group& g = groups[gi];
         if (key_mod > 0 && g.key % key_mod != key_rem) continue;
         if (key_mod < 0 && g.key != key_rem) continue;  // exact key (one memory-aware stage)
+        upload_group(gi, stream);  // first launch after a finalize: this group's descriptors
         const int n = g.count;
         const Tile* t = base + g.begin;
         switch (g.cls) {
@@ -1286,7 +1330,9 @@ int Executor::launch_multicast(cudaStream_t stream) const {
     if (!mc_ || mc_->groups.empty()) return 0;
     const Tile* base = static_cast<const Tile*>(mc_->dev);
     int n = 0;
-    for (const TileSet::Group& g : mc_->groups) {
+    for (size_t gi = 0; gi < mc_->groups.size(); ++gi) {
+        const TileSet::Group& g = mc_->groups[gi];
+        mc_->upload_group(gi, stream);
         const char* mcc = std::getenv("RS_MC_CTAS_PER_SM");
         const int grid = std::min(g.count, sms_ * (mcc ? std::max(1, std::atoi(mcc)) : 1));
         copy_tiles_kernel<16, true><<<grid, kThreads, 0, stream>>>(base + g.begin, g.count, 0, 0);
@@ -1305,6 +1351,9 @@ int Executor::run_graph(cudaStream_t stream) {
     if (!graph_exec_ || graph_stream_ != stream) {
         if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;
+        // descriptors go up outside the capture (the graph replays kernels only)
+        if (fused_) fused_->flush_uploads(stream);
+        if (mc_) mc_->flush_uploads(stream);
         cudaGraph_t g = nullptr;
         RS_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         try {

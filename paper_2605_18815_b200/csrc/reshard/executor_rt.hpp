@@ -92,6 +92,19 @@ struct TileSet {
     // be outstanding)
     mutable std::vector<cudaEvent_t> fences[2];
     mutable std::vector<cudaEvent_t> fence_pool;
+    // Lazy upload: finalize leaves the descriptors in this set's own pinned buffer; the
+    // first launch of each group copies that group's slice on the launch stream right
+    // before the kernel, so the uploads of later groups overlap earlier groups' kernels
+    // and prepare() never waits for a DMA. hfences guard the pinned buffer's reuse,
+    // wait_first holds the previous readers of dev_buf[cur] the first upload must follow.
+    PinnedBuf* hbuf[2] = {nullptr, nullptr};
+    mutable std::vector<cudaEvent_t> hfences[2];
+    mutable std::vector<cudaEvent_t> wait_first;
+    mutable std::vector<char> uploaded;
+    /// upload every group not uploaded yet on `stream` (before a graph capture)
+    void flush_uploads(cudaStream_t stream) const;
+    void upload_group(size_t gi, cudaStream_t stream) const;
+    cudaEvent_t take_event() const;
     /// record a fence for the current descriptors on `stream` (skipped while capturing:
     /// run_graph fences after the graph launch)
     void fence(cudaStream_t stream) const;
