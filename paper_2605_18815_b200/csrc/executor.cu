@@ -706,6 +706,51 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     // side array and interleaved into place.
     const auto t_fin0 = std::chrono::steady_clock::now();
     const size_t nrec = pending.size();
+    // Lane interleave at record granularity (default): within each key the recorded
+    // copies are reordered so every destination lane progresses in proportion to its
+    // bytes (the tile-level rule applied to whole copies: O(records x lanes), and the
+    // tiles then need no reordering). RS_INTERLEAVE_TILES=1: the exact tile-level merge.
+    static const bool tile_level = [] {
+        const char* v = std::getenv("RS_INTERLEAVE_TILES");
+        return v && std::string(v) == "1";
+    }();
+    if (interleave && !tile_level && nrec > 1) {
+        std::vector<Pending> out;
+        out.reserve(nrec);
+        std::vector<size_t> idx(nrec);
+        for (size_t i = 0; i < nrec; ++i) idx[i] = i;
+        std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return pending[a].key < pending[b].key; });
+        for (size_t lo = 0; lo < nrec;) {
+            size_t hi = lo;
+            while (hi < nrec && pending[idx[hi]].key == pending[idx[lo]].key) ++hi;
+            int nl = 0;
+            for (size_t i = lo; i < hi; ++i) nl = std::max(nl, pending[idx[i]].lane + 1);
+            std::vector<std::vector<size_t>> q(static_cast<size_t>(nl));
+            std::vector<double> total(static_cast<size_t>(nl), 0.0), done(static_cast<size_t>(nl), 0.0);
+            auto bytes = [&](size_t i) { return static_cast<double>(pending[i].rows) * static_cast<double>(pending[i].rb); };
+            for (size_t i = lo; i < hi; ++i) {
+                q[static_cast<size_t>(pending[idx[i]].lane)].push_back(idx[i]);
+                total[static_cast<size_t>(pending[idx[i]].lane)] += bytes(idx[i]);
+            }
+            std::vector<size_t> head(static_cast<size_t>(nl), 0);
+            for (size_t k = lo; k < hi; ++k) {
+                int best = -1;
+                double bk = 0;
+                for (int l = 0; l < nl; ++l) {
+                    const size_t L = static_cast<size_t>(l);
+                    if (head[L] >= q[L].size()) continue;
+                    const double key = (done[L] + 0.5 * bytes(q[L][head[L]])) / total[L];
+                    if (best < 0 || key < bk) best = l, bk = key;
+                }
+                const size_t B = static_cast<size_t>(best);
+                const size_t i = q[B][head[B]++];
+                done[B] += bytes(i);
+                out.push_back(pending[i]);
+            }
+            lo = hi;
+        }
+        pending.swap(out);
+    }
     const size_t nt = std::max<size_t>(1, std::min<size_t>(pool::size(), nrec / 256 + 1));
     int max_key = -1;
     for (const Pending& q : pending) max_key = std::max(max_key, q.key);
@@ -739,7 +784,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
             if (l0 < 0) l0 = lane0[t][b];
             else if (l0 != lane0[t][b]) multi[b] = 1;
         }
-        if (!interleave) multi[b] = 0;
+        if (!interleave || !tile_level) multi[b] = 0;
         begin[b] = total;
         bucket_n[b] = n;
         if (!n) continue;
