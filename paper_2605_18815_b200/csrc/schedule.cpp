@@ -34,7 +34,7 @@ std::vector<std::vector<int>> memory_aware_chunk(const std::vector<int>& steps, 
                                            "budget %lld)", s, static_cast<long long>(c), static_cast<long long>(M)));
         if (used + c > M && !cur.empty()) {
             stages.push_back(cur);
-            cur = {s};
+            cur.assign(1, s);
             used = c;
         } else {
             cur.push_back(s);
