@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,7 @@
 
 #include "reshard/executor.hpp"
 #include "reshard/executor_rt.hpp"
+#include "reshard/tiles.hpp"
 #include "reshard/schedule.hpp"
 #include "reshard/pool.hpp"
 
@@ -363,14 +365,6 @@ CUresult mem_get_address_range(CUdeviceptr* base, size_t* size, CUdeviceptr p) {
     return fn(base, size, p);
 }
 
-int align_class(std::uint64_t x) {
-    if (x % 16 == 0) return 16;
-    if (x % 8 == 0) return 8;
-    if (x % 4 == 0) return 4;
-    if (x % 2 == 0) return 2;
-    return 1;
-}
-int class_index(int v) { return v == 16 ? 0 : v == 8 ? 1 : v == 4 ? 2 : v == 2 ? 3 : 4; }
 
 }  // namespace
 
@@ -578,6 +572,21 @@ void Executor::import_ipc(const std::uint8_t* blob, size_t len) {
     }
 }
 
+/// The descriptor cut on the GPU: one thread per recorded copy writes its tiles at the
+/// per-(record, alignment class) offsets the host derived from the tile counts.
+__global__ void cut_kernel(const CopyRec* __restrict__ recs, const std::int32_t* __restrict__ pos, int n,
+                           Tile* __restrict__ out) {
+    const int i = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
+    const std::int32_t* p = pos + 5 * static_cast<size_t>(i);
+    int c[5] = {0, 0, 0, 0, 0};
+    auto emit = [&](int b, const Tile& t) {
+        const int cls = b % 5;
+        out[p[cls] + c[cls]++] = t;
+    };
+    cut_tiles(recs[i], emit);
+}
+
 void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t rows, std::int64_t rb, std::int64_t sp,
                   std::int64_t dp, std::int64_t kTile, int lane) {
     // recorded here, cut into tiles by finalize() on host threads
@@ -585,57 +594,6 @@ void TileSet::add(int key, std::uint64_t src, std::uint64_t dst, std::int64_t ro
     pending.push_back(Pending{src, dst, rows, rb, sp, dp, kTile, key, lane});
 }
 
-namespace {
-
-/// Cut one recorded copy into tiles: emit(bucket = key * 5 + alignment class, tile, lane)
-template <class Emit>
-void cut_tiles(const TileSet::Pending& q, Emit&& emit_to) {
-    std::int64_t rows = q.rows, rb = q.rb;
-    const std::int64_t sp = q.sp, dp = q.dp, kTile = q.kTile;
-    if (rows > 1 && sp == rb && dp == rb) {  // contiguous block
-        rb *= rows;
-        rows = 1;
-    }
-    auto emit = [&](std::uint64_t s, std::uint64_t d, std::int64_t nr, std::int64_t nb) {
-        const Tile t{s, d, static_cast<std::uint64_t>(sp), static_cast<std::uint64_t>(dp), static_cast<std::uint32_t>(nr),
-                     static_cast<std::uint32_t>(nb)};
-        std::uint64_t a = s | d | static_cast<std::uint64_t>(nb);
-        if (nr > 1) a |= static_cast<std::uint64_t>(sp) | static_cast<std::uint64_t>(dp);
-        emit_to(static_cast<size_t>(q.key) * 5 + class_index(align_class(a)), t);
-    };
-    if (rows == 1 || rb >= kTile) {
-        for (std::int64_t r = 0; r < rows; ++r) {
-            std::uint64_t s = q.src + static_cast<std::uint64_t>(r * sp), d = q.dst + static_cast<std::uint64_t>(r * dp);
-            std::int64_t left = rb;
-            // peel an unaligned head so the body runs 16-byte vectors when both sides
-            // share the same misalignment (relative offsets keep it: bases are 256-B aligned)
-            if ((s % 16) == (d % 16) && (s % 16) != 0) {
-                const std::int64_t head = std::min<std::int64_t>(left, 16 - static_cast<std::int64_t>(s % 16));
-                emit(s, d, 1, head);
-                s += static_cast<std::uint64_t>(head);
-                d += static_cast<std::uint64_t>(head);
-                left -= head;
-            }
-            while (left > 0) {
-                const std::int64_t n = std::min(left, kTile);
-                const bool aligned = (s % 16) == 0 && (d % 16) == 0;
-                const std::int64_t body = (aligned && n > 16) ? n - n % 16 : n;
-                emit(s, d, 1, body);
-                s += static_cast<std::uint64_t>(body);
-                d += static_cast<std::uint64_t>(body);
-                left -= body;
-            }
-        }
-    } else {
-        const std::int64_t per = std::max<std::int64_t>(1, kTile / rb);
-        for (std::int64_t r = 0; r < rows; r += per) {
-            const std::int64_t nr = std::min(per, rows - r);
-            emit(q.src + static_cast<std::uint64_t>(r * sp), q.dst + static_cast<std::uint64_t>(r * dp), nr, rb);
-        }
-    }
-}
-
-}  // namespace
 
 void PinnedBuf::grow(size_t bytes) {
     if (ptr) cudaFreeHost(ptr);
@@ -755,45 +713,61 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     int max_key = -1;
     for (const Pending& q : pending) max_key = std::max(max_key, q.key);
     const size_t nb = static_cast<size_t>(max_key + 1) * 5;
-    std::vector<std::vector<size_t>> cnt(nt, std::vector<size_t>(nb, 0));
-    std::vector<std::vector<std::uint8_t>> lane_mask(nt, std::vector<std::uint8_t>(nb, 0));  // bit 0: seen, bit 1: several lanes
-    std::vector<std::vector<std::uint8_t>> lane0(nt, std::vector<std::uint8_t>(nb, 0));
     auto parallel = [&](auto&& fn) { pool::run(nt, fn); };
-    parallel([&](size_t t) {
-        for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
-            const Pending& q = pending[i];
-            cut_tiles(q, [&](size_t b, const Tile&) {
-                ++cnt[t][b];
-                if (!(lane_mask[t][b] & 1)) lane_mask[t][b] = 1, lane0[t][b] = static_cast<std::uint8_t>(q.lane);
-                else if (lane0[t][b] != q.lane) lane_mask[t][b] |= 2;
-            });
-        }
-    });
-    const auto t_cut = std::chrono::steady_clock::now();
-    groups.clear();
+    gpu_cut = !(interleave && tile_level) && !host_tiles_forced();
     std::vector<size_t> begin(nb, 0), bucket_n(nb, 0);
+    std::vector<std::array<std::int32_t, 5>> rc;  // GPU cut: tiles per (record, class)
+    std::vector<std::vector<size_t>> cnt;         // host cut: tiles per (thread, bucket)
     std::vector<char> multi(nb, 0);
+    groups.clear();
     size_t total = 0;
-    for (size_t b = 0; b < nb; ++b) {
-        size_t n = 0;
-        int l0 = -1;
-        for (size_t t = 0; t < nt; ++t) {
-            n += cnt[t][b];
-            if (!(lane_mask[t][b] & 1)) continue;
-            if (lane_mask[t][b] & 2) multi[b] = 1;
-            if (l0 < 0) l0 = lane0[t][b];
-            else if (l0 != lane0[t][b]) multi[b] = 1;
+    if (gpu_cut) {
+        rc.assign(nrec, {0, 0, 0, 0, 0});
+        pool::parallel_for(nrec, [&](size_t i) {
+            auto count = [&](int b, const Tile&) { ++rc[i][static_cast<size_t>(b % 5)]; };
+            cut_tiles(pending[i], count);
+        });
+        for (size_t i = 0; i < nrec; ++i)
+            for (int c = 0; c < 5; ++c) bucket_n[static_cast<size_t>(pending[i].key) * 5 + c] += static_cast<size_t>(rc[i][c]);
+    } else {
+        cnt.assign(nt, std::vector<size_t>(nb, 0));
+        std::vector<std::vector<std::uint8_t>> lane_mask(nt, std::vector<std::uint8_t>(nb, 0));  // bit 0: seen, 1: several
+        std::vector<std::vector<std::uint8_t>> lane0(nt, std::vector<std::uint8_t>(nb, 0));
+        parallel([&](size_t t) {
+            for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
+                const Pending& q = pending[i];
+                auto count = [&](int bi, const Tile&) {
+                    const size_t b = static_cast<size_t>(bi);
+                    ++cnt[t][b];
+                    if (!(lane_mask[t][b] & 1)) lane_mask[t][b] = 1, lane0[t][b] = static_cast<std::uint8_t>(q.lane);
+                    else if (lane0[t][b] != q.lane) lane_mask[t][b] |= 2;
+                };
+                cut_tiles(q, count);
+            }
+        });
+        for (size_t b = 0; b < nb; ++b) {
+            int l0 = -1;
+            for (size_t t = 0; t < nt; ++t) {
+                bucket_n[b] += cnt[t][b];
+                if (!(lane_mask[t][b] & 1)) continue;
+                if (lane_mask[t][b] & 2) multi[b] = 1;
+                if (l0 < 0) l0 = lane0[t][b];
+                else if (l0 != lane0[t][b]) multi[b] = 1;
+            }
+            if (!interleave || !tile_level) multi[b] = 0;
         }
-        if (!interleave || !tile_level) multi[b] = 0;
+    }
+    const auto t_cut = std::chrono::steady_clock::now();
+    for (size_t b = 0; b < nb; ++b) {
         begin[b] = total;
-        bucket_n[b] = n;
-        if (!n) continue;
+        if (!bucket_n[b]) continue;
         const int c = static_cast<int>(b % 5);
-        groups.push_back({c, static_cast<int>(total), static_cast<int>(n), static_cast<int>(b / 5)});
-        if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(n);
-        total += n;
+        groups.push_back({c, static_cast<int>(total), static_cast<int>(bucket_n[b]), static_cast<int>(b / 5)});
+        if (stats) stats->tiles_by_class[c] += static_cast<std::int64_t>(bucket_n[b]);
+        total += bucket_n[b];
     }
     (void)staging;
+    const size_t host_bytes = gpu_cut ? nrec * (sizeof(CopyRec) + 5 * sizeof(std::int32_t)) : total * sizeof(Tile);
     Tile* out = nullptr;
     if (total) {
         // descriptors alternate between two slots (host pinned + device): this finalize
@@ -806,35 +780,51 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
             fence_pool.push_back(e);
         }
         hfences[this->cur].clear();
-        if (hb->size() < total * sizeof(Tile)) hb->grow(total * sizeof(Tile) * 5 / 4);
+        if (hb->size() < host_bytes) hb->grow(host_bytes * 5 / 4);
         out = static_cast<Tile*>(hb->ptr);
     }
-    // side arrays of the multi-lane buckets (tiles + lanes, interleaved afterwards)
-    std::vector<std::vector<Tile>> side_t(nb);
-    std::vector<std::vector<std::uint8_t>> side_l(nb);
-    for (size_t b = 0; b < nb; ++b)
-        if (multi[b]) side_t[b].resize(bucket_n[b]), side_l[b].resize(bucket_n[b]);
-    // per (thread, bucket) write cursor: the bucket's start + the earlier threads' counts
-    std::vector<std::vector<size_t>> cur(nt, std::vector<size_t>(nb, 0));
-    for (size_t b = 0; b < nb; ++b) {
-        size_t at = multi[b] ? 0 : begin[b];
-        for (size_t t = 0; t < nt; ++t) cur[t][b] = at, at += cnt[t][b];
-    }
-    parallel([&](size_t t) {
-        std::vector<size_t>& c = cur[t];
-        for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
-            const Pending& q = pending[i];
-            cut_tiles(q, [&](size_t b, const Tile& tile) {
-                if (multi[b]) {
-                    side_l[b][c[b]] = static_cast<std::uint8_t>(q.lane);
-                    side_t[b][c[b]++] = tile;
-                } else {
-                    out[c[b]++] = tile;
-                }
-            });
+    if (gpu_cut && total) {
+        // records + per-(record, class) tile offsets: the GPU writes the tiles (cut_kernel)
+        CopyRec* recs = static_cast<CopyRec*>(hbuf[this->cur]->ptr);
+        std::int32_t* pos = reinterpret_cast<std::int32_t*>(recs + nrec);
+        std::vector<size_t> run(begin);
+        for (size_t i = 0; i < nrec; ++i) {
+            recs[i] = pending[i];
+            for (int c = 0; c < 5; ++c) {
+                const size_t b = static_cast<size_t>(pending[i].key) * 5 + c;
+                pos[5 * i + c] = static_cast<std::int32_t>(run[b]);
+                run[b] += static_cast<size_t>(rc[i][c]);
+            }
         }
-    });
-    {
+        nrec_cut = nrec;
+    } else if (total) {
+        // side arrays of the multi-lane buckets (tiles + lanes, interleaved afterwards)
+        std::vector<std::vector<Tile>> side_t(nb);
+        std::vector<std::vector<std::uint8_t>> side_l(nb);
+        for (size_t b = 0; b < nb; ++b)
+            if (multi[b]) side_t[b].resize(bucket_n[b]), side_l[b].resize(bucket_n[b]);
+        // per (thread, bucket) write cursor: the bucket's start + the earlier threads' counts
+        std::vector<std::vector<size_t>> cur(nt, std::vector<size_t>(nb, 0));
+        for (size_t b = 0; b < nb; ++b) {
+            size_t at = multi[b] ? 0 : begin[b];
+            for (size_t t = 0; t < nt; ++t) cur[t][b] = at, at += cnt[t][b];
+        }
+        parallel([&](size_t t) {
+            std::vector<size_t>& c = cur[t];
+            for (size_t i = nrec * t / nt; i < nrec * (t + 1) / nt; ++i) {
+                const Pending& q = pending[i];
+                auto write = [&](int bi, const Tile& tile) {
+                    const size_t b = static_cast<size_t>(bi);
+                    if (multi[b]) {
+                        side_l[b][c[b]] = static_cast<std::uint8_t>(q.lane);
+                        side_t[b][c[b]++] = tile;
+                    } else {
+                        out[c[b]++] = tile;
+                    }
+                };
+                cut_tiles(q, write);
+            }
+        });
         std::vector<size_t> mb;
         for (size_t b = 0; b < nb; ++b)
             if (multi[b] && bucket_n[b]) mb.push_back(b);
@@ -861,15 +851,24 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         wait_first = std::move(fences[this->cur]);
         fences[this->cur].clear();
         dev = dev_buf[this->cur];
+        if (gpu_cut && host_bytes > rec_bytes[this->cur]) {
+            if (dev_rec[this->cur]) cudaFree(dev_rec[this->cur]);
+            dev_rec[this->cur] = nullptr;
+            rec_bytes[this->cur] = host_bytes * 5 / 4;
+            RS_CUDA(cudaMalloc(&dev_rec[this->cur], rec_bytes[this->cur]));
+        }
         uploaded.assign(groups.size(), 0);
+        materialized = false;
     } else {
         uploaded.clear();
+        materialized = true;
     }
     (void)upload;
     ntiles = total;
     if (std::getenv("RS_TIMING") && total > 4096) {
         const auto t_up = std::chrono::steady_clock::now();
-        std::fprintf(stderr, "[reshard] finalize: count %.2f ms (%zu threads), write %.2f ms, upload %.2f ms\n",
+        std::fprintf(stderr, "[reshard] finalize (%s cut): count %.2f ms (%zu threads), write %.2f ms, rest %.2f ms\n",
+                     gpu_cut ? "GPU" : "host",
                      std::chrono::duration<double, std::milli>(t_cut - t_fin0).count(), nt,
                      std::chrono::duration<double, std::milli>(t_asm - t_cut).count(),
                      std::chrono::duration<double, std::milli>(t_up - t_asm).count());
@@ -887,6 +886,8 @@ TileSet::~TileSet() {
     for (PinnedBuf* b : hbuf) delete b;
     for (void* p : dev_buf)
         if (p) cudaFree(p);
+    for (void* p : dev_rec)
+        if (p) cudaFree(p);
     for (auto& v : fences)
         for (cudaEvent_t e : v) cudaEventDestroy(e);
     for (cudaEvent_t e : fence_pool) cudaEventDestroy(e);
@@ -903,7 +904,31 @@ cudaEvent_t TileSet::take_event() const {
     return e;
 }
 
+void TileSet::materialize(cudaStream_t stream) const {
+    if (materialized) return;
+    for (cudaEvent_t e : wait_first) {
+        RS_CUDA(cudaStreamWaitEvent(stream, e, 0));
+        fence_pool.push_back(e);
+    }
+    wait_first.clear();
+    const size_t bytes = nrec_cut * (sizeof(CopyRec) + 5 * sizeof(std::int32_t));
+    RS_CUDA(cudaMemcpyAsync(dev_rec[cur], hbuf[cur]->ptr, bytes, cudaMemcpyHostToDevice, stream));
+    cudaEvent_t e = take_event();
+    RS_CUDA(cudaEventRecord(e, stream));
+    hfences[cur].push_back(e);
+    const CopyRec* recs = static_cast<const CopyRec*>(dev_rec[cur]);
+    const std::int32_t* pos = reinterpret_cast<const std::int32_t*>(recs + nrec_cut);
+    const int n = static_cast<int>(nrec_cut);
+    cut_kernel<<<(n + 127) / 128, 128, 0, stream>>>(recs, pos, n, static_cast<Tile*>(dev));
+    RS_CUDA(cudaGetLastError());
+    materialized = true;
+}
+
 void TileSet::upload_group(size_t gi, cudaStream_t stream) const {
+    if (gpu_cut) {
+        materialize(stream);
+        return;
+    }
     if (gi >= uploaded.size() || uploaded[gi]) return;
     for (cudaEvent_t e : wait_first) {
         RS_CUDA(cudaStreamWaitEvent(stream, e, 0));
@@ -921,6 +946,10 @@ void TileSet::upload_group(size_t gi, cudaStream_t stream) const {
 }
 
 void TileSet::flush_uploads(cudaStream_t stream) const {
+    if (gpu_cut) {
+        materialize(stream);
+        return;
+    }
     for (size_t gi = 0; gi < uploaded.size(); ++gi) upload_group(gi, stream);
 }
 

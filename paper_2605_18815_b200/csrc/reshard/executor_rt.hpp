@@ -4,12 +4,14 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "reshard/executor.hpp"
+#include "reshard/tiles.hpp"
 
 namespace reshard {
 namespace exec {
@@ -71,12 +73,8 @@ struct TileSet {
     struct Group {
         int cls, begin, count, key;
     };
-    /// a recorded 2-D copy (add), cut into tiles at finalize
-    struct Pending {
-        std::uint64_t src, dst;
-        std::int64_t rows, rb, sp, dp, kTile;
-        int key, lane;
-    };
+    /// a recorded 2-D copy (add), cut into tiles at finalize (host) or first launch (GPU)
+    using Pending = CopyRec;
     std::vector<Pending> pending;
     bool interleave = false;  // finalize: interleave lanes in proportion to their bytes
     std::vector<Tile> host;   // unused since finalize assembles in pinned staging
@@ -101,6 +99,23 @@ struct TileSet {
     mutable std::vector<cudaEvent_t> hfences[2];
     mutable std::vector<cudaEvent_t> wait_first;
     mutable std::vector<char> uploaded;
+    // GPU cut (default): the pinned slot holds the records and their per-class tile
+    // offsets; the first launch uploads them (~76 B per record instead of 40 B per
+    // tile) and cut_kernel writes the tiles on the device. RS_HOST_TILES=1 or the
+    // tile-level interleave keep the host cut.
+    bool gpu_cut = false;
+    mutable bool materialized = true;
+    size_t nrec_cut = 0;
+    void* dev_rec[2] = {nullptr, nullptr};
+    size_t rec_bytes[2] = {0, 0};
+    void materialize(cudaStream_t stream) const;
+    static bool host_tiles_forced() {
+        static const bool v = [] {
+            const char* e = std::getenv("RS_HOST_TILES");
+            return e && e[0] == '1';
+        }();
+        return v;
+    }
     /// upload every group not uploaded yet on `stream` (before a graph capture)
     void flush_uploads(cudaStream_t stream) const;
     void upload_group(size_t gi, cudaStream_t stream) const;
