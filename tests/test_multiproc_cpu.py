@@ -127,3 +127,64 @@ def test_placement_covers_d2_plan_exactly():
         plan = RoutingPlan.from_scenario(S.config2(L).reversed(), allow_oversourced=True)
         st = plan.placement(1, 0)
         assert st.local_bytes == plan.bytes_moved() - 7 * 64 + plan.bytes_retained() + 8 * 64
+
+
+def _token_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_18815_b200.api import fdx_close, fdx_listen, fdx_recv, fdx_send
+    from paper_2605_18815_b200.runtime import _split_token, job_token
+    tok = job_token("t")
+    toks = [None] * world
+    dist.all_gather_object(toks, tok)
+    ok = len(set(toks)) == 1 and tok.startswith("t-") and len(tok) > 10
+    # a payload from another job (other token) is rejected; one from this job passes
+    sock = fdx_listen(f"reshard-tok-{tok}-{rank}")
+    dist.barrier()
+    import threading
+    got = []
+
+    def receive():  # the runtime receives on a thread too (a send waits for its reader)
+        for _ in range(2):
+            fds, payload = fdx_recv(sock)
+            for fd in fds:
+                os.close(fd)
+            try:
+                got.append(_split_token(payload, tok))
+            except Exception:
+                got.append(None)
+
+    th = threading.Thread(target=receive)
+    th.start()
+    peer = (rank + 1) % world
+    r, w = os.pipe()
+    fdx_send(f"reshard-tok-{tok}-{peer}", [r], tok.encode() + b"\0" + b"hello")
+    fdx_send(f"reshard-tok-{tok}-{peer}", [w], b"t-other\0" + b"evil")
+    os.close(r)
+    os.close(w)
+    th.join()
+    fdx_close(sock)
+    ok = ok and got == [b"hello", None]
+    res = [None] * world
+    dist.all_gather_object(res, ok)
+    if rank == 0:
+        q.put(res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_job_token_guards_fd_exchange():
+    """Two concurrent jobs never share socket names or accept each other's payloads: rank 0
+    draws a per-job token that every rank uses in the socket names, and payloads carrying
+    another token are rejected."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_token_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res == [True, True]
