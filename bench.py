@@ -220,7 +220,7 @@ def run_reference(args):
            "scaling": "strong", "vs_baseline": None, "dtype": "u16/u32 payload copy", "data": "synthetic (canon payloads)",
            "impl": "reference", "verified_mismatches": bad,
            "config": {"workload": f"llama3-8b tp8->dp2xtp4 zero1, CPU sample L={args.cpu_layers}",
-                      "model": "Llama-3-8B", "parallelism": "tp8 -> dp2xtp4 + zero1"},
+                      "state": "Llama-3-8B full training state", "parallelism": "tp8 -> dp2xtp4 + zero1"},
            "cpu_baseline": cb.describe(v),
            "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     _emit(out)
@@ -507,7 +507,7 @@ def run_ours(args):
             "transport": args.transport,
             "config": {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1: one forward transition per step "
                                    f"(the way back restores the state between steps, reported as way_back)",
-                       "model": "Llama-3-8B", "layers": args.layers, "virtual_ranks": 8,
+                       "state": "Llama-3-8B full training state", "layers": args.layers, "virtual_ranks": 8,
                        "parallelism": f"tp8 -> dp2xtp4 + zero1 on {n} GPU(s)", "l2": "inputs >> L2 (no flush needed)",
                        "plan_bytes_per_transition": ab.bytes_moved()},
             "reconfig_s": round(fwd_avg / 1e3, 5),
