@@ -5,6 +5,9 @@
 #include "reshard/pool.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -446,6 +449,16 @@ D2Route d2_route(const PlanCore& P, int j, const std::vector<const stair::Triple
 
 PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const ParallelConfig& dstc,
                     const WorldMap* wmp, const Topology& topo, const PlanOptions& opts, bool allow_oversourced) {
+    // RS_TIMING=1: per-phase wall time on stderr
+    static const bool timing = std::getenv("RS_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    std::string phases;
+    auto phase = [&](const char* name) {
+        if (!timing) return;
+        const auto t = std::chrono::steady_clock::now();
+        phases += strfmt(" %s %.2f", name, std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     // CLI order: validate both configs, then the routing passes.
     ModelSpec ms;
     ms.num_layers = space.num_layers();
@@ -481,6 +494,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     for (int j = 0; j < dstc.world_size(); ++j) P.dst.ranks[static_cast<size_t>(j)].phys = P.wm.dst_phys[static_cast<size_t>(j)];
     for (int phys : P.wm.participants()) P.routes.push_back({phys, P.wm.src_rank_of(phys), P.wm.dst_rank_of(phys)});
 
+    phase("sides");
     // ---- box routing: recv cells with candidates, in the reference's pending order
     // (routing.hpp:205-222, :253-265; cells per route, tensors in id order).
     std::vector<Pending> pend;
@@ -542,6 +556,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
                 pend.push_back(std::move(o));
             }
 
+    phase("box-pending");
     // ---- resolve_peers for box pendings (routing.hpp:360-396)
     std::int64_t cursor = 0;
     P.box.reserve(pend.size());
@@ -573,6 +588,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     }
     std::sort(P.box.begin(), P.box.end(), [&](const BoxXfer& a, const BoxXfer& b) { return box_xfer_less(P, a, b); });
 
+    phase("box-resolve");
     // ---- retained boxes (routing.hpp:98 retain = R_src ∩ R_dst), same device
     std::int64_t retained = 0;
     for (const RouteInfo& r : P.routes) {
@@ -608,6 +624,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         }
     }
 
+    phase("retain");
     // ---- ZeRO optimizer routing (routing.hpp:305-336) in closed form
     std::int64_t flat_elems = 0;
     if (srcc.zero_enabled) {
@@ -638,6 +655,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         }
         for (const stair::Triple& T : P.retain_triples) retained += triple_count(T) * kOptimStateBytes;
 
+        phase("triples");
         // D2: only tensors replicated across src TP ranks can be covered by two shards.
         bool d2_possible = false;
         if (srcc.tp > 1)
@@ -690,6 +708,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
                 return a.lo < b.lo;
             });
         }
+        phase("d2");
         // transfer count + bytes: the triples' runs, minus those inside over-sourced
         // intervals, plus the D2 runs that replace them
         // (src, dst) groups of consecutive triples are independent: count them in parallel
@@ -724,6 +743,8 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         P.n_flat = total_runs - d2_regular_runs + static_cast<std::int64_t>(P.d2_runs.size());
     }
 
+    phase("count");
+    if (timing) std::fprintf(stderr, "[reshard] build_plan (ms):%s\n", phases.c_str());
     // ---- scalars (routing.hpp:341-353)
     if (P.wm.src_world_size() > 0) {
         P.has_scalars = true;
