@@ -522,9 +522,16 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
                     for (Box& cell : split_by_projection_grid(space, srcc, ts.tensor_id, rb)) {
                         std::vector<int> cands;
                         for (int k = 0; k < ns; ++k) {
+                            // containment straight on the segment's box (no Box built per test)
                             const RankGeom& K = P.src.ranks[static_cast<size_t>(k)];
                             const int sk = K.seg_of[static_cast<size_t>(t)];
-                            if (sk >= 0 && box_of(K.segs[static_cast<size_t>(sk)], nd).contains(cell)) cands.push_back(k);
+                            if (sk < 0) continue;
+                            const Seg& g = K.segs[static_cast<size_t>(sk)];
+                            bool in = true;
+                            for (int d = 0; d < nd && in; ++d)
+                                in = g.blo[d] <= cell.dims[static_cast<size_t>(d)].lo &&
+                                     cell.dims[static_cast<size_t>(d)].hi <= g.bhi[d];
+                            if (in) cands.push_back(k);
                         }
                         if (cands.empty())
                             throw ConfigError(strfmt("unreachable state: no source holds %s %s needed by device %d",
