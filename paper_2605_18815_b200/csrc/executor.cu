@@ -935,6 +935,7 @@ TileSet::~TileSet() {
         if (p) cudaFree(p);
     for (void* p : dev_rec)
         if (p) cudaFree(p);
+    if (mat_ev) cudaEventDestroy(mat_ev);
     for (auto& v : fences)
         for (cudaEvent_t e : v) cudaEventDestroy(e);
     for (cudaEvent_t e : fence_pool) cudaEventDestroy(e);
@@ -969,14 +970,26 @@ void TileSet::materialize(cudaStream_t stream) const {
     cut_kernel<<<(n + 127) / 128, 128, 0, stream>>>(recs, pos, n, static_cast<Tile*>(dev));
     RS_CUDA(cudaGetLastError());
     materialized = true;
+    if (!mat_ev) RS_CUDA(cudaEventCreateWithFlags(&mat_ev, cudaEventDisableTiming));
+    RS_CUDA(cudaEventRecord(mat_ev, stream));
+    mat_stream = stream;
+}
+
+void TileSet::order_after_upload(cudaStream_t stream) const {
+    // descriptors written on another stream: this launch follows them
+    if (mat_ev && stream != mat_stream) RS_CUDA(cudaStreamWaitEvent(stream, mat_ev, 0));
 }
 
 void TileSet::upload_group(size_t gi, cudaStream_t stream) const {
     if (gpu_cut) {
-        materialize(stream);
+        if (!materialized) materialize(stream);
+        else order_after_upload(stream);
         return;
     }
-    if (gi >= uploaded.size() || uploaded[gi]) return;
+    if (gi >= uploaded.size() || uploaded[gi]) {
+        order_after_upload(stream);
+        return;
+    }
     for (cudaEvent_t e : wait_first) {
         RS_CUDA(cudaStreamWaitEvent(stream, e, 0));
         fence_pool.push_back(e);
@@ -990,6 +1003,11 @@ void TileSet::upload_group(size_t gi, cudaStream_t stream) const {
     RS_CUDA(cudaEventRecord(e, stream));
     hfences[cur].push_back(e);
     uploaded[gi] = 1;
+    // later launches on other streams follow every upload done so far on this one
+    if (mat_stream && mat_stream != stream) order_after_upload(stream);
+    if (!mat_ev) RS_CUDA(cudaEventCreateWithFlags(&mat_ev, cudaEventDisableTiming));
+    RS_CUDA(cudaEventRecord(mat_ev, stream));
+    mat_stream = stream;
 }
 
 void TileSet::flush_uploads(cudaStream_t stream) const {

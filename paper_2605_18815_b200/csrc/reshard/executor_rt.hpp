@@ -109,6 +109,12 @@ struct TileSet {
     void* dev_rec[2] = {nullptr, nullptr};
     size_t rec_bytes[2] = {0, 0};
     void materialize(cudaStream_t stream) const;
+    // the stream the descriptors were uploaded (and cut) on, and an event after that:
+    // launches of this set on any other stream wait for it
+    mutable cudaStream_t mat_stream = nullptr;
+    mutable cudaEvent_t mat_ev = nullptr;
+    mutable bool mat_pending = false;
+    void order_after_upload(cudaStream_t stream) const;
     static bool host_tiles_forced() {
         static const bool v = [] {
             const char* e = std::getenv("RS_HOST_TILES");
