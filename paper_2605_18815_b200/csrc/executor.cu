@@ -672,7 +672,9 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         const char* v = std::getenv("RS_INTERLEAVE_TILES");
         return v && std::string(v) == "1";
     }();
-    if (interleave && !tile_level && nrec > 1) {
+    bool lanes = false;  // several destination lanes at all (N>1)
+    for (size_t i = 1; i < nrec && !lanes; ++i) lanes = pending[i].lane != pending[0].lane;
+    if (interleave && !tile_level && lanes) {
         // split large copies at tile boundaries into pieces of ~kPieceTiles tiles (the
         // pieces cut into exactly the tiles of the whole copy), so a multi-GB copy to one
         // peer does not occupy every CTA for its whole length
