@@ -678,48 +678,9 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         // split large copies at tile boundaries into pieces of ~kPieceTiles tiles (the
         // pieces cut into exactly the tiles of the whole copy), so a multi-GB copy to one
         // peer does not occupy every CTA for its whole length
-        constexpr std::int64_t kPieceTiles = 16;
         std::vector<Pending> split;
         split.reserve(nrec);
-        for (const Pending& q0 : pending) {
-            Pending q = q0;
-            if (q.rows > 1 && q.sp == q.rb && q.dp == q.rb) q.rb *= q.rows, q.rows = 1, q.sp = q.dp = q.rb;
-            const std::int64_t piece = kPieceTiles * q.kTile;
-            if (q.rows * q.rb <= piece) {
-                split.push_back(q0);
-                continue;
-            }
-            if (q.rows == 1) {
-                // contiguous: the head peel (shared misalignment) rides with the first piece,
-                // then whole multiples of kTile
-                std::int64_t head = 0;
-                if ((q.src % 16) == (q.dst % 16) && (q.src % 16) != 0)
-                    head = std::min<std::int64_t>(q.rb, 16 - static_cast<std::int64_t>(q.src % 16));
-                for (std::int64_t off = 0; off < q.rb;) {
-                    const std::int64_t len = std::min(q.rb - off, (off == 0 ? head : 0) + piece);
-                    Pending p = q;
-                    p.src = q.src + static_cast<std::uint64_t>(off);
-                    p.dst = q.dst + static_cast<std::uint64_t>(off);
-                    p.rb = len;
-                    p.sp = p.dp = len;
-                    split.push_back(p);
-                    off += len;
-                }
-            } else {
-                // strided: whole tiles' worth of rows per piece
-                const std::int64_t tiles_per_row = q.rb >= q.kTile ? (q.rb + q.kTile - 1) / q.kTile + 1 : 0;
-                const std::int64_t rows_per_tile = q.rb < q.kTile ? std::max<std::int64_t>(1, q.kTile / q.rb) : 0;
-                const std::int64_t step = q.rb < q.kTile ? rows_per_tile * kPieceTiles
-                                                         : std::max<std::int64_t>(1, kPieceTiles / tiles_per_row);
-                for (std::int64_t r = 0; r < q.rows; r += step) {
-                    Pending p = q;
-                    p.src = q.src + static_cast<std::uint64_t>(r * q.sp);
-                    p.dst = q.dst + static_cast<std::uint64_t>(r * q.dp);
-                    p.rows = std::min(step, q.rows - r);
-                    split.push_back(p);
-                }
-            }
-        }
+        for (const Pending& q0 : pending) split_rec(q0, 16, split);
         pending.swap(split);
         nrec = pending.size();
         std::vector<Pending> out;

@@ -80,5 +80,60 @@ RS_HD void cut_tiles(const CopyRec& q, Emit& emit_to) {
     }
 }
 
+/// Split a copy at tile boundaries into pieces of about `piece_tiles` tiles, appended to
+/// `out` (host). Cutting the pieces yields exactly the tiles of the whole copy, in order
+/// (pitch fields of single-row tiles aside, which the kernels ignore).
+template <class Vec>
+inline void split_rec(const CopyRec& q0, std::int64_t piece_tiles, Vec& out) {
+    CopyRec q = q0;
+    if (q.rows > 1 && q.sp == q.rb && q.dp == q.rb) q.rb *= q.rows, q.rows = 1, q.sp = q.dp = q.rb;
+    const std::int64_t piece = piece_tiles * q.kTile;
+    if (q.rows * q.rb <= piece) {
+        out.push_back(q0);
+        return;
+    }
+    if (q.rows == 1) {
+        // contiguous: the head peel (shared misalignment) rides with the first piece, then
+        // whole multiples of kTile
+        std::int64_t head = 0;
+        if ((q.src % 16) == (q.dst % 16) && (q.src % 16) != 0) {
+            head = 16 - static_cast<std::int64_t>(q.src % 16);
+            if (head > q.rb) head = q.rb;
+        }
+        for (std::int64_t off = 0; off < q.rb;) {
+            std::int64_t len = (off == 0 ? head : 0) + piece;
+            if (len > q.rb - off) len = q.rb - off;
+            CopyRec p = q;
+            p.src = q.src + static_cast<std::uint64_t>(off);
+            p.dst = q.dst + static_cast<std::uint64_t>(off);
+            p.rb = len;
+            p.sp = p.dp = len;
+            out.push_back(p);
+            off += len;
+        }
+        return;
+    }
+    // strided: whole tiles' worth of rows per piece
+    std::int64_t step;
+    if (q.rb < q.kTile) {
+        const std::int64_t rows_per_tile = q.kTile / q.rb > 1 ? q.kTile / q.rb : 1;
+        step = rows_per_tile * piece_tiles;
+    } else {
+        const std::int64_t tiles_per_row = (q.rb + q.kTile - 1) / q.kTile + 1;
+        step = piece_tiles / tiles_per_row > 1 ? piece_tiles / tiles_per_row : 1;
+    }
+    for (std::int64_t r = 0; r < q.rows;) {
+        CopyRec p = q;
+        p.src = q.src + static_cast<std::uint64_t>(r * q.sp);
+        p.dst = q.dst + static_cast<std::uint64_t>(r * q.dp);
+        p.rows = step < q.rows - r ? step : q.rows - r;
+        // a lone last row would be cut as a single-row copy (head peel); keep it with the
+        // piece before, where it is the last row group exactly as in the whole copy
+        if (q.rows - r - p.rows == 1) ++p.rows;
+        out.push_back(p);
+        r += p.rows;
+    }
+}
+
 }  // namespace exec
 }  // namespace reshard
