@@ -114,9 +114,14 @@ def test_config5_one_gpu_under_180gb_cap():
     torch.cuda.synchronize()
     bad, first = e1.verify(1, SEED)
     assert bad == 0, f"forward: {bad} mismatches, first flat index {first}"
+    from test_gpu_exec import _oracle_canon_samples  # the oracle's canon, sampled from HBM
+    checked, bad = _oracle_canon_samples(ab, e1, SEED, A.SIDE_DST)
+    assert checked > 200 and bad == 0, f"forward: {bad} of {checked} sampled elements differ from the oracle"
     e2.run()
     torch.cuda.synchronize()
     bad, first = e2.verify(1, SEED)
     assert bad == 0, f"way back: {bad} mismatches, first flat index {first}"
+    checked, bad = _oracle_canon_samples(ba, e2, SEED, A.SIDE_DST)
+    assert checked > 200 and bad == 0, f"way back: {bad} of {checked} sampled elements differ from the oracle"
     del e1, e2, arena
     gc.collect()

@@ -417,6 +417,56 @@ def test_eight_rank_placement_oversubscribed():
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+def _oracle_canon_samples(plan, ex, seed, side, per_rank=24, rng_seed=5):
+    """Independent spot check of a full-size state against the ORACLE's canon (oracle.c,
+    not the product's common.hpp / verify kernel): random elements of random segments of
+    every rank of `side`, param bytes and (inside the ZeRO shard) master / m / v, read
+    back from HBM. Returns (elements checked, mismatches)."""
+    import random
+    import struct
+    from paper_2605_18815_b200.state import model_tensors, rank_geom, segments
+    rng = random.Random(rng_seed)
+    tens = model_tensors(plan)
+    off, acc = [], 0
+    for t in tens:
+        off.append(acc)
+        n = 1
+        for d in t.shape:
+            n *= d
+        acc += n
+    nranks = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
+    checked = bad = 0
+    for r in range(nranks):
+        g = rank_geom(plan, side, r)
+        segs = segments(plan, side, r)
+        for _ in range(per_rank):
+            sg = rng.choice(segs)
+            t = tens[sg.tensor]
+            nd = len(t.shape)
+            ext = [sg.box_hi[d] - sg.box_lo[d] for d in range(nd)]
+            coord = [sg.box_lo[d] + rng.randrange(ext[d]) for d in range(nd)]
+            idx = 0  # row-major index inside the segment's box
+            gk = 0   # row-major index inside the whole tensor
+            for d in range(nd):
+                idx = idx * ext[d] + (coord[d] - sg.box_lo[d])
+                gk = gk * t.shape[d] + coord[d]
+            k = off[sg.tensor] + gk
+            w = t.dtype_bytes
+            got = ex.read(side, r, A.BUF_PARAM, sg.param_byte_off + idx * w, w)
+            want = (O.canon(seed, k, 0) & ((1 << (8 * w)) - 1)).to_bytes(w, "little")
+            checked += 1
+            bad += got != want
+            li = sg.local_lo + idx
+            lo, hi = (g.eshard_lo, g.eshard_hi) if sg.expert else (g.dshard_lo, g.dshard_hi)
+            if lo <= li < hi:
+                oi = li - lo + ((g.dshard_hi - g.dshard_lo) if sg.expert else 0)
+                c1, c2 = O.canon(seed, k, 1), O.canon(seed ^ 0x5EED, k, 1)
+                for b, val in ((A.BUF_MASTER, c1 & 0xFFFFFFFF), (A.BUF_M, c1 >> 32), (A.BUF_V, c2 & 0xFFFFFFFF)):
+                    checked += 1
+                    bad += ex.read(side, r, b, 4 * oi, 4) != struct.pack("<I", val)
+    return checked, bad
+
+
 def test_north_star_full_size_round_trip():
     """BASELINE config 2 at full size (Llama-3-8B, L=32, 112.42 GB of plan bytes; 240.9 GB
     of old + new state) on one B200 through the memory-aware arena. Size-independent
@@ -443,10 +493,14 @@ def test_north_star_full_size_round_trip():
     torch.cuda.synchronize()
     bad, first = e1.verify(1, SEED)
     assert bad == 0, f"forward: {bad} mismatches, first flat index {first}"
+    checked, bad = _oracle_canon_samples(ab, e1, SEED, A.SIDE_DST)
+    assert checked > 400 and bad == 0, f"forward: {bad} of {checked} sampled elements differ from the oracle's canon"
     e2.run()
     torch.cuda.synchronize()
     bad, first = e2.verify(1, SEED)
     assert bad == 0, f"way back: {bad} mismatches, first flat index {first}"
+    checked, bad = _oracle_canon_samples(ba, e2, SEED, A.SIDE_DST)
+    assert checked > 400 and bad == 0, f"way back: {bad} of {checked} sampled elements differ from the oracle's canon"
 
 
 @pytest.mark.parametrize("flags", [[], ["--dedup-early"]])
