@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--gpus", type=int, default=2)
+    ap.add_argument("--ctas", type=int, default=0, help="CTAs per SM of the copy kernels (0: default)")
+    ap.add_argument("--tile-bytes", type=int, default=0, help="tile size (0: default 512 KiB)")
     ap.add_argument("--same-device", action="store_true",
                     help="place every executor's GPU on device 0 (one-GPU boxes: the one-process multi-executor path)")
     args = ap.parse_args()
@@ -40,7 +42,8 @@ def main():
             if dev(a) != dev(b):
                 enable_peer_access(dev(a), dev(b))
     plan = RoutingPlan.from_scenario(S.config2(args.layers))
-    ex = [Executor(plan, n_gpus=G, gpu=g, device=dev(g)) for g in range(G)]
+    ex = [Executor(plan, n_gpus=G, gpu=g, device=dev(g), ctas_per_sm=args.ctas, tile_bytes=args.tile_bytes)
+          for g in range(G)]
     keep = []
     for side in (A.SIDE_SRC, A.SIDE_DST):
         n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
@@ -84,6 +87,7 @@ def main():
     bad = sum(e.verify(A.SIDE_DST, seed)[0] for e in ex)
     st = [e.stats() for e in ex]
     out = {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1 forward, {G} GPUs from one process (peer access)",
+           "ctas_per_sm": args.ctas, "tile_bytes": args.tile_bytes,
            "ms_per_gpu": [round(t, 3) for t in best],
            "remote_gb_per_gpu": [round(s.remote_bytes / 1e9, 3) for s in st],
            "local_gb_per_gpu": [round(s.local_bytes / 1e9, 3) for s in st],
