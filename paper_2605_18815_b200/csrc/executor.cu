@@ -1213,8 +1213,15 @@ void Executor::prepare(bool staged) {
     // (then latency-bound: smaller tiles, down to one 32 KiB bulk stage, spread it out)
     std::int64_t kTile = cfg_.tile_bytes > 0 ? cfg_.tile_bytes : (512 << 10);
     std::int64_t here = 0;  // bytes this GPU moves
+    bool pushes = false;    // any of them bound for a peer GPU
     for (const CopyOp& op : ops)
-        if (bufs_[0][static_cast<size_t>(op.src_side_rank)].gpu == cfg_.gpu) here += op.rows * op.row_bytes;
+        if (bufs_[0][static_cast<size_t>(op.src_side_rank)].gpu == cfg_.gpu) {
+            here += op.rows * op.row_bytes;
+            pushes = pushes || bufs_[1][static_cast<size_t>(op.dst_rank)].gpu != cfg_.gpu;
+        }
+    // peer pushes: 256 KiB tiles spread the lanes finer (measured +0.6 % of NVLink rate at
+    // N=2, tools/runs/r02_push_sweep.sh); local copies keep 512 KiB
+    if (cfg_.tile_bytes <= 0 && pushes) kTile = 256 << 10;
     if (cfg_.tile_bytes <= 0) {
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cfg_.device);
