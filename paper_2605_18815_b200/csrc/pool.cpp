@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <exception>
 #include <mutex>
@@ -28,6 +29,7 @@ public:
             std::lock_guard<std::mutex> lk(mu_);
             stop_ = true;
             ++gen_;
+            gen_atomic_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto& w : workers_) w.join();
@@ -49,6 +51,7 @@ public:
             pending_ = n;
             error_ = nullptr;
             ++gen_;
+            gen_atomic_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         work();
@@ -81,6 +84,13 @@ private:
     void loop() {
         std::uint64_t seen = 0;
         for (;;) {
+            // a planner / descriptor build issues several short loops back to back: spin
+            // briefly on the generation counter before sleeping, so the next loop does not
+            // pay a condition-variable wake-up per worker
+            const auto t0 = std::chrono::steady_clock::now();
+            while (gen_atomic_.load(std::memory_order_acquire) == seen &&
+                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(300))
+                std::this_thread::yield();
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return gen_ != seen; });
@@ -100,6 +110,7 @@ private:
     std::size_t n_ = 0, pending_ = 0;
     std::atomic<std::size_t> next_{0};
     std::uint64_t gen_ = 0;
+    std::atomic<std::uint64_t> gen_atomic_{0};  // gen_, readable without the lock (spin)
     bool stop_ = false;
     std::exception_ptr error_;
 };
