@@ -89,7 +89,7 @@ private:
             // pay a condition-variable wake-up per worker
             const auto t0 = std::chrono::steady_clock::now();
             while (gen_atomic_.load(std::memory_order_acquire) == seen &&
-                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(300))
+                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100))
                 std::this_thread::yield();
             {
                 std::unique_lock<std::mutex> lk(mu_);
