@@ -117,6 +117,65 @@ bool make_triple(const ModelSpace& space, int t, const RankGeom& k, const RankGe
     return true;
 }
 
+/// Stairs of every (rank, tensor) of one side, built once per plan (a triple needs three
+/// of them; the (src, dst, tensor) loop would otherwise rebuild each one many times)
+struct StairTable {
+    std::vector<std::vector<char>> ok;            // [rank][tensor]
+    std::vector<std::vector<stair::Stair>> st;    // [rank][tensor]
+};
+
+StairTable stair_table(const ModelSpace& space, const Side& side) {
+    StairTable T;
+    const int nt = static_cast<int>(space.entries().size());
+    T.ok.assign(side.ranks.size(), std::vector<char>(static_cast<size_t>(nt), 0));
+    T.st.assign(side.ranks.size(), std::vector<stair::Stair>(static_cast<size_t>(nt)));
+    for (size_t r = 0; r < side.ranks.size(); ++r) {
+        const RankGeom& g = side.ranks[r];
+        for (int t = 0; t < nt; ++t) {
+            const int sg = g.seg_of[static_cast<size_t>(t)];
+            if (sg < 0) continue;
+            const Seg& S = g.segs[static_cast<size_t>(sg)];
+            T.ok[r][static_cast<size_t>(t)] =
+                make_stair(space.entries()[static_cast<size_t>(t)].spec, S, shard_of(g, S), &T.st[r][static_cast<size_t>(t)]);
+        }
+    }
+    return T;
+}
+
+/// make_triple from precomputed stairs (same result)
+bool make_triple_cached(const ModelSpace& space, int t, const StairTable& src, const StairTable& dst, int k, int j,
+                        int own, const std::vector<stair::TensorView>& views, stair::Triple* T) {
+    const size_t tt = static_cast<size_t>(t);
+    if (!src.ok[static_cast<size_t>(k)][tt] || !dst.ok[static_cast<size_t>(j)][tt]) return false;
+    (void)space;
+    stair::Triple X{};
+    X.K = src.st[static_cast<size_t>(k)][tt];
+    X.J = dst.st[static_cast<size_t>(j)][tt];
+    X.t = views[tt];
+    std::int64_t n = 1;
+    for (int i = 0; i < X.t.np; ++i) {
+        X.plo[i] = std::max(X.K.plo[i], X.J.plo[i]);
+        X.phi[i] = std::min(X.K.phi[i], X.J.phi[i]);
+        if (X.plo[i] >= X.phi[i]) return false;
+        n *= X.phi[i] - X.plo[i];
+    }
+    X.rlo = std::max(X.K.rlo, X.J.rlo);
+    X.rhi = std::min(X.K.rhi, X.J.rhi);
+    if (X.rlo >= X.rhi) return false;
+    if (std::max(X.K.clo, X.J.clo) >= std::min(X.K.chi, X.J.chi)) return false;
+    X.nrows = n * (X.rhi - X.rlo);
+    X.has_i = 0;
+    if (own >= 0 && src.ok[static_cast<size_t>(own)][tt]) {
+        X.I = src.st[static_cast<size_t>(own)][tt];
+        X.has_i = 1;
+    }
+    X.src = k;
+    X.dst = j;
+    X.tensor = t;
+    *T = X;
+    return true;
+}
+
 }  // namespace
 
 void append_runs(const stair::Triple& T, std::vector<FlatXfer>& out) {
@@ -637,16 +696,23 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     if (srcc.zero_enabled) {
         const int ndst = dstc.world_size();
         std::vector<std::vector<const stair::Triple*>> by_dst(static_cast<size_t>(ndst));
+        StairTable src_st, dst_st;
+        pool::run(2, [&](size_t w) {
+            if (w == 0) src_st = stair_table(space, P.src);
+            else dst_st = stair_table(space, P.dst);
+        });
+        std::vector<stair::TensorView> views;
+        views.reserve(static_cast<size_t>(nt));
+        for (int t = 0; t < nt; ++t) views.push_back(view_of(space.entries()[static_cast<size_t>(t)]));
         std::vector<std::vector<stair::Triple>> per_pair(static_cast<size_t>(ns) * ndst);
         parallel_for(per_pair.size(), [&](size_t kj) {
             const int k = static_cast<int>(kj) / ndst, j = static_cast<int>(kj) % ndst;
             const RankGeom& J = P.dst.ranks[static_cast<size_t>(j)];
             const int own = P.wm.src_rank_of(J.phys);
             if (own == k) return;  // R_j ∩ S_own = ∅
-            const RankGeom* O = own >= 0 ? &P.src.ranks[static_cast<size_t>(own)] : nullptr;
             for (int t = 0; t < nt; ++t) {
                 stair::Triple T;
-                if (make_triple(space, t, P.src.ranks[static_cast<size_t>(k)], J, O, &T)) per_pair[kj].push_back(T);
+                if (make_triple_cached(space, t, src_st, dst_st, k, j, own, views, &T)) per_pair[kj].push_back(T);
             }
         });
         for (const auto& v : per_pair) P.triples.insert(P.triples.end(), v.begin(), v.end());
