@@ -148,22 +148,28 @@ bool make_triple_cached(const ModelSpace& space, int t, const StairTable& src, c
     const size_t tt = static_cast<size_t>(t);
     if (!src.ok[static_cast<size_t>(k)][tt] || !dst.ok[static_cast<size_t>(j)][tt]) return false;
     (void)space;
-    stair::Triple X{};
-    X.K = src.st[static_cast<size_t>(k)][tt];
-    X.J = dst.st[static_cast<size_t>(j)][tt];
-    X.t = views[tt];
-    std::int64_t n = 1;
-    for (int i = 0; i < X.t.np; ++i) {
-        X.plo[i] = std::max(X.K.plo[i], X.J.plo[i]);
-        X.phi[i] = std::min(X.K.phi[i], X.J.phi[i]);
-        if (X.plo[i] >= X.phi[i]) return false;
-        n *= X.phi[i] - X.plo[i];
+    // reject on the references first: most (src, dst, tensor) combinations do not meet
+    const stair::Stair& K = src.st[static_cast<size_t>(k)][tt];
+    const stair::Stair& J = dst.st[static_cast<size_t>(j)][tt];
+    const stair::TensorView& V = views[tt];
+    std::int64_t plo[2] = {0, 0}, phi[2] = {0, 0}, n = 1;
+    for (int i = 0; i < V.np; ++i) {
+        plo[i] = std::max(K.plo[i], J.plo[i]);
+        phi[i] = std::min(K.phi[i], J.phi[i]);
+        if (plo[i] >= phi[i]) return false;
+        n *= phi[i] - plo[i];
     }
-    X.rlo = std::max(X.K.rlo, X.J.rlo);
-    X.rhi = std::min(X.K.rhi, X.J.rhi);
-    if (X.rlo >= X.rhi) return false;
-    if (std::max(X.K.clo, X.J.clo) >= std::min(X.K.chi, X.J.chi)) return false;
-    X.nrows = n * (X.rhi - X.rlo);
+    const std::int64_t rlo = std::max(K.rlo, J.rlo), rhi = std::min(K.rhi, J.rhi);
+    if (rlo >= rhi) return false;
+    if (std::max(K.clo, J.clo) >= std::min(K.chi, J.chi)) return false;
+    stair::Triple X{};
+    X.K = K;
+    X.J = J;
+    X.t = V;
+    for (int i = 0; i < 2; ++i) X.plo[i] = plo[i], X.phi[i] = phi[i];
+    X.rlo = rlo;
+    X.rhi = rhi;
+    X.nrows = n * (rhi - rlo);
     X.has_i = 0;
     if (own >= 0 && src.ok[static_cast<size_t>(own)][tt]) {
         X.I = src.st[static_cast<size_t>(own)][tt];
