@@ -237,10 +237,13 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     n = args.gpus
+    shared = False
     if world > 1:
         assert world == n, f"--gpus {n} but WORLD_SIZE {world}"
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU: NCCL plumbing; more ranks than GPUs (a placement check, not a
+        # measurement): ranks share devices over gloo (runtime.init_dist)
+        from paper_2605_18815_b200.runtime import init_dist
+        rank, world, local, shared = init_dist()
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -531,6 +534,8 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         # copy launches of both transitions per step, plus the two device barriers at N>1
+        if shared:
+            out["note"] = "more ranks than GPUs: ranks share devices (gloo plumbing); a placement check, not a measurement"
         out["gpu_launches"] = (st_f.launches + bwd.ex.stats().launches + (2 if world > 1 else 0)) * args.steps
         if arena is not None:
             a = arena.stats()
