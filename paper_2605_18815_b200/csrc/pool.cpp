@@ -6,6 +6,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -16,6 +17,16 @@ namespace pool {
 namespace {
 
 thread_local bool t_in_pool = false;
+
+/// one parallel loop: workers claim indices of THIS loop only, so a worker still leaving
+/// the previous loop can never take (or count) an index of the next one
+struct Job {
+    const std::function<void(std::size_t)>* fn = nullptr;
+    std::size_t n = 0;
+    std::atomic<std::size_t> next{0};
+    std::size_t pending = 0;  // guarded by Pool::mu_
+    std::exception_ptr error;  // guarded by Pool::mu_
+};
 
 class Pool {
 public:
@@ -43,40 +54,40 @@ public:
             return;
         }
         std::lock_guard<std::mutex> serial(run_mu_);  // one parallel loop at a time
+        auto job = std::make_shared<Job>();
+        job->fn = &fn;
+        job->n = n;
+        job->pending = n;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            fn_ = &fn;
-            n_ = n;
-            next_.store(0);
-            pending_ = n;
-            error_ = nullptr;
+            job_ = job;
             ++gen_;
             gen_atomic_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
-        work();
+        work(*job);
         std::unique_lock<std::mutex> lk(mu_);
-        done_cv_.wait(lk, [this] { return pending_ == 0; });
-        fn_ = nullptr;
-        if (error_) std::rethrow_exception(error_);
+        done_cv_.wait(lk, [&] { return job->pending == 0; });
+        job_.reset();
+        if (job->error) std::rethrow_exception(job->error);
     }
 
 private:
-    void work() {
+    void work(Job& j) {
         const bool was = t_in_pool;
         t_in_pool = true;
         for (;;) {
-            const std::size_t t = next_.fetch_add(1);
-            if (t >= n_) break;
+            const std::size_t t = j.next.fetch_add(1);
+            if (t >= j.n) break;
             std::exception_ptr e;
             try {
-                (*fn_)(t);
+                (*j.fn)(t);
             } catch (...) {
                 e = std::current_exception();
             }
             std::lock_guard<std::mutex> lk(mu_);
-            if (e && !error_) error_ = e;
-            if (--pending_ == 0) done_cv_.notify_all();
+            if (e && !j.error) j.error = e;
+            if (--j.pending == 0) done_cv_.notify_all();
         }
         t_in_pool = was;
     }
@@ -91,14 +102,15 @@ private:
             while (gen_atomic_.load(std::memory_order_acquire) == seen &&
                    std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100))
                 std::this_thread::yield();
+            std::shared_ptr<Job> j;
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return gen_ != seen; });
                 seen = gen_;
                 if (stop_) return;
-                if (!fn_) continue;
+                j = job_;
             }
-            work();
+            if (j) work(*j);
         }
     }
 
@@ -106,13 +118,10 @@ private:
     std::vector<std::thread> workers_;
     std::mutex mu_, run_mu_;
     std::condition_variable cv_, done_cv_;
-    const std::function<void(std::size_t)>* fn_ = nullptr;
-    std::size_t n_ = 0, pending_ = 0;
-    std::atomic<std::size_t> next_{0};
+    std::shared_ptr<Job> job_;  // the loop in progress (guarded by mu_)
     std::uint64_t gen_ = 0;
     std::atomic<std::uint64_t> gen_atomic_{0};  // gen_, readable without the lock (spin)
     bool stop_ = false;
-    std::exception_ptr error_;
 };
 
 Pool& instance() {

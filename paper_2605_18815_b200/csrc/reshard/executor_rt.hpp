@@ -77,7 +77,6 @@ struct TileSet {
     using Pending = CopyRec;
     std::vector<Pending> pending;
     bool interleave = false;  // finalize: interleave lanes in proportion to their bytes
-    std::vector<Tile> host;   // unused since finalize assembles in pinned staging
     size_t ntiles = 0;
     std::vector<Group> groups;
     void* dev = nullptr;                    // descriptors of the last finalize (dev_buf[cur])
