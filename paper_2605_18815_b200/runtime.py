@@ -272,10 +272,10 @@ def exchange_arena(arena, rank: int, world: int, tag: str) -> None:
 
 
 def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: int, device: int, cap_bytes: int = 0,
-                 tag: str = "0", chunk_bytes: int = 0):
+                 tag: str = "0", chunk_bytes: int = 0, level: Optional[int] = None):
     """Memory-aware arena over `world` GPUs: every GPU plans the buffers it hosts with the
     same schedule level (layer bands x concurrency groups: the cheapest level that fits
-    every GPU's cap, max over ranks),
+    every GPU's cap, max over ranks; `level` forces one ladder level, which must fit),
     then the buffers are shared (exchange_arena). Returns (arena, global stage cuts)."""
     import torch
     import torch.distributed as dist
@@ -299,7 +299,12 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
         raise A.ReshardError(A.RS_ERR_BUDGET, f"infeasible budget on some GPU (this GPU needs >= {min(need) / 1e9:.2f} GB, "
                                               f"cap {cap_bytes / 1e9:.2f} GB)")
     t = est.tolist()
-    lv = min(fits, key=lambda i: (t[i], i))
+    if level is not None:
+        if level not in fits:
+            raise A.ReshardError(A.RS_ERR_BUDGET, f"schedule level {level} does not fit the cap on every GPU")
+        lv = level
+    else:
+        lv = min(fits, key=lambda i: (t[i], i))
     bands, k = memory_schedule_level(ab, lv, world)
     arena = Arena.multi(ab, ba, world, rank, device, cap_bytes=cap_bytes, chunk_bytes=chunk_bytes, groups=k, bands=bands)
     exchange_arena(arena, rank, world, tag)

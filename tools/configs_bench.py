@@ -48,14 +48,15 @@ def scenario(cfg: int, layers: int):
     raise SystemExit(f"unknown config {cfg}")
 
 
-def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False):
+def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False, level=None):
     plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
     arena = None
     if arena_cap:
         # old + new state do not fit: the memory-aware arena under a per-GPU cap, stages
         # with a barrier between them (runtime.run_stages)
         arena, cuts = shared_arena(plan, None, rank, world, local, cap_bytes=int(arena_cap * 1e9),
-                                   tag=f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}")
+                                   tag=f"{os.environ.get('MASTER_PORT', '0')}-{sc.name}-{level}-{int(host_barriers)}",
+                                   level=level)
         tr = Transition(plan, world, rank, local, alloc=False)
         arena.bind(tr.ex, None, cuts)
         tr.ex.prepare()
@@ -112,9 +113,36 @@ def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False):
         out["arena"] = {"cap_gb": arena_cap, "physical_gb": round(st.physical_bytes / 1e9, 2),
                         "stage_barriers": "host" if host_barriers else "device",
                         "old_gb": round(st.a_bytes / 1e9, 2), "new_gb": round(st.b_bytes / 1e9, 2),
-                        "aliased_gb": round(st.aliased_bytes / 1e9, 2), "bands": st.bands, "stages": ex.num_stages()}
+                        "aliased_gb": round(st.aliased_bytes / 1e9, 2), "bands": st.bands, "stages": ex.num_stages(),
+                        "level": level if level is not None else "fastest fitting"}
     del tr, ex, arena
     torch.cuda.synchronize()
+    return out
+
+
+def barrier_probe(rank, world, local, n):
+    """SynchronizeAll latency: n device barriers enqueued back to back on one stream, timed
+    with events (max over ranks); the per-barrier cost a memory-aware stage boundary adds."""
+    dbar = device_barrier(rank, world, local)
+    stream = torch.cuda.Stream()
+    for _ in range(10):
+        dbar(stream.cuda_stream)
+    torch.cuda.synchronize()
+    out = {"what": "device barrier (SynchronizeAll) latency", "n_gpus": world, "barriers": n}
+    for label, k in (("per_barrier_us", n),):
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            dbar(stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e3 / k], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out[label] = round(t.item(), 2)
+    out["timed_out"] = dbar.timed_out()
     return out
 
 
@@ -127,15 +155,27 @@ def main():
                     help="GB per GPU: run under the memory-aware arena (old + new need not fit)")
     ap.add_argument("--host-barriers", action="store_true",
                     help="arena stages separated by host synchronize + dist.barrier instead of the device barrier")
+    ap.add_argument("--level", type=int, action="append",
+                    help="with --arena-cap: force this schedule ladder level (repeatable); default: the fastest that fits")
+    ap.add_argument("--both-barriers", action="store_true", help="run every arena case with device and host barriers")
+    ap.add_argument("--barrier-probe", type=int, default=0,
+                    help="time N back-to-back device barriers (SynchronizeAll latency) and exit")
     args = ap.parse_args()
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    for cfg in args.config or [1, 4]:
-        res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap, args.host_barriers)
+    if args.barrier_probe:
+        res = barrier_probe(rank, world, local, args.barrier_probe)
         if rank == 0:
             print(json.dumps(res), flush=True)
+    else:
+        for cfg in args.config or [1, 4]:
+            for lv in (args.level or [None]):
+                for hb in ((False, True) if args.both_barriers else (args.host_barriers,)):
+                    res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap, hb, lv)
+                    if rank == 0:
+                        print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
