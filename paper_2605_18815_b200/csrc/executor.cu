@@ -733,10 +733,7 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
     size_t total = 0;
     if (gpu_cut) {
         rc.assign(nrec, {0, 0, 0, 0, 0});
-        pool::parallel_for(nrec, [&](size_t i) {
-            auto count = [&](int b, const Tile&) { ++rc[i][static_cast<size_t>(b % 5)]; };
-            cut_tiles(pending[i], count);
-        });
+        pool::parallel_for(nrec, [&](size_t i) { count_tiles(pending[i], rc[i].data()); });
         for (size_t i = 0; i < nrec; ++i)
             for (int c = 0; c < 5; ++c) bucket_n[static_cast<size_t>(pending[i].key) * 5 + c] += static_cast<size_t>(rc[i][c]);
     } else {

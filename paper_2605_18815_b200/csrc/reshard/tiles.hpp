@@ -80,6 +80,74 @@ RS_HD void cut_tiles(const CopyRec& q, Emit& emit_to) {
     }
 }
 
+/// Tiles per alignment class (16/8/4/2/1 B) that cut_tiles emits for the record, added to
+/// n[5], in closed form: O(1) per row of a long-row copy and O(1) for a short-row copy
+/// (per-row only when every tile holds one row). Same result as counting cut_tiles'
+/// emissions (tests/cpp/tiles_check.cpp); a kTile that is not a multiple of 16 is counted
+/// by cutting.
+template <class Int>
+RS_HD void count_tiles(const CopyRec& q, Int n[5]) {
+    std::int64_t rows = q.rows, rb = q.rb;
+    const std::int64_t sp = q.sp, dp = q.dp, kTile = q.kTile;
+    if (kTile % 16) {  // a caller-chosen tile size: count the emissions
+        auto c = [&](int b, const Tile&) { ++n[b % 5]; };
+        cut_tiles(q, c);
+        return;
+    }
+    if (rows > 1 && sp == rb && dp == rb) {
+        rb *= rows;
+        rows = 1;
+    }
+    auto cls = [](std::uint64_t a) { return class_index(align_class(a)); };
+    if (rows == 1 || rb >= kTile) {
+        for (std::int64_t r = 0; r < rows; ++r) {
+            const std::uint64_t s = q.src + static_cast<std::uint64_t>(r * sp), d = q.dst + static_cast<std::uint64_t>(r * dp);
+            std::int64_t left = rb;
+            if ((s % 16) == (d % 16) && (s % 16) != 0) {  // head peel, then the body is aligned
+                const std::int64_t head = left < 16 - static_cast<std::int64_t>(s % 16) ? left : 16 - static_cast<std::int64_t>(s % 16);
+                ++n[cls(s | d | static_cast<std::uint64_t>(head))];
+                left -= head;
+            }
+            if (left <= 0) continue;
+            if ((s % 16) == (d % 16)) {  // aligned body: full tiles, a 16-B multiple, a tail
+                n[0] += static_cast<Int>(left / kTile);
+                const std::int64_t rem = left % kTile;
+                if (rem > 16) {
+                    ++n[0];
+                    if (rem % 16) ++n[cls(static_cast<std::uint64_t>(rem % 16))];
+                } else if (rem > 0) {
+                    ++n[cls(static_cast<std::uint64_t>(rem))];
+                }
+            } else {  // different misalignment: kTile pieces keep s, d mod 16
+                const std::uint64_t low = (s | d) & 15;
+                n[cls(low)] += static_cast<Int>(left / kTile);
+                const std::int64_t rem = left % kTile;
+                if (rem > 0) ++n[cls(low | static_cast<std::uint64_t>(rem))];
+            }
+        }
+    } else {
+        const std::int64_t per = kTile / rb > 1 ? kTile / rb : 1;
+        if (per == 1) {  // one row per tile: each row's own alignment
+            for (std::int64_t r = 0; r < rows; ++r)
+                ++n[cls((q.src + static_cast<std::uint64_t>(r * sp)) | (q.dst + static_cast<std::uint64_t>(r * dp)) |
+                        static_cast<std::uint64_t>(rb))];
+            return;
+        }
+        // multi-row tiles: the pitches in the alignment make the class row-independent
+        const std::int64_t full = rows / per, last = rows % per;
+        const std::uint64_t a = q.src | q.dst | static_cast<std::uint64_t>(rb) | static_cast<std::uint64_t>(sp) |
+                                static_cast<std::uint64_t>(dp);
+        n[cls(a)] += static_cast<Int>(full);
+        if (last > 1) {
+            ++n[cls(a)];
+        } else if (last == 1) {
+            const std::int64_t r = rows - 1;
+            ++n[cls((q.src + static_cast<std::uint64_t>(r * sp)) | (q.dst + static_cast<std::uint64_t>(r * dp)) |
+                    static_cast<std::uint64_t>(rb))];
+        }
+    }
+}
+
 /// Split a copy at tile boundaries into pieces of about `piece_tiles` tiles, appended to
 /// `out` (host). Cutting the pieces yields exactly the tiles of the whole copy, in order
 /// (pitch fields of single-row tiles aside, which the kernels ignore).

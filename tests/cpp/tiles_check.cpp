@@ -66,6 +66,15 @@ int main() {
             if (a % static_cast<std::uint64_t>(V)) return std::printf("FAIL alignment class (case %d)\n", it), 1;
             if (x.bucket / 5 != q.key) return std::printf("FAIL key (case %d)\n", it), 1;
         }
+        // the closed-form count equals the cutter's emissions per class
+        std::int64_t counted[5] = {0, 0, 0, 0, 0}, emitted[5] = {0, 0, 0, 0, 0};
+        count_tiles(q, counted);
+        for (const T& x : whole) ++emitted[x.bucket % 5];
+        for (int c = 0; c < 5; ++c)
+            if (counted[c] != emitted[c])
+                return std::printf("FAIL count_tiles class %d: %lld != %lld (case %d: rows %lld rb %lld sp %lld dp %lld kTile %lld src%%16 %d dst%%16 %d)\n",
+                                   c, (long long)counted[c], (long long)emitted[c], it, (long long)q.rows, (long long)q.rb,
+                                   (long long)q.sp, (long long)q.dp, (long long)q.kTile, (int)(q.src % 16), (int)(q.dst % 16)), 1;
         if (bytes != q.rows * q.rb) return std::printf("FAIL coverage %lld != %lld (case %d)\n", (long long)bytes, (long long)(q.rows * q.rb), it), 1;
         // split pieces cut into the same tiles
         std::vector<CopyRec> pieces;
