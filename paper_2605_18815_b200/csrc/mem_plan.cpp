@@ -6,6 +6,7 @@
 #include <map>
 
 #include "reshard/arena.hpp"
+#include "reshard/pool.hpp"
 
 namespace reshard {
 namespace mem {
@@ -475,9 +476,23 @@ std::vector<std::pair<std::int64_t, double>> schedule_costs(const core::PlanCore
     const std::vector<exec::CopyOp> ops_ab = exec::build_ops(ab);
     const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
     std::vector<std::pair<std::int64_t, double>> out;
+    const int G = std::max(1, n_gpus);
     for (const ScheduleLevel& L : schedule_levels(ab, n_gpus)) {
-        const MemoryPlan mp = plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, gpu, L.groups, L.bands);
-        out.push_back({mp.stats.physical_bytes, estimate_seconds(mp, ab, ba, ops_ab, ops_ba, n_gpus)});
+        // the run barriers wherever ANY GPU's aliasing needs a cut (runtime.global_stage_cuts),
+        // so the level is modeled with the union of every GPU's cuts (each GPU plans only
+        // the chunks it hosts; the stage order is common)
+        std::vector<MemoryPlan> mps(static_cast<size_t>(G));
+        pool::parallel_for(mps.size(), [&](size_t g) {
+            mps[g] = plan_memory_ops(ab, ba, ops_ab, ops_ba, C, with_grads, n_gpus, static_cast<int>(g), L.groups, L.bands);
+        });
+        MemoryPlan& mp = mps[static_cast<size_t>(gpu)];
+        const std::int64_t physical = mp.stats.physical_bytes;
+        for (int d = 0; d < 2; ++d)
+            for (const MemoryPlan& o : mps) {
+                if (o.cut[d].size() > mp.cut[d].size()) mp.cut[d].resize(o.cut[d].size(), 0);
+                for (size_t s = 0; s < o.cut[d].size(); ++s) mp.cut[d][s] = mp.cut[d][s] || o.cut[d][s];
+            }
+        out.push_back({physical, estimate_seconds(mp, ab, ba, ops_ab, ops_ba, n_gpus)});
     }
     return out;
 }

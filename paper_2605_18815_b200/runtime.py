@@ -284,9 +284,9 @@ def shared_arena(ab: RoutingPlan, ba: Optional[RoutingPlan], rank: int, world: i
     if cap_bytes <= 0:
         cap_bytes = torch.cuda.mem_get_info(device)[0] - (1 << 30)
     # every rank marks the ladder levels that fit its cap and models each level's time
-    # (stage groups in sequence, each bound by its busiest GPU's NVLink or HBM); the group
-    # takes the fastest level feasible on all GPUs (max over ranks of the modeled time:
-    # each rank models with its own stage cuts, the union of cuts only adds groups)
+    # (stage groups in sequence, each bound by its busiest GPU's NVLink or HBM, with the
+    # union of every GPU's stage cuts: the same on every rank); the group takes the
+    # fastest level feasible on all GPUs
     costs = memory_schedule_costs(ab, ba, world, rank, chunk_bytes)
     need = [b for b, _ in costs]
     ok = torch.tensor([1 if x <= cap_bytes else 0 for x in need], dtype=torch.int32, device="cuda")

@@ -141,3 +141,18 @@ def test_band_interleaved_level_is_the_fastest_that_fits():
     for g in range(4):
         st, viol, _, _ = memory_plan(ab, None, n_gpus=4, gpu=g, groups=-2, bands=bands)
         assert viol == 0 and st.physical_bytes <= 180e9
+
+
+def test_time_model_uses_the_union_of_every_gpus_cuts():
+    """The run barriers wherever any GPU's aliasing needs a cut, so every GPU models a level
+    with the same (union) stage structure: identical modeled times on every GPU, and a
+    level's time never drops below its one-stage time. Calibration on B200s (N=4 north
+    star, profiles/r02_stage_levels_n4.jsonl): 8x8 modeled 62.6 ms / measured 62.3, 32x8
+    53.3 / 53.5, 16x16 67.6 / 65.6."""
+    from paper_2605_18815_b200.api import memory_schedule_costs
+    ab = RoutingPlan.from_scenario(S.config2(32))
+    costs = [memory_schedule_costs(ab, None, 4, g) for g in range(4)]
+    for i in range(len(costs[0])):
+        ts = {round(costs[g][i][1], 12) for g in range(4)}
+        assert len(ts) == 1, (i, ts)
+        assert costs[0][i][1] >= costs[0][0][1] - 1e-9
