@@ -707,6 +707,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
             if (w == 0) src_st = stair_table(space, P.src);
             else dst_st = stair_table(space, P.dst);
         });
+        phase("stairs");
         std::vector<stair::TensorView> views;
         views.reserve(static_cast<size_t>(nt));
         for (int t = 0; t < nt; ++t) views.push_back(view_of(space.entries()[static_cast<size_t>(t)]));
@@ -723,6 +724,7 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         });
         for (const auto& v : per_pair) P.triples.insert(P.triples.end(), v.begin(), v.end());
         for (const stair::Triple& T : P.triples) by_dst[static_cast<size_t>(T.dst)].push_back(&T);
+        phase("triples-pairs");
         for (const RouteInfo& r : P.routes) {
             if (r.src_rank < 0 || r.dst_rank < 0) continue;
             for (int t = 0; t < nt; ++t) {
