@@ -1185,6 +1185,7 @@ void Executor::set_multicast(int id, void* mc_va) {
 }
 
 void Executor::prepare(bool staged) {
+    const pool::Warm warm;  // op build, tile counts and interleave: short loops back to back
     const auto t_begin = std::chrono::steady_clock::now();
     RS_CUDA(cudaSetDevice(cfg_.device));
     const char* sr = std::getenv("RS_SPLIT_REMOTE");

@@ -477,6 +477,7 @@ std::vector<std::pair<std::int64_t, double>> schedule_costs(const core::PlanCore
     const std::vector<exec::CopyOp> ops_ba = ba ? exec::build_ops(*ba) : std::vector<exec::CopyOp>{};
     std::vector<std::pair<std::int64_t, double>> out;
     const int G = std::max(1, n_gpus);
+    const pool::Warm warm;
     for (const ScheduleLevel& L : schedule_levels(ab, n_gpus)) {
         // the run barriers wherever ANY GPU's aliasing needs a cut (runtime.global_stage_cuts),
         // so the level is modeled with the union of every GPU's cuts (each GPU plans only

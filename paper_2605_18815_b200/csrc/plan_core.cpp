@@ -514,6 +514,7 @@ D2Route d2_route(const PlanCore& P, int j, const std::vector<const stair::Triple
 
 PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const ParallelConfig& dstc,
                     const WorldMap* wmp, const Topology& topo, const PlanOptions& opts, bool allow_oversourced) {
+    const pool::Warm warm;  // several short parallel loops follow: keep the workers hot
     // RS_TIMING=1: per-phase wall time on stderr
     static const bool timing = std::getenv("RS_TIMING") != nullptr;
     auto t_last = std::chrono::steady_clock::now();

@@ -17,6 +17,7 @@ namespace pool {
 namespace {
 
 thread_local bool t_in_pool = false;
+std::atomic<int> g_warm{0};  // live Warm guards
 
 /// one parallel loop: workers claim indices of THIS loop only, so a worker still leaving
 /// the previous loop can never take (or count) an index of the next one
@@ -100,7 +101,8 @@ private:
             // pay a condition-variable wake-up per worker
             const auto t0 = std::chrono::steady_clock::now();
             while (gen_atomic_.load(std::memory_order_acquire) == seen &&
-                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100))
+                   (g_warm.load(std::memory_order_relaxed) > 0 ||
+                    std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100)))
                 std::this_thread::yield();
             std::shared_ptr<Job> j;
             {
@@ -132,6 +134,13 @@ Pool& instance() {
 }  // namespace
 
 std::size_t size() { return instance().size(); }
+
+Warm::Warm() {
+    instance();  // the workers exist before the first loop
+    g_warm.fetch_add(1, std::memory_order_relaxed);
+}
+
+Warm::~Warm() { g_warm.fetch_sub(1, std::memory_order_relaxed); }
 
 void run(std::size_t n, const std::function<void(std::size_t)>& fn) { instance().run(n, fn); }
 

@@ -16,6 +16,19 @@ std::size_t size();
 /// done; the first exception thrown by any fn is rethrown here. Nested calls run inline.
 void run(std::size_t n, const std::function<void(std::size_t)>& fn);
 
+/// While a Warm guard lives (any thread), idle workers spin (yielding) between loops
+/// instead of going to sleep: a plan or a descriptor build runs several short parallel
+/// loops separated by serial work, and a condition-variable wake-up of every worker per
+/// loop costs about as much as the loops. Workers sleep again ~100 us after the last
+/// guard ends.
+class Warm {
+public:
+    Warm();
+    ~Warm();
+    Warm(const Warm&) = delete;
+    Warm& operator=(const Warm&) = delete;
+};
+
 /// fn(i) for every i in [0, n), split into contiguous slices over the pool
 template <class F>
 void parallel_for(std::size_t n, F&& fn) {

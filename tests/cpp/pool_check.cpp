@@ -29,6 +29,16 @@ int main() {
                 return 1;
             }
     }
+    {  // the same under a Warm guard (workers spin between loops)
+        const pool::Warm warm;
+        for (int it = 0; it < 5000; ++it) {
+            const std::size_t n = 1 + static_cast<std::size_t>((it * 40503u) % 61);
+            for (std::size_t i = 0; i < n; ++i) hits[i].store(0);
+            pool::run(n, [&](std::size_t t) { hits[t].fetch_add(1); });
+            for (std::size_t i = 0; i < n; ++i)
+                if (hits[i].load() != 1) return std::printf("FAIL warm loop %d index %zu\n", it, i), 1;
+        }
+    }
     bool threw = false;
     try {
         pool::run(64, [](std::size_t t) {
