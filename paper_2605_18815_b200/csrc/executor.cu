@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <limits>
 #include <array>
 #include <chrono>
 #include <cstdio>
@@ -701,18 +702,23 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
                 total[static_cast<size_t>(pending[idx[i]].lane)] += bytes(idx[i]);
             }
             std::vector<size_t> head(static_cast<size_t>(nl), 0);
+            // each lane's progress key (bytes done + half the next copy, over its total),
+            // recomputed only for the lane that advanced; the first lane with the smallest
+            // key goes next
+            const double kDone = std::numeric_limits<double>::infinity();
+            std::vector<double> key(static_cast<size_t>(nl), kDone);
+            auto rekey = [&](size_t L) {
+                if (head[L] >= q[L].size()) key[L] = kDone;
+                else key[L] = total[L] > 0 ? (done[L] + 0.5 * bytes(q[L][head[L]])) / total[L] : 0.0;
+            };
+            for (size_t L = 0; L < static_cast<size_t>(nl); ++L) rekey(L);
             for (size_t k = lo; k < hi; ++k) {
-                int best = -1;
-                double bk = 0;
-                for (int l = 0; l < nl; ++l) {
-                    const size_t L = static_cast<size_t>(l);
-                    if (head[L] >= q[L].size()) continue;
-                    const double key = (done[L] + 0.5 * bytes(q[L][head[L]])) / total[L];
-                    if (best < 0 || key < bk) best = l, bk = key;
-                }
-                const size_t B = static_cast<size_t>(best);
+                size_t B = 0;
+                for (size_t L = 1; L < static_cast<size_t>(nl); ++L)
+                    if (key[L] < key[B]) B = L;
                 const size_t i = q[B][head[B]++];
                 done[B] += bytes(i);
+                rekey(B);
                 out.push_back(pending[i]);
             }
             lo = hi;
