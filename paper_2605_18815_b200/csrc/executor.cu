@@ -686,9 +686,14 @@ void TileSet::finalize(ExecStats* stats, cudaStream_t upload, PinnedBuf* staging
         nrec = pending.size();
         std::vector<Pending> out;
         out.reserve(nrec);
-        std::vector<size_t> idx(nrec);
-        for (size_t i = 0; i < nrec; ++i) idx[i] = i;
-        std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return pending[a].key < pending[b].key; });
+        // records grouped by key, recorded order kept within a key (a counting sort: keys
+        // are launch-group indices)
+        int kmax = 0;
+        for (const Pending& q0 : pending) kmax = std::max(kmax, q0.key);
+        std::vector<size_t> idx(nrec), kstart(static_cast<size_t>(kmax) + 2, 0);
+        for (const Pending& q0 : pending) ++kstart[static_cast<size_t>(q0.key) + 1];
+        for (size_t k = 1; k < kstart.size(); ++k) kstart[k] += kstart[k - 1];
+        for (size_t i = 0; i < nrec; ++i) idx[kstart[static_cast<size_t>(pending[i].key)]++] = i;
         for (size_t lo = 0; lo < nrec;) {
             size_t hi = lo;
             while (hi < nrec && pending[idx[hi]].key == pending[idx[lo]].key) ++hi;
