@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 final multi-GPU validation (gpurun --gpus 4): outputs under gpurun_out/r02zm/.
-O=gpurun_out/r02zm; mkdir -p $O
+O=gpurun_out/${OUT:-r02zm}; mkdir -p $O
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -rs --durations=10 > $O/pytest_gpu.txt 2>&1; echo rc=$? >> $O/pytest_gpu.txt

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Round-2 final one-GPU validation (what the driver runs): outputs under gpurun_out/r02z/.
-O=gpurun_out/r02z; mkdir -p $O
+O=gpurun_out/${OUT:-r02z}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -rs --durations=10 > $O/pytest_gpu.txt 2>&1; echo rc=$? >> $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; echo rc=$? >> $O/smoke.txt
