@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <exception>
 #include <memory>
 #include <mutex>
@@ -32,8 +33,13 @@ struct Job {
 class Pool {
 public:
     Pool() {
+        // the host's cores are shared by the rank processes on it (torchrun exports
+        // LOCAL_WORLD_SIZE); RS_HOST_THREADS overrides
         const std::size_t hw = std::max(1u, std::thread::hardware_concurrency());
-        nthreads_ = std::min<std::size_t>(hw, 16);
+        std::size_t local = 1;
+        if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) local = static_cast<std::size_t>(std::max(1, std::atoi(lw)));
+        nthreads_ = std::max<std::size_t>(1, std::min<std::size_t>(hw / local, 16));
+        if (const char* ht = std::getenv("RS_HOST_THREADS")) nthreads_ = static_cast<std::size_t>(std::max(1, std::atoi(ht)));
         for (std::size_t i = 1; i < nthreads_; ++i) workers_.emplace_back([this] { loop(); });
     }
     ~Pool() {

@@ -9,7 +9,9 @@
 namespace reshard {
 namespace pool {
 
-/// number of threads parallel_for uses (workers + the caller), >= 1
+/// number of threads parallel_for uses (workers + the caller), >= 1: the host's cores
+/// divided by the rank processes sharing it (LOCAL_WORLD_SIZE), at most 16;
+/// RS_HOST_THREADS overrides
 std::size_t size();
 
 /// fn(t) for t in [0, n) on the pool (the caller runs one share); returns when all are
