@@ -460,7 +460,9 @@ def run_ours(args):
                     "frac": round(t_roof / (fwd_avg / 1e3), 4),
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
                     "frac_of_nominal_900": round(t_roof_nominal / (fwd_avg / 1e3), 4),
-                    "traffic": None, "kernel": "copy_tiles_kernel<16> mixed local/peer launch (forward transition, binding GPU)",
+                    "traffic": None,
+                    "kernel": ("copy_tiles_kernel<16, false, true> (256-bit loads/stores)" if os.environ.get("RS_VEC32") != "0"
+                               else "copy_tiles_kernel<16>") + " mixed local/peer launch (forward transition, binding GPU)",
                     "algorithmic_bytes_per_launch": link, "t_roof_s": round(t_roof, 5),
                     "per_gpu_out_in_gb": [[round(p.out_bytes / 1e9, 2), round(p.in_bytes / 1e9, 2)] for p in pl],
                     **nvlink_wire(nv),
@@ -468,8 +470,10 @@ def run_ours(args):
             # DRAM read + write of the binding GPU's forward launch (the longest) from the
             # committed ncu capture of the same transition at this N (tools/p2p_profile.py, one
             # process driving all GPUs): its HBM side, local copies r+w + peer-bound reads
-            tname = f"r01_traffic_n{n}_L32.json"
-            tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", tname)
+            prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+            tname = next((f for f in (f"r02_traffic_n{n}_L32.json", f"r01_traffic_n{n}_L32.json")
+                          if os.path.exists(os.path.join(prof, f))), f"r01_traffic_n{n}_L32.json")
+            tp = os.path.join(prof, tname)
             if args.layers == 32 and os.path.exists(tp):
                 with open(tp) as f:
                     cap = json.load(f)
