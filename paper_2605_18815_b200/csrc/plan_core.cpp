@@ -78,45 +78,6 @@ bool make_stair(const TensorSpec& t, const Seg& s, Interval range, stair::Stair*
 
 const Interval& shard_of(const RankGeom& g, const Seg& s) { return s.expert ? g.eshard : g.dshard; }
 
-/// Triple (J ∩ K) \ I; false if the iteration space is empty.
-bool make_triple(const ModelSpace& space, int t, const RankGeom& k, const RankGeom& j, const RankGeom* own,
-                 stair::Triple* T) {
-    const int sk = k.seg_of[static_cast<size_t>(t)], sj = j.seg_of[static_cast<size_t>(t)];
-    if (sk < 0 || sj < 0) return false;
-    const auto& e = space.entries()[static_cast<size_t>(t)];
-    const Seg& Sk = k.segs[static_cast<size_t>(sk)];
-    const Seg& Sj = j.segs[static_cast<size_t>(sj)];
-    stair::Triple X{};
-    if (!make_stair(e.spec, Sk, shard_of(k, Sk), &X.K)) return false;
-    if (!make_stair(e.spec, Sj, shard_of(j, Sj), &X.J)) return false;
-    X.t = view_of(e);
-    std::int64_t n = 1;
-    for (int i = 0; i < X.t.np; ++i) {
-        X.plo[i] = std::max(X.K.plo[i], X.J.plo[i]);
-        X.phi[i] = std::min(X.K.phi[i], X.J.phi[i]);
-        if (X.plo[i] >= X.phi[i]) return false;
-        n *= X.phi[i] - X.plo[i];
-    }
-    X.rlo = std::max(X.K.rlo, X.J.rlo);
-    X.rhi = std::min(X.K.rhi, X.J.rhi);
-    if (X.rlo >= X.rhi) return false;
-    if (std::max(X.K.clo, X.J.clo) >= std::min(X.K.chi, X.J.chi)) return false;
-    X.nrows = n * (X.rhi - X.rlo);
-    X.has_i = 0;
-    if (own) {
-        const int si = own->seg_of[static_cast<size_t>(t)];
-        if (si >= 0) {
-            const Seg& Si = own->segs[static_cast<size_t>(si)];
-            if (make_stair(e.spec, Si, shard_of(*own, Si), &X.I)) X.has_i = 1;
-        }
-    }
-    X.src = k.rank;
-    X.dst = j.rank;
-    X.tensor = t;
-    *T = X;
-    return true;
-}
-
 /// Stairs of every (rank, tensor) of one side, built once per plan (a triple needs three
 /// of them; the (src, dst, tensor) loop would otherwise rebuild each one many times)
 struct StairTable {
@@ -142,7 +103,8 @@ StairTable stair_table(const ModelSpace& space, const Side& side) {
     return T;
 }
 
-/// make_triple from precomputed stairs (same result)
+/// Triple (J ∩ K) \ I from precomputed stairs (own < 0: no I); false if the iteration
+/// space is empty
 bool make_triple_cached(const ModelSpace& space, int t, const StairTable& src, const StairTable& dst, int k, int j,
                         int own, const std::vector<stair::TensorView>& views, stair::Triple* T) {
     const size_t tt = static_cast<size_t>(t);
@@ -554,8 +516,10 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
     P.id_rank.resize(static_cast<size_t>(nt));
     for (int i = 0; i < nt; ++i) P.id_rank[static_cast<size_t>(P.by_id[static_cast<size_t>(i)])] = i;
 
-    P.src = build_side(space, srcc);
-    P.dst = build_side(space, dstc);
+    pool::run(2, [&](size_t w) {
+        if (w == 0) P.src = build_side(space, srcc);
+        else P.dst = build_side(space, dstc);
+    });
     for (int i = 0; i < srcc.world_size(); ++i) P.src.ranks[static_cast<size_t>(i)].phys = P.wm.src_phys[static_cast<size_t>(i)];
     for (int j = 0; j < dstc.world_size(); ++j) P.dst.ranks[static_cast<size_t>(j)].phys = P.wm.dst_phys[static_cast<size_t>(j)];
     for (int phys : P.wm.participants()) P.routes.push_back({phys, P.wm.src_rank_of(phys), P.wm.dst_rank_of(phys)});
@@ -726,15 +690,17 @@ PlanCore build_plan(const ModelSpace& space, const ParallelConfig& srcc, const P
         for (const auto& v : per_pair) P.triples.insert(P.triples.end(), v.begin(), v.end());
         for (const stair::Triple& T : P.triples) by_dst[static_cast<size_t>(T.dst)].push_back(&T);
         phase("triples-pairs");
-        for (const RouteInfo& r : P.routes) {
-            if (r.src_rank < 0 || r.dst_rank < 0) continue;
-            for (int t = 0; t < nt; ++t) {
+        std::vector<std::vector<stair::Triple>> per_route_retain(P.routes.size());
+        parallel_for(P.routes.size(), [&](size_t ri) {
+            const RouteInfo& r = P.routes[ri];
+            if (r.src_rank < 0 || r.dst_rank < 0) return;
+            for (int t = 0; t < nt; ++t) {  // (J ∩ K) of the device's own old and new rank
                 stair::Triple T;
-                if (make_triple(space, t, P.src.ranks[static_cast<size_t>(r.src_rank)],
-                                P.dst.ranks[static_cast<size_t>(r.dst_rank)], nullptr, &T))
-                    P.retain_triples.push_back(T);
+                if (make_triple_cached(space, t, src_st, dst_st, r.src_rank, r.dst_rank, -1, views, &T))
+                    per_route_retain[ri].push_back(T);
             }
-        }
+        });
+        for (const auto& v : per_route_retain) P.retain_triples.insert(P.retain_triples.end(), v.begin(), v.end());
         for (const stair::Triple& T : P.retain_triples) retained += triple_count(T) * kOptimStateBytes;
 
         phase("triples");
