@@ -248,6 +248,19 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     sc = S.config2(args.layers)
+    # fewer GPUs than the transition's 8 devices: which devices share a GPU is ours to
+    # choose (at N=8 each device is a GPU). Balanced: the grouping with the fastest busiest
+    # GPU from the plan's device traffic matrix (runtime.colocation), applied by relabelling
+    # the identity world map so the executor's contiguous blocks are those groups; the plan
+    # (ranks, transfers, bytes) is unchanged. Contiguous: devices 2g, 2g+1 on GPU g (N=4).
+    colocated = None
+    if 1 < n < 8 and args.placement == "balanced":
+        import dataclasses
+
+        from paper_2605_18815_b200.runtime import colocated_world, colocation
+        colocated = colocation(RoutingPlan.from_scenario(sc).traffic(), n)
+        w = colocated_world(colocated)
+        sc = dataclasses.replace(sc, world_src=w, world_dst=w)
     t0 = time.perf_counter()
     ab = RoutingPlan.from_scenario(sc)
     plan_s = time.perf_counter() - t0
@@ -391,7 +404,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        plan_i = plan_transition(space, sc.src, sc.dst, nodes=sc.nodes, rpn=sc.rpn, scalar_words=sc.scalar_words)
+        plan_i = plan_transition(space, sc.src, sc.dst, world_src=sc.world_src, world_dst=sc.world_dst, nodes=sc.nodes,
+                                 rpn=sc.rpn, scalar_words=sc.scalar_words)
         t1 = time.perf_counter()
         fwd.ex.set_plan(plan_i)
         reprepare[0]()
@@ -471,8 +485,9 @@ def run_ours(args):
             # committed ncu capture of the same transition at this N (tools/p2p_profile.py, one
             # process driving all GPUs): its HBM side, local copies r+w + peer-bound reads
             prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
-            tname = next((f for f in (f"r02_traffic_n{n}_L32.json", f"r01_traffic_n{n}_L32.json")
-                          if os.path.exists(os.path.join(prof, f))), f"r01_traffic_n{n}_L32.json")
+            names = ((f"r02_traffic_n{n}_L32_balanced.json",) if colocated else
+                     (f"r02_traffic_n{n}_L32.json", f"r01_traffic_n{n}_L32.json"))
+            tname = next((f for f in names if os.path.exists(os.path.join(prof, f))), names[0])
             tp = os.path.join(prof, tname)
             if args.layers == 32 and os.path.exists(tp):
                 with open(tp) as f:
@@ -520,6 +535,9 @@ def run_ours(args):
                                    f"(the way back restores the state between steps, reported as way_back)",
                        "state": "Llama-3-8B full training state", "layers": args.layers, "virtual_ranks": 8,
                        "parallelism": f"tp8 -> dp2xtp4 + zero1 on {n} GPU(s)", "l2": "inputs >> L2 (no flush needed)",
+                       "colocation": ({"policy": "traffic-balanced (runtime.colocation)", "world_ranks_per_gpu": colocated}
+                                      if colocated else {"policy": "contiguous" if 1 < n < 8 else "one device per GPU"
+                                                         if n >= 8 else "all devices on one GPU"}),
                        "plan_bytes_per_transition": ab.bytes_moved()},
             "reconfig_s": round(fwd_avg / 1e3, 5),
             "gbs_per_gpu": round(ab.bytes_moved() / (fwd_avg / 1e3) / 1e9 / n, 2),
@@ -567,6 +585,8 @@ def main():
     ap.add_argument("--arena-multi", action="store_true",
                     help="N>1: memory-aware arena across GPUs (stage barriers) instead of plain allocations")
     ap.add_argument("--hbm-cap", type=int, default=0, help="arena physical budget in bytes (0: free HBM - 1 GiB)")
+    ap.add_argument("--placement", default="balanced", choices=["balanced", "contiguous"],
+                    help="1 < N < 8: which of the 8 devices share a GPU (balanced: from the traffic matrix)")
     ap.add_argument("--transport", default="fused", choices=["fused", "nccl"],
                     help="fused: one-sided NVLink stores (product); nccl: pack -> NCCL send/recv -> unpack (comparison)")
     args = ap.parse_args()

@@ -170,6 +170,11 @@ int rs_plan_tensor(const rs_plan_t* p, int index, char* id_buf, int cap, int64_t
 int rs_plan_num_tensors(const rs_plan_t* p, int* n);
 
 int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stats_t* out);
+/* copy bytes between physical devices: out[s * n + d] (n = *n_phys, highest participating
+ * phys + 1; fills when cap >= n * n). Off-diagonal entries sum to bytes_moved; the
+ * diagonal holds on-device copies. Input of the co-location search when devices share a GPU
+ * (no reference counterpart: the reference runs one device per GPU). */
+int rs_plan_traffic(const rs_plan_t* p, int64_t* out, int cap, int* n_phys);
 /* participating physical devices, ascending (WorldMap::participants, worldmap.hpp:60-68);
  * *n = count (fills at most cap) */
 int rs_plan_participants(const rs_plan_t* p, int* phys, int cap, int* n);

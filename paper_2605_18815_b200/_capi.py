@@ -23,7 +23,7 @@ EXPORTED = [
     "rs_exec_fill", "rs_exec_run", "rs_exec_verify", "rs_exec_stats", "rs_exec_set_stages",
     "rs_memory_plan", "rs_config_groups", "rs_rank_coord", "rs_exec_prepare_staged", "rs_exec_channel_bytes", "rs_exec_pack", "rs_exec_unpack", "rs_plan_placement", "rs_xor_peer", "rs_memory_aware_chunk", "rs_schedule_build", "rs_schedule_destroy",
     "rs_schedule_summary", "rs_schedule_stage", "rs_schedule_peer", "rs_schedule_collective", "rs_schedule_dump",
-    "rs_arena_create", "rs_arena_destroy", "rs_exec_gpu_of_phys", "rs_plan_participants", "rs_exec_set_plan", "rs_exec_set_collectives", "rs_arena_release_through", "rs_sync_create", "rs_sync_destroy", "rs_sync_export", "rs_sync_import", "rs_sync_barrier", "rs_sync_status", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
+    "rs_arena_create", "rs_arena_destroy", "rs_exec_gpu_of_phys", "rs_plan_traffic", "rs_plan_participants", "rs_exec_set_plan", "rs_exec_set_collectives", "rs_arena_release_through", "rs_sync_create", "rs_sync_destroy", "rs_sync_export", "rs_sync_import", "rs_sync_barrier", "rs_sync_status", "rs_arena_buffer", "rs_arena_stage_order", "rs_arena_stats",
 ]
 
 
@@ -150,6 +150,7 @@ def lib():
     L.rs_exec_prepare_staged.argtypes = [vp]
     L.rs_exec_channel_bytes.argtypes = [vp, C.c_int, C.c_int, P(i64)]
     L.rs_exec_gpu_of_phys.argtypes = [vp, C.c_int, P(C.c_int)]
+    L.rs_plan_traffic.argtypes = [vp, P(C.c_int64), C.c_int, P(C.c_int)]
     L.rs_exec_set_plan.argtypes = [vp, vp]
     L.rs_exec_set_collectives.argtypes = [vp, C.c_int]
     L.rs_arena_release_through.argtypes = [vp, C.c_int, P(i64)]

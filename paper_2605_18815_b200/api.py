@@ -80,6 +80,15 @@ class RoutingPlan:
         A.check(A.lib().rs_plan_placement(self.h, n_gpus, gpu, C.byref(s)))
         return s
 
+    def traffic(self) -> List[List[int]]:
+        """Copy bytes between physical devices, m[s][d] (rs_plan_traffic): off-diagonal
+        entries sum to bytes_moved, the diagonal holds on-device copies."""
+        n = C.c_int()
+        A.check(A.lib().rs_plan_traffic(self.h, None, 0, C.byref(n)))
+        buf = (C.c_int64 * max(1, n.value * n.value))()
+        A.check(A.lib().rs_plan_traffic(self.h, buf, n.value * n.value, C.byref(n)))
+        return [list(buf[i * n.value:(i + 1) * n.value]) for i in range(n.value)]
+
     def participants(self) -> List[int]:
         """Participating physical devices, ascending (WorldMap::participants)."""
         n = C.c_int()

@@ -508,6 +508,16 @@ int rs_plan_placement(const rs_plan_t* p, int n_gpus, int gpu, rs_placement_stat
     });
 }
 
+int rs_plan_traffic(const rs_plan_t* p, int64_t* out, int cap, int* n_phys) {
+    return guarded([&] {
+        int n = 0;
+        const std::vector<std::int64_t> m = exec::traffic_matrix(p->core, &n);
+        if (n_phys) *n_phys = n;
+        if (out && cap >= n * n) std::copy(m.begin(), m.end(), out);
+        return RS_OK;
+    });
+}
+
 int rs_plan_regions(const rs_plan_t* p, int side, char** out, size_t* len) {
     return guarded([&] {
         const ModelSpace& space = *p->core.space;

@@ -224,3 +224,22 @@ void buffer_sizes(const PlanCore& P, int side, int rank, bool with_grads, std::i
 
 }  // namespace exec
 }  // namespace reshard
+
+namespace reshard {
+namespace exec {
+
+std::vector<std::int64_t> traffic_matrix(const PlanCore& P, int* n_out) {
+    int n = 0;
+    for (const auto& r : P.routes) n = std::max(n, r.phys + 1);
+    std::vector<std::int64_t> m(static_cast<size_t>(n) * static_cast<size_t>(n), 0);
+    for (const CopyOp& op : build_ops(P)) {
+        const int s = P.wm.src_phys[static_cast<size_t>(op.src_side_rank)];
+        const int d = P.wm.dst_phys[static_cast<size_t>(op.dst_rank)];
+        m[static_cast<size_t>(s) * static_cast<size_t>(n) + static_cast<size_t>(d)] += op.rows * op.row_bytes;
+    }
+    if (n_out) *n_out = n;
+    return m;
+}
+
+}  // namespace exec
+}  // namespace reshard

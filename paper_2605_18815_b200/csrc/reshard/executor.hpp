@@ -55,6 +55,12 @@ struct PlacementStats {
 };
 PlacementStats placement_stats(const core::PlanCore& P, int n_gpus, int gpu);
 
+/// The transition's copy bytes between physical devices (host only): m[s * n + d] for
+/// n = highest participating phys + 1; off-diagonal entries sum to bytes_moved, the
+/// diagonal holds the on-device copies (retained regions). Input of a co-location search
+/// when several devices share a GPU.
+std::vector<std::int64_t> traffic_matrix(const core::PlanCore& P, int* n);
+
 /// Buffer sizes of a rank (bytes) for one side.
 void buffer_sizes(const core::PlanCore& P, int side, int rank, bool with_grads, std::int64_t out[kNumBufs]);
 

@@ -560,3 +560,64 @@ def run_dedup_early(ex: Executor, stream, side_stream, group=None) -> None:
 def local_ranks(plan: RoutingPlan, ex: Executor, side: int) -> List[int]:
     n = plan.summary.src_world if side == A.SIDE_SRC else plan.summary.dst_world
     return [r for r in range(n) if ex.buffer(side, r, A.BUF_PARAM)[2] == ex.gpu]
+
+
+def colocation(traffic: List[List[int]], n_gpus: int, nvlink_gbs: float = 690.0,
+               hbm_gbs: float = 6200.0) -> List[List[int]]:
+    """Which physical devices share each GPU when there are fewer GPUs than devices (the
+    8-device transitions at N = 2, 4): the equal-size grouping whose busiest GPU is fastest
+    under the arena time model's bounds (NVLink out, NVLink in, HBM = on-GPU copies read and
+    written + peer traffic), from the plan's device traffic matrix (RoutingPlan.traffic()).
+    Ties keep the first grouping in enumeration order, contiguous blocks first, so every
+    rank derives the same answer. Returns the groups, GPU by GPU (sorted device ids)."""
+    import itertools
+    n = len(traffic)
+    contiguous = [list(range(g * (n // max(1, n_gpus)), (g + 1) * (n // max(1, n_gpus)))) for g in range(n_gpus)]
+    if n_gpus <= 1 or n_gpus >= n or n % n_gpus:
+        return contiguous
+    size = n // n_gpus
+
+    def partitions(rest):
+        if not rest:
+            yield []
+            return
+        for comb in itertools.combinations(rest[1:], size - 1):
+            g = (rest[0],) + comb
+            for p in partitions([x for x in rest if x not in g]):
+                yield [list(g)] + p
+
+    def cost(groups):
+        of = {d: i for i, g in enumerate(groups) for d in g}
+        out, inn, loc = [0] * n_gpus, [0] * n_gpus, [0] * n_gpus
+        for s in range(n):
+            for d in range(n):
+                b = traffic[s][d]
+                if of[s] == of[d]:
+                    loc[of[s]] += b
+                else:
+                    out[of[s]] += b
+                    inn[of[d]] += b
+        return max(max(out[g], inn[g]) / nvlink_gbs for g in range(n_gpus)) if max(out) else 0.0, \
+            max((2 * loc[g] + out[g] + inn[g]) / hbm_gbs for g in range(n_gpus))
+
+    import math
+    if math.comb(n - 1, size - 1) ** (n_gpus - 1) > 200000:  # too many groupings to try
+        return contiguous
+    best, best_t = contiguous, max(cost(contiguous))
+    for p in partitions(list(range(n))):
+        t = max(cost(p))
+        if t < best_t - 1e-9:
+            best, best_t = p, t
+    return best
+
+
+def colocated_world(groups: List[List[int]]) -> List[int]:
+    """Device ids for an identity world map relabelled so the executor's contiguous blocks
+    (device // devices-per-GPU) are `groups`: entry r is the device that hosts world rank r
+    (old and new configuration alike)."""
+    size = len(groups[0])
+    new_id = {}
+    for g, devs in enumerate(groups):
+        for i, d in enumerate(devs):
+            new_id[d] = g * size + i
+    return [new_id[r] for r in range(len(new_id))]

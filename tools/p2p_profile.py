@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=2)
     ap.add_argument("--ctas", type=int, default=0, help="CTAs per SM of the copy kernels (0: default)")
     ap.add_argument("--tile-bytes", type=int, default=0, help="tile size (0: default 512 KiB)")
+    ap.add_argument("--placement", default="contiguous", choices=["balanced", "contiguous"],
+                    help="which devices share a GPU (balanced: bench.py's default co-location)")
     ap.add_argument("--same-device", action="store_true",
                     help="place every executor's GPU on device 0 (one-GPU boxes: the one-process multi-executor path)")
     args = ap.parse_args()
@@ -41,7 +43,14 @@ def main():
         for b in range(G):
             if dev(a) != dev(b):
                 enable_peer_access(dev(a), dev(b))
-    plan = RoutingPlan.from_scenario(S.config2(args.layers))
+    sc = S.config2(args.layers)
+    if args.placement == "balanced" and 1 < G < 8:  # the bench's co-location (runtime.colocation)
+        import dataclasses
+
+        from paper_2605_18815_b200.runtime import colocated_world, colocation
+        w = colocated_world(colocation(RoutingPlan.from_scenario(sc).traffic(), G))
+        sc = dataclasses.replace(sc, world_src=w, world_dst=w)
+    plan = RoutingPlan.from_scenario(sc)
     ex = [Executor(plan, n_gpus=G, gpu=g, device=dev(g), ctas_per_sm=args.ctas, tile_bytes=args.tile_bytes)
           for g in range(G)]
     keep = []
@@ -87,6 +96,7 @@ def main():
     bad = sum(e.verify(A.SIDE_DST, seed)[0] for e in ex)
     st = [e.stats() for e in ex]
     out = {"workload": f"llama3-8b (L={args.layers}) tp8->dp2xtp4 zero1 forward, {G} GPUs from one process (peer access)",
+           "placement": args.placement, "world": list(sc.world_src) if sc.world_src is not None else None,
            "ctas_per_sm": args.ctas, "tile_bytes": args.tile_bytes,
            "ms_per_gpu": [round(t, 3) for t in best],
            "remote_gb_per_gpu": [round(s.remote_bytes / 1e9, 3) for s in st],
