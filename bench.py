@@ -525,9 +525,11 @@ def run_ours(args):
         out = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "strong",
-            "scaling_note": ("the same 8-virtual-rank transition at every N: at N=1 it is an HBM-only permutation "
-                             "(roofline 39 ms), from N=2 on bytes cross NVLink (roofline 35.7 ms at N=2 and 4, "
-                             "17.8 ms at N=8, SURVEY 8d); roofline.frac is the per-N efficiency"),
+            "scaling_note": ("the same 8-device transition (same plan) at every N: at N=1 it is an HBM-only "
+                             "permutation (roofline 39 ms); from N=2 on the bytes between devices on different GPUs "
+                             "cross NVLink, so the roofline follows the busiest GPU of the co-location "
+                             "(config.colocation; at 900 GB/s: 17.8 ms at N=2 balanced, 26.8 ms at N=4 balanced, "
+                             "35.7 ms contiguous, 17.8 ms at N=8); roofline.frac is the per-N efficiency"),
             "vs_baseline": None, "dtype": "u16/u32 payload copy (bf16 params, fp32 master/m/v)",
             "data": "synthetic (canon payloads, bit-exact verified)",
             "transport": args.transport,
