@@ -48,8 +48,19 @@ def scenario(cfg: int, layers: int):
     raise SystemExit(f"unknown config {cfg}")
 
 
-def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False, level=None):
+def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False, level=None, placement="contiguous"):
     plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
+    colocated = None
+    if placement == "balanced" and 1 < world < len(plan.traffic()) and sc.world_src is None and sc.world_dst is None \
+            and sc.src.world() == sc.dst.world():
+        # which devices share a GPU, from the plan's traffic matrix (bench.py's default)
+        import dataclasses
+
+        from paper_2605_18815_b200.runtime import colocated_world, colocation
+        colocated = colocation(plan.traffic(), world)
+        w = colocated_world(colocated)
+        sc = dataclasses.replace(sc, world_src=w, world_dst=w)
+        plan = RoutingPlan.from_scenario(sc, allow_oversourced=True)
     arena = None
     if arena_cap:
         # old + new state do not fit: the memory-aware arena under a per-GPU cap, stages
@@ -102,6 +113,7 @@ def run_one(sc, rank, world, local, reps, arena_cap=0.0, host_barriers=False, le
     hbm_gbs = peaks()
     t_roof = max(link / (NVLINK_GBS * 1e9), hbm / (hbm_gbs * 1e9))
     out = {"config": sc.name, "n_gpus": world, "plan_bytes": plan.bytes_moved(), "retained_bytes": plan.bytes_retained(),
+           "colocation": colocated or placement,
            "transfers": plan.num_transfers(), "ms": round(ms, 3), "mismatches": int(bad),
            "gbs_per_gpu": round(plan.bytes_moved() / (ms / 1e3) / 1e9 / world, 1),
            "roofline": {"bound": "nvlink" if link / NVLINK_GBS > hbm / hbm_gbs else "hbm",
@@ -158,6 +170,8 @@ def main():
     ap.add_argument("--level", type=int, action="append",
                     help="with --arena-cap: force this schedule ladder level (repeatable); default: the fastest that fits")
     ap.add_argument("--both-barriers", action="store_true", help="run every arena case with device and host barriers")
+    ap.add_argument("--placement", default="contiguous", choices=["balanced", "contiguous"],
+                    help="which of the scenario's devices share a GPU when there are fewer GPUs (runtime.colocation)")
     ap.add_argument("--barrier-probe", type=int, default=0,
                     help="time N back-to-back device barriers (SynchronizeAll latency) and exit")
     args = ap.parse_args()
@@ -173,7 +187,8 @@ def main():
         for cfg in args.config or [1, 4]:
             for lv in (args.level or [None]):
                 for hb in ((False, True) if args.both_barriers else (args.host_barriers,)):
-                    res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap, hb, lv)
+                    res = run_one(scenario(cfg, args.layers), rank, world, local, args.reps, args.arena_cap, hb, lv,
+                                  args.placement)
                     if rank == 0:
                         print(json.dumps(res), flush=True)
     if world > 1:
