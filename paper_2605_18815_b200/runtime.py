@@ -586,7 +586,7 @@ def colocation(traffic: List[List[int]], n_gpus: int, nvlink_gbs: float = 690.0,
             for p in partitions([x for x in rest if x not in g]):
                 yield [list(g)] + p
 
-    def cost(groups):
+    def seconds(groups):  # the busiest GPU's bound (bytes / (GB/s) -> ns; only compared)
         of = {d: i for i, g in enumerate(groups) for d in g}
         out, inn, loc = [0] * n_gpus, [0] * n_gpus, [0] * n_gpus
         for s in range(n):
@@ -597,16 +597,16 @@ def colocation(traffic: List[List[int]], n_gpus: int, nvlink_gbs: float = 690.0,
                 else:
                     out[of[s]] += b
                     inn[of[d]] += b
-        return max(max(out[g], inn[g]) / nvlink_gbs for g in range(n_gpus)) if max(out) else 0.0, \
-            max((2 * loc[g] + out[g] + inn[g]) / hbm_gbs for g in range(n_gpus))
+        return max(max(out[g] / nvlink_gbs, inn[g] / nvlink_gbs, (2 * loc[g] + out[g] + inn[g]) / hbm_gbs)
+                   for g in range(n_gpus))
 
     import math
     if math.comb(n - 1, size - 1) ** (n_gpus - 1) > 200000:  # too many groupings to try
         return contiguous
-    best, best_t = contiguous, max(cost(contiguous))
+    best, best_t = contiguous, seconds(contiguous)
     for p in partitions(list(range(n))):
-        t = max(cost(p))
-        if t < best_t - 1e-9:
+        t = seconds(p)
+        if t < best_t * (1 - 1e-12):
             best, best_t = p, t
     return best
 
