@@ -50,6 +50,23 @@ def main():
             dst = S.random_cfg(rng, m, max_world=8, zero=src.zero)
             scenarios.append(S.Scenario(m, src, dst, world_src=list(range(src.world())),
                                         world_dst=list(range(dst.world())), name=f"random-moe-{k}"))
+    if "--colocate" in sys.argv:
+        # bench.py's balanced co-location: devices grouped onto GPUs from the plan's traffic
+        # matrix, applied by relabelling identity world maps (same-size worlds only)
+        import dataclasses
+
+        from paper_2605_18815_b200.runtime import colocated_world, colocation
+        out = []
+        for sc in scenarios:
+            identity = sc.world_src in (None, list(range(sc.src.world()))) and \
+                sc.world_dst in (None, list(range(sc.dst.world())))
+            if identity and sc.src.world() == sc.dst.world() and 1 < world < sc.src.world():
+                w = colocated_world(colocation(RoutingPlan.from_scenario(sc, allow_oversourced=True).traffic(), world))
+                sc = dataclasses.replace(sc, world_src=w, world_dst=w, name=sc.name + ".colocated")
+            out.append(sc)
+        scenarios = out
+        if rank == 0:
+            print(f"COLOCATED {sum(sc.name.endswith('.colocated') for sc in scenarios)}", flush=True)
     for sc in scenarios:
         ab = RoutingPlan.from_scenario(sc, allow_oversourced=True)
         ba = RoutingPlan.from_scenario(sc.reversed(), allow_oversourced=True)

@@ -204,16 +204,21 @@ def test_arena_round_trip_aliased():
         assert e2.verify(1, SEED)[0] == 0
 
 
-def test_multi_gpu_push_over_nvlink():
-    """N>1: torchrun one process per GPU; skipped on a 1-GPU box."""
+@pytest.mark.parametrize("colocate", [[], ["--colocate"]])
+def test_multi_gpu_push_over_nvlink(colocate):
+    """N>1 (one process per GPU; on a 1-GPU box the rank processes share it), every local
+    buffer byte-compared with the oracle; with --colocate the 8-device scenarios are grouped
+    onto the GPUs as bench.py does (runtime.colocation, relabelled world maps)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={_ranks()}",
-                        "--master-addr", "127.0.0.1", "--master-port", "29531",
-                        os.path.join(root, "tests", "mgpu_check.py"), "2", "--oracle"],
+                        "--master-addr", "127.0.0.1", "--master-port", "29531" if not colocate else "29532",
+                        os.path.join(root, "tests", "mgpu_check.py"), "2", "--oracle"] + colocate,
                        capture_output=True, text=True, timeout=900)
     assert "MGPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    if colocate:
+        assert "COLOCATED 0" not in r.stdout and "COLOCATED" in r.stdout, r.stdout[-3000:]
 
 
 @pytest.mark.parametrize("dedup", [[], ["--dedup"]])
