@@ -40,6 +40,9 @@ def main():
                     help="--dedup with the replica copies overlapping the tail of the pushes")
     ap.add_argument("--multicast", action="store_true",
                     help="state in shareable VMM buffers; the grow's parameter broadcast over NVLS multicast")
+    ap.add_argument("--placement", default="matched", choices=["matched", "contiguous"],
+                    help="8 devices on fewer GPUs: matched puts one device of the 4-rank world (and its DP8 "
+                         "partner) on each GPU; contiguous puts devices 2g, 2g+1 on GPU g (round 1)")
     ap.add_argument("--no-nccl-comms", action="store_true",
                     help="skip the new world's NCCL communicators (always skipped when ranks share a GPU)")
     args = ap.parse_args()
@@ -49,6 +52,19 @@ def main():
     nccl_comms = not args.no_nccl_comms and not shared
     early = (torch.cuda.Stream(), dist.new_group(backend="gloo")) if args.dedup_early else None
     shrink, grow = S.config3(args.layers)
+    if args.placement == "matched" and 1 < world < 8 and 4 % world == 0:
+        # devices share GPUs (8 devices on `world` GPUs): spread the 4-rank world over every
+        # GPU (device d and its old-world partner d + 4 on GPU d % world), so each process
+        # hosts its share of the new world, and relabel the identity world maps so the
+        # executor's contiguous blocks are those groups (runtime.colocated_world)
+        import dataclasses
+
+        from paper_2605_18815_b200.runtime import colocated_world
+        groups = [sorted([d for d in range(4) if d % world == g] + [d + 4 for d in range(4) if d % world == g])
+                  for g in range(world)]
+        w = colocated_world(groups)
+        shrink = dataclasses.replace(shrink, world_src=w[:8], world_dst=w[:4])
+        grow = dataclasses.replace(grow, world_src=w[:4], world_dst=w[:8])
     grow.balance = args.balance
     edm = ElasticDeviceManager()
     train_stream = torch.cuda.Stream()
@@ -242,6 +258,7 @@ def main():
         torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps({"config": "BASELINE config 3: Llama-3-8B DP8->DP4->DP8, ZeRO-1", "layers": args.layers,
+                          "placement": args.placement, "world_src_shrink": shrink.world_src,
                           "n_gpus": world, "grow_balance_fanout": args.balance, "multicast": args.multicast, "dedup": args.dedup, "dedup_early": args.dedup_early,
                           "results": results}), flush=True)
     dist.barrier()
