@@ -258,9 +258,11 @@ def run_ours(args):
         import dataclasses
 
         from paper_2605_18815_b200.runtime import colocated_world, colocation
+        t0 = time.perf_counter()
         colocated = colocation(RoutingPlan.from_scenario(sc).traffic(), n)
         w = colocated_world(colocated)
         sc = dataclasses.replace(sc, world_src=w, world_dst=w)
+        colocation_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     ab = RoutingPlan.from_scenario(sc)
     plan_s = time.perf_counter() - t0
@@ -537,7 +539,8 @@ def run_ours(args):
                                    f"(the way back restores the state between steps, reported as way_back)",
                        "state": "Llama-3-8B full training state", "layers": args.layers, "virtual_ranks": 8,
                        "parallelism": f"tp8 -> dp2xtp4 + zero1 on {n} GPU(s)", "l2": "inputs >> L2 (no flush needed)",
-                       "colocation": ({"policy": "traffic-balanced (runtime.colocation)", "world_ranks_per_gpu": colocated}
+                       "colocation": ({"policy": "traffic-balanced (runtime.colocation)", "world_ranks_per_gpu": colocated,
+                                       "search_s": round(colocation_s, 4)}
                                       if colocated else {"policy": "contiguous" if 1 < n < 8 else "one device per GPU"
                                                          if n >= 8 else "all devices on one GPU"}),
                        "plan_bytes_per_transition": ab.bytes_moved()},
