@@ -72,3 +72,25 @@ def test_relabelled_world_map_keeps_the_plan():
         # the placement the executor and the roofline see
         pl = [RoutingPlan.from_scenario(sc2).placement(n, g) for g in range(n)]
         assert max(max(p.out_bytes, p.in_bytes) for p in pl) == _cut(ab.traffic(), groups)
+
+
+def test_traffic_matrix_follows_the_relabelling():
+    """Relabelling devices permutes the traffic matrix and nothing else: entry (s, d) of
+    the identity plan is entry (w[s], w[d]) of the relabelled one, for random permutations
+    of config 2, config 5 and config 3's two events."""
+    rng = random.Random(5)
+    shrink, grow = S.config3(2)
+    for sc in (S.config2(2), S.config5(2)):
+        t = RoutingPlan.from_scenario(sc, allow_oversourced=True).traffic()
+        for _ in range(3):
+            w = list(range(8))
+            rng.shuffle(w)
+            t2 = RoutingPlan.from_scenario(dataclasses.replace(sc, world_src=w, world_dst=w),
+                                           allow_oversourced=True).traffic()
+            assert all(t2[w[s]][w[d]] == t[s][d] for s in range(8) for d in range(8))
+    w = list(range(8))
+    rng.shuffle(w)
+    for sc, ws, wd in ((shrink, w, w[:4]), (grow, w[:4], w)):
+        t = RoutingPlan.from_scenario(sc).traffic()
+        t2 = RoutingPlan.from_scenario(dataclasses.replace(sc, world_src=ws, world_dst=wd)).traffic()
+        assert all(t2[w[s]][w[d]] == t[s][d] for s in range(8) for d in range(8))
