@@ -254,7 +254,7 @@ def run_ours(args):
     # the identity world map so the executor's contiguous blocks are those groups; the plan
     # (ranks, transfers, bytes) is unchanged. Contiguous: devices 2g, 2g+1 on GPU g (N=4).
     colocated = None
-    if 1 < n < 8 and args.placement == "balanced":
+    if 1 < n < 8 and 8 % n == 0 and args.placement == "balanced":
         import dataclasses
 
         from paper_2605_18815_b200.runtime import colocated_world, colocation

@@ -572,9 +572,10 @@ def colocation(traffic: List[List[int]], n_gpus: int, nvlink_gbs: float = 690.0,
     rank derives the same answer. Returns the groups, GPU by GPU (sorted device ids)."""
     import itertools
     n = len(traffic)
-    contiguous = [list(range(g * (n // max(1, n_gpus)), (g + 1) * (n // max(1, n_gpus)))) for g in range(n_gpus)]
-    if n_gpus <= 1 or n_gpus >= n or n % n_gpus:
-        return contiguous
+    if n_gpus <= 1 or n_gpus >= n or n % n_gpus:  # one GPU, one device per GPU, or uneven
+        per = -(-n // max(1, n_gpus))  # the executor's blocks: device // ceil(n / n_gpus)
+        return [list(range(g * per, min(n, (g + 1) * per))) for g in range(n_gpus)]
+    contiguous = [list(range(g * (n // n_gpus), (g + 1) * (n // n_gpus))) for g in range(n_gpus)]
     size = n // n_gpus
 
     def partitions(rest):
