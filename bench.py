@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Benchmark: Llama-3-8B full training state resharded TP8 -> DP2xTP4 + ZeRO-1
-(BASELINE.json metric / configs[1]) on N B200s, 8 virtual ranks in contiguous blocks.
+(BASELINE.json metric / configs[1]) on N B200s: 8 devices, grouped onto the GPUs by traffic when N < 8 (--placement).
 
 A step is ONE forward transition TP8 -> DP2xTP4 (the metric's), timed with CUDA events
 on the launching stream; the way back DP2xTP4 -> TP8 runs between steps (untimed for
